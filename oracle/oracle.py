@@ -1,0 +1,575 @@
+"""ctypes view of the CPU oracle (liboracle.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, by ``__graft_entry__.smoke()`` (as
+the checker) and by bench.py's CPU-baseline / ``--impl reference`` legs. The
+product package ``paper_2201_05989_b200`` never imports this module.
+
+The functions below restate the reference's hot path (see nf_oracle.hpp for
+the file:line citations) on numpy arrays laid out exactly like the reference's
+Eigen column-major matrices: X is (B, d) C-order == d x B column-major, Y is
+(B, L*F), MLP weights are (in, out) C-order == out x in column-major.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_BUILD = os.path.join(_HERE, "_build")
+
+_f32p = np.ctypeslib.ndpointer(dtype=np.float32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
+_vp = C.c_void_p
+
+
+def build(native: bool = False) -> str:
+    """Compile the oracle with its Makefile; returns the .so path."""
+    target = "native" if native else "all"
+    name = "liboracle_native.so" if native else "liboracle.so"
+    subprocess.run(["make", "-s", "-C", _HERE, target], check=True)
+    return os.path.join(_BUILD, name)
+
+
+_LIBS = {}
+
+
+def lib(native: bool = False) -> C.CDLL:
+    key = bool(native)
+    if key in _LIBS:
+        return _LIBS[key]
+    name = "liboracle_native.so" if native else "liboracle.so"
+    path = os.path.join(_BUILD, name)
+    if not os.path.exists(path):
+        build(native)
+    L = C.CDLL(path)
+    _declare(L)
+    _LIBS[key] = L
+    return L
+
+
+def _declare(L: C.CDLL) -> None:
+    def d(name, res, *args):
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = list(args)
+
+    d("orc_last_error", C.c_char_p)
+    d("orc_set_threads", None, C.c_int)
+    d("orc_max_threads", C.c_int)
+    d("orc_growth_factor", C.c_double, _i32p)
+    d("orc_levels", C.c_int64, _i32p, _u32p, _u32p, _i32p, _u64p)
+    d("orc_hash", C.c_uint32, _u32p, C.c_int, C.c_uint32)
+    d("orc_vertex_index", C.c_uint32, C.c_uint32, C.c_int, _u32p, C.c_int, C.c_uint32)
+    d("orc_smoothstep_d", C.c_double, C.c_double)
+    d("orc_weights_d", None, _f64p, C.c_int, C.c_int, _f64p)
+    d("orc_weights_f", None, _f32p, C.c_int, C.c_int, _f32p)
+    d("orc_voxel_f", None, C.c_float, C.c_uint32, C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_float))
+    for sfx, fp in (("f", _f32p), ("d", _f64p)):
+        d(f"orc_encode_fwd_{sfx}", C.c_int, _i32p, fp, fp, C.c_int64, fp, _vp, _vp)
+        d(f"orc_encode_bwd_{sfx}", C.c_int, _i32p, _u32p, fp, C.c_int64, fp, fp)
+        d(f"orc_glorot_{sfx}", C.c_int, _i32p, C.c_uint64, fp, fp)
+        d(f"orc_mlp_{sfx}", C.c_int, _i32p, fp, fp, fp, C.c_int64, fp, _vp, _vp, _vp, _vp)
+        d(f"orc_loss_{sfx}", C.c_float if sfx == "f" else C.c_double, C.c_int, fp, fp, C.c_int64, fp)
+    d("orc_init_tables_f", None, C.c_uint64, C.c_float, _f32p, C.c_uint64)
+    d("orc_init_tables_d", None, C.c_uint64, C.c_double, _f64p, C.c_uint64)
+    d("orc_psnr_f", C.c_double, _f32p, _f32p, C.c_int64)
+    d("orc_adam_f", C.c_int, C.POINTER(C.c_uint64), C.c_int, _i32p, _vp, _vp, _vp, _vp, _u64p, _vp,
+      _f64p, C.c_float)
+    d("orc_adam_d", C.c_int, C.POINTER(C.c_uint64), C.c_int, _i32p, _vp, _vp, _vp, _vp, _u64p, _vp,
+      _f64p, C.c_double)
+    d("orc_lr_at", C.c_double, _i64p, C.c_int, C.c_double, C.c_double, C.c_int64)
+    d("orc_default_milestones", C.c_int, C.c_int64, _i64p, C.c_int)
+    d("orc_field_create", _vp, _i32p, _i32p, _f64p)
+    d("orc_field_destroy", None, _vp)
+    d("orc_field_init", None, _vp, C.c_uint64)
+    d("orc_field_set_schedule", None, _vp, _i64p, C.c_int, C.c_double)
+    d("orc_field_buffer", C.POINTER(C.c_float), _vp, C.c_int, C.POINTER(C.c_uint64))
+    d("orc_field_sizes", None, _vp, _u64p)
+    d("orc_field_step", C.c_uint64, _vp)
+    d("orc_field_set_step", None, _vp, C.c_uint64)
+    d("orc_field_train_step", C.c_int, _vp, _f32p, _f32p, C.c_int64, C.c_int, C.c_int64,
+      C.POINTER(C.c_float), _vp)
+    d("orc_field_evaluate", C.c_int, _vp, _f32p, C.c_int64, _f32p)
+    d("orc_field_times", None, _vp, _f64p)
+    d("orc_field_reset_times", None, _vp)
+    d("orc_rng_create", _vp, C.c_uint64, C.c_uint64)
+    d("orc_rng_destroy", None, _vp)
+    d("orc_rng_u32", C.c_uint32, _vp)
+    d("orc_rng_below", C.c_uint32, _vp, C.c_uint32)
+    d("orc_rng_f32", C.c_float, _vp)
+    d("orc_rng_f64", C.c_double, _vp)
+    d("orc_rng_fill_f32", None, _vp, _f32p, C.c_int64)
+    d("orc_rng_fill_f64", None, _vp, _f64p, C.c_int64)
+    d("orc_rng_fill_u32", None, _vp, _u32p, C.c_int64)
+    d("orc_image_batch", None, _vp, _f32p, C.c_int, C.c_int, C.c_int64, _f32p, _f32p)
+    d("orc_make_test_image", None, C.c_int, C.c_int, _f32p)
+    d("orc_csg_sdf", None, _f32p, C.c_int64, _f32p)
+
+
+class OracleError(Exception):
+    pass
+
+
+class OracleInvalidArgument(OracleError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class OracleRuntimeError(OracleError, RuntimeError):
+    """std::runtime_error in the reference."""
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib().orc_last_error().decode()
+    if status == 1:
+        raise OracleInvalidArgument(msg)
+    if status == 2:
+        raise OracleRuntimeError(msg)
+    raise OracleError(msg)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# --------------------------------------------------------------------------
+# Config mirrors (reference grid.hpp:25-57, mlp.hpp:15-40, adam.hpp:13-25)
+# --------------------------------------------------------------------------
+@dataclass
+class GridCfg:
+    levels: int = 16
+    table_size: int = 1 << 14
+    features: int = 2
+    n_min: int = 16
+    n_max: int = 512
+    dims: int = 3
+    smoothstep: bool = False
+
+    def arr(self) -> np.ndarray:
+        return np.array([self.levels, self.table_size, self.features, self.n_min, self.n_max,
+                         self.dims, int(self.smoothstep)], dtype=np.int32)
+
+    @property
+    def output_width(self) -> int:
+        return self.levels * self.features
+
+
+@dataclass
+class MlpCfg:
+    input_width: int = 32
+    hidden_layers: int = 2
+    hidden_width: int = 64
+    output_width: int = 3
+    sigmoid: bool = False
+
+    def arr(self) -> np.ndarray:
+        return np.array([self.input_width, self.hidden_layers, self.hidden_width,
+                         self.output_width, int(self.sigmoid)], dtype=np.int32)
+
+    def layer_shapes(self) -> List[tuple]:
+        shapes, fan_in = [], self.input_width
+        for k in range(self.hidden_layers + 1):
+            out = self.hidden_width if k < self.hidden_layers else self.output_width
+            shapes.append((fan_in, out))
+            fan_in = out
+        return shapes
+
+    @property
+    def weight_count(self) -> int:
+        return sum(i * o for i, o in self.layer_shapes())
+
+    @property
+    def bias_count(self) -> int:
+        return sum(o for _, o in self.layer_shapes())
+
+
+@dataclass
+class Hyper:
+    lr: float = 1e-2
+    beta1: float = 0.9
+    beta2: float = 0.99
+    eps: float = 1e-15
+    l2: float = 1e-6
+
+    def arr(self) -> np.ndarray:
+        return np.array([self.lr, self.beta1, self.beta2, self.eps, self.l2], dtype=np.float64)
+
+
+LOSS_L2, LOSS_MAPE, LOSS_REL_L2 = 0, 1, 2
+
+
+# --------------------------------------------------------------------------
+# Grid
+# --------------------------------------------------------------------------
+@dataclass
+class LevelSpec:
+    level: int
+    resolution: int
+    table_len: int
+    dense: bool
+    row_offset: int
+
+
+def growth_factor(cfg: GridCfg) -> float:
+    return lib().orc_growth_factor(cfg.arr())
+
+
+def level_resolutions(cfg: GridCfg) -> List[LevelSpec]:
+    L = max(cfg.levels, 1)
+    res = np.zeros(L, np.uint32)
+    ln = np.zeros(L, np.uint32)
+    dn = np.zeros(L, np.int32)
+    off = np.zeros(L, np.uint64)
+    total = lib().orc_levels(cfg.arr(), res, ln, dn, off)
+    if total < 0:
+        raise OracleInvalidArgument(lib().orc_last_error().decode())
+    return [LevelSpec(l, int(res[l]), int(ln[l]), bool(dn[l]), int(off[l])) for l in range(cfg.levels)]
+
+
+def table_param_count(cfg: GridCfg) -> int:
+    return sum(s.table_len for s in level_resolutions(cfg)) * cfg.features
+
+
+def spatial_hash(coords: Sequence[int], dims: int, T: int) -> int:
+    c = np.zeros(3, np.uint32)
+    c[: len(coords)] = np.asarray(coords, dtype=np.uint64).astype(np.uint32)
+    return int(lib().orc_hash(c, dims, T))
+
+
+def grid_vertex_index(resolution: int, dense: bool, coords: Sequence[int], dims: int, T: int) -> int:
+    c = np.zeros(3, np.uint32)
+    c[: len(coords)] = np.asarray(coords, dtype=np.uint64).astype(np.uint32)
+    return int(lib().orc_vertex_index(resolution, int(dense), c, dims, T))
+
+
+def smoothstep(x: float) -> float:
+    return lib().orc_smoothstep_d(x)
+
+
+def interpolation_weights(frac, dims: int, smooth: bool, dtype=np.float64) -> np.ndarray:
+    f = np.zeros(3, dtype)
+    f[:dims] = frac
+    w = np.zeros(8, dtype)
+    (lib().orc_weights_d if dtype == np.float64 else lib().orc_weights_f)(f, dims, int(smooth), w)
+    return w[: 1 << dims]
+
+
+def voxel_of(x: float, resolution: int, half: bool):
+    corner = C.c_uint32()
+    frac = C.c_float()
+    lib().orc_voxel_f(float(x), resolution, int(half), C.byref(corner), C.byref(frac))
+    return corner.value, frac.value
+
+
+def init_tables(cfg: GridCfg, seed: int, magnitude: float = 1e-4, dtype=np.float32) -> np.ndarray:
+    n = table_param_count(cfg)
+    p = np.zeros(n, dtype)
+    if dtype == np.float32:
+        lib().orc_init_tables_f(seed, magnitude, p, n)
+    else:
+        lib().orc_init_tables_d(seed, magnitude, p, n)
+    return p
+
+
+@dataclass
+class EncodeCache:
+    rows: np.ndarray      # (L, B, 2^d) uint32
+    weights: np.ndarray   # (L, B, 2^d)
+
+
+def encode_forward(cfg: GridCfg, params: np.ndarray, X: np.ndarray, want_cache: bool = True):
+    dt = params.dtype
+    X = np.ascontiguousarray(X, dtype=dt)
+    if X.ndim != 2 or X.shape[1] != cfg.dims:
+        raise OracleInvalidArgument("encode_forward: input dimensionality mismatch")
+    B = X.shape[0]
+    Y = np.zeros((B, cfg.output_width), dt)
+    nc = 1 << cfg.dims
+    rows = np.zeros((cfg.levels, B, nc), np.uint32) if want_cache else None
+    wts = np.zeros((cfg.levels, B, nc), dt) if want_cache else None
+    fn = lib().orc_encode_fwd_f if dt == np.float32 else lib().orc_encode_fwd_d
+    _check(fn(cfg.arr(), np.ascontiguousarray(params), X, B, Y, _ptr(rows), _ptr(wts)))
+    return Y, (EncodeCache(rows, wts) if want_cache else None)
+
+
+def encode_backward(cfg: GridCfg, cache: EncodeCache, dY: np.ndarray, grads: np.ndarray) -> None:
+    dt = grads.dtype
+    dY = np.ascontiguousarray(dY, dtype=dt)
+    B = dY.shape[0]
+    if dY.shape[1] != cfg.output_width or cache.rows.shape[1] != B:
+        raise OracleInvalidArgument("encode_backward: gradient shape does not match cache")
+    fn = lib().orc_encode_bwd_f if dt == np.float32 else lib().orc_encode_bwd_d
+    _check(fn(cfg.arr(), cache.rows, np.ascontiguousarray(cache.weights, dtype=dt), B, dY, grads))
+
+
+# --------------------------------------------------------------------------
+# MLP
+# --------------------------------------------------------------------------
+def glorot_init(cfg: MlpCfg, seed: int, dtype=np.float32):
+    W = np.zeros(cfg.weight_count, dtype)
+    b = np.zeros(cfg.bias_count, dtype)
+    fn = lib().orc_glorot_f if dtype == np.float32 else lib().orc_glorot_d
+    _check(fn(cfg.arr(), seed, W, b))
+    return W, b
+
+
+def split_weights(cfg: MlpCfg, W: np.ndarray) -> List[np.ndarray]:
+    """Flat weight block -> list of (out, in) matrices (the reference's MatX)."""
+    mats, off = [], 0
+    for fin, fout in cfg.layer_shapes():
+        mats.append(W[off: off + fin * fout].reshape(fin, fout).T)
+        off += fin * fout
+    return mats
+
+
+def mlp_forward(cfg: MlpCfg, W, b, Y):
+    dt = W.dtype
+    Y = np.ascontiguousarray(Y, dtype=dt)
+    if Y.shape[1] != cfg.input_width:
+        raise OracleInvalidArgument("mlp_forward: input width mismatch")
+    B = Y.shape[0]
+    out = np.zeros((B, cfg.output_width), dt)
+    fn = lib().orc_mlp_f if dt == np.float32 else lib().orc_mlp_d
+    _check(fn(cfg.arr(), W, b, Y, B, out, None, None, None, None))
+    return out
+
+
+def mlp_forward_backward(cfg: MlpCfg, W, b, Y, dOut, gW=None, gb=None):
+    """Forward then mlp_backward (grads ACCUMULATE into gW/gb, mlp.hpp:147-148)."""
+    dt = W.dtype
+    Y = np.ascontiguousarray(Y, dtype=dt)
+    dOut = np.ascontiguousarray(dOut, dtype=dt)
+    B = Y.shape[0]
+    out = np.zeros((B, cfg.output_width), dt)
+    gW = np.zeros_like(W) if gW is None else gW
+    gb = np.zeros_like(b) if gb is None else gb
+    dY = np.zeros((B, cfg.input_width), dt)
+    fn = lib().orc_mlp_f if dt == np.float32 else lib().orc_mlp_d
+    _check(fn(cfg.arr(), W, b, Y, B, out, _ptr(dOut), _ptr(gW), _ptr(gb), _ptr(dY)))
+    return out, gW, gb, dY
+
+
+# --------------------------------------------------------------------------
+# Losses
+# --------------------------------------------------------------------------
+def loss_with_grad(kind: int, pred: np.ndarray, target: np.ndarray):
+    if pred.shape != target.shape:
+        raise OracleInvalidArgument("loss: shape mismatch")
+    dt = pred.dtype
+    p = np.ascontiguousarray(pred)
+    t = np.ascontiguousarray(target, dtype=dt)
+    dp = np.zeros_like(p)
+    fn = lib().orc_loss_f if dt == np.float32 else lib().orc_loss_d
+    return fn(kind, p, t, p.size, dp), dp
+
+
+def psnr(a: np.ndarray, b: np.ndarray) -> float:
+    if a.shape != b.shape:
+        raise OracleInvalidArgument("psnr: shape mismatch")
+    return lib().orc_psnr_f(np.ascontiguousarray(a, np.float32), np.ascontiguousarray(b, np.float32), a.size)
+
+
+# --------------------------------------------------------------------------
+# Adam
+# --------------------------------------------------------------------------
+@dataclass
+class ParamGroup:
+    name: str
+    params: np.ndarray
+    grads: np.ndarray
+    apply_l2: bool = False
+    skip_zero_grad: bool = False
+
+
+@dataclass
+class AdamState:
+    step: int = 0
+    m: List[np.ndarray] = field(default_factory=list)
+    v: List[np.ndarray] = field(default_factory=list)
+
+    def init(self, groups: Sequence[ParamGroup]) -> None:
+        self.step = 0
+        self.m = [np.zeros_like(g.params) for g in groups]
+        self.v = [np.zeros_like(g.params) for g in groups]
+
+
+def adam_step(state: AdamState, groups: Sequence[ParamGroup], hyper: Hyper, lr_now: float) -> None:
+    ng = len(groups)
+    dt = groups[0].params.dtype
+    flags = np.array([[int(g.apply_l2), int(g.skip_zero_grad)] for g in groups], np.int32).ravel()
+    arrp = C.c_void_p * ng
+    P = arrp(*[_ptr(g.params) for g in groups])
+    G = arrp(*[_ptr(g.grads) for g in groups])
+    M = arrp(*[_ptr(m) for m in state.m])
+    V = arrp(*[_ptr(v) for v in state.v])
+    n = np.array([g.params.size for g in groups], np.uint64)
+    names_b = [g.name.encode() for g in groups]
+    names = (C.c_char_p * ng)(*names_b)
+    st = C.c_uint64(state.step)
+    fn = lib().orc_adam_f if dt == np.float32 else lib().orc_adam_d
+    status = fn(C.byref(st), ng, flags, C.cast(P, C.c_void_p), C.cast(G, C.c_void_p),
+                C.cast(M, C.c_void_p), C.cast(V, C.c_void_p), n, C.cast(names, C.c_void_p),
+                hyper.arr(), lr_now)
+    _check(status)
+    state.step = int(st.value)
+
+
+def lr_at(milestones: Sequence[int], factor: float, base_lr: float, step: int) -> float:
+    ms = np.asarray(milestones, np.int64)
+    return lib().orc_lr_at(np.ascontiguousarray(ms), len(ms), factor, base_lr, step)
+
+
+def default_milestones(total_steps: int) -> List[int]:
+    out = np.zeros(64, np.int64)
+    n = lib().orc_default_milestones(total_steps, out, 64)
+    return [int(x) for x in out[:n]]
+
+
+# --------------------------------------------------------------------------
+# Field model (FieldModel, model.hpp:21-63)
+# --------------------------------------------------------------------------
+class Field:
+    def __init__(self, grid: GridCfg, mlp: MlpCfg, hyper: Hyper = Hyper(), native: bool = False):
+        self._lib = lib(native)
+        mlp = MlpCfg(grid.output_width, mlp.hidden_layers, mlp.hidden_width, mlp.output_width, mlp.sigmoid)
+        self.grid, self.mlp, self.hyper = grid, mlp, hyper
+        self.h = self._lib.orc_field_create(grid.arr(), mlp.arr(), hyper.arr())
+        if not self.h:
+            raise OracleInvalidArgument(self._lib.orc_last_error().decode())
+        sz = np.zeros(3, np.uint64)
+        self._lib.orc_field_sizes(self.h, sz)
+        self.n_tab, self.n_w, self.n_b = (int(x) for x in sz)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.orc_field_destroy(self.h)
+            self.h = None
+
+    def init(self, seed: int) -> None:
+        self._lib.orc_field_init(self.h, seed)
+
+    def set_schedule(self, milestones: Sequence[int], factor: float = 0.33) -> None:
+        ms = np.ascontiguousarray(np.asarray(milestones, np.int64))
+        self._lib.orc_field_set_schedule(self.h, ms, len(ms), factor)
+
+    def buffer(self, which: int) -> np.ndarray:
+        n = C.c_uint64()
+        p = self._lib.orc_field_buffer(self.h, which, C.byref(n))
+        return np.ctypeslib.as_array(p, shape=(n.value,))
+
+    params = property(lambda self: self.buffer(0))
+    grads = property(lambda self: self.buffer(1))
+    m = property(lambda self: self.buffer(2))
+    v = property(lambda self: self.buffer(3))
+
+    @property
+    def step(self) -> int:
+        return int(self._lib.orc_field_step(self.h))
+
+    @step.setter
+    def step(self, s: int) -> None:
+        self._lib.orc_field_set_step(self.h, s)
+
+    def train_step(self, X, target, loss_kind: int, step: int, want_pred: bool = False):
+        X = np.ascontiguousarray(X, np.float32)
+        target = np.ascontiguousarray(target, np.float32)
+        B = X.shape[0]
+        loss = C.c_float()
+        pred = np.zeros((B, self.mlp.output_width), np.float32) if want_pred else None
+        status = self._lib.orc_field_train_step(self.h, X, target, B, loss_kind, step, C.byref(loss), _ptr(pred))
+        if status:
+            msg = self._lib.orc_last_error().decode()
+            raise (OracleInvalidArgument if status == 1 else OracleRuntimeError)(msg)
+        return (loss.value, pred) if want_pred else loss.value
+
+    def evaluate(self, X) -> np.ndarray:
+        X = np.ascontiguousarray(X, np.float32)
+        out = np.zeros((X.shape[0], self.mlp.output_width), np.float32)
+        status = self._lib.orc_field_evaluate(self.h, X, X.shape[0], out)
+        if status:
+            raise OracleInvalidArgument(self._lib.orc_last_error().decode())
+        return out
+
+    def phase_times(self) -> dict:
+        t = np.zeros(6, np.float64)
+        self._lib.orc_field_times(self.h, t)
+        keys = ("encode_fwd", "mlp_fwd", "loss", "mlp_bwd", "encode_bwd", "adam")
+        return dict(zip(keys, (float(x) for x in t)))
+
+    def reset_times(self) -> None:
+        self._lib.orc_field_reset_times(self.h)
+
+
+# --------------------------------------------------------------------------
+# RNG and fixtures
+# --------------------------------------------------------------------------
+class Pcg32:
+    def __init__(self, seed: int, seq: int = 1):
+        self._lib = lib()
+        self.h = self._lib.orc_rng_create(seed, seq)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.orc_rng_destroy(self.h)
+            self.h = None
+
+    def next_u32(self) -> int:
+        return int(self._lib.orc_rng_u32(self.h))
+
+    def next_below(self, bound: int) -> int:
+        return int(self._lib.orc_rng_below(self.h, bound))
+
+    def next_float(self) -> float:
+        return float(self._lib.orc_rng_f32(self.h))
+
+    def next_double(self) -> float:
+        return float(self._lib.orc_rng_f64(self.h))
+
+    def floats(self, n: int) -> np.ndarray:
+        out = np.zeros(n, np.float32)
+        self._lib.orc_rng_fill_f32(self.h, out, n)
+        return out
+
+    def doubles(self, n: int) -> np.ndarray:
+        out = np.zeros(n, np.float64)
+        self._lib.orc_rng_fill_f64(self.h, out, n)
+        return out
+
+    def u32s(self, n: int) -> np.ndarray:
+        out = np.zeros(n, np.uint32)
+        self._lib.orc_rng_fill_u32(self.h, out, n)
+        return out
+
+    def image_batch(self, rgb: np.ndarray, w: int, h: int, B: int):
+        X = np.zeros((B, 2), np.float32)
+        t = np.zeros((B, 3), np.float32)
+        self._lib.orc_image_batch(self.h, np.ascontiguousarray(rgb, np.float32), w, h, B, X, t)
+        return X, t
+
+
+def make_test_image(w: int, h: int) -> np.ndarray:
+    """(w*h, 3) float32, pixel i = y*w + x (reference tests/helpers.hpp:99-125)."""
+    rgb = np.zeros((w * h, 3), np.float32)
+    lib().orc_make_test_image(w, h, rgb)
+    return rgb
+
+
+def csg_sdf(X: np.ndarray) -> np.ndarray:
+    X = np.ascontiguousarray(X, np.float32)
+    out = np.zeros(X.shape[0], np.float32)
+    lib().orc_csg_sdf(X, X.shape[0], out)
+    return out
+
+
+def set_threads(n: int) -> None:
+    lib().orc_set_threads(n)
