@@ -1,0 +1,201 @@
+/* nfg.h — C ABI of the B200 (sm_100a) hash-grid encoding + fused MLP + Adam path.
+ *
+ * This is the drop-in boundary for the reference's C++ hot-path API
+ * (/root/reference/proj/include/nf/{grid,mlp,adam,losses,model}.hpp). Every
+ * entry point names the reference interface it replaces. Plain C types only:
+ * no torch, no Eigen, no C++ in the signatures. The C++ shim in include/nf/
+ * and the Python package paper_2201_05989_b200 sit on top of this.
+ *
+ * Layouts are the reference's Eigen column-major layouts:
+ *   X       d x B            X[s*d + i]
+ *   Y, dY   (L*F) x B        Y[s*L*F + l*F + f]
+ *   out     n_out x B        out[s*n_out + o]
+ *   params  one flat fp32 vector in param-group order (model.cpp:117-143):
+ *           [tables: level 0 rows .. level L-1 rows, F floats per row]
+ *           [MLP weights: W_0 .. W_n, each out x in column-major]
+ *           [MLP biases: b_0 .. b_n]
+ *   grads, Adam m and v use the same flat layout.
+ *
+ * Errors: every call returns an nfg_status; nfg_last_error() (thread-local)
+ * holds the message. The reference's std::invalid_argument maps to
+ * NFG_EINVAL, std::runtime_error (non-finite gradient, adam.hpp:86-90) to
+ * NFG_ENONFINITE, std::logic_error to NFG_ELOGIC.
+ *
+ * Host-pointer calls are synchronous (reference semantics). *_device calls take
+ * device pointers and are asynchronous on the context's stream.
+ */
+#ifndef NFG_H
+#define NFG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NFG_ABI_VERSION 1
+
+typedef enum {
+    NFG_OK = 0,
+    NFG_EINVAL = 1,        /* std::invalid_argument */
+    NFG_ENONFINITE = 2,    /* std::runtime_error from adam_step / non-finite loss */
+    NFG_EUNSUPPORTED = 3,  /* valid for the reference, not built for sm_100a (e.g. hidden_width != 64) */
+    NFG_ECUDA = 4,
+    NFG_ENCCL = 5,
+    NFG_ELOGIC = 6
+} nfg_status;
+
+typedef enum { NFG_INTERP_LINEAR = 0, NFG_INTERP_SMOOTHSTEP = 1 } nfg_interpolation; /* grid.hpp:20 */
+typedef enum { NFG_ACT_LINEAR = 0, NFG_ACT_SIGMOID = 1 } nfg_output_activation;     /* mlp.hpp:13 */
+typedef enum { NFG_LOSS_L2 = 0, NFG_LOSS_MAPE = 1, NFG_LOSS_RELATIVE_L2 = 2 } nfg_loss_kind; /* model.hpp:17 */
+typedef enum { NFG_BUF_PARAMS = 0, NFG_BUF_GRADS = 1, NFG_BUF_ADAM_M = 2, NFG_BUF_ADAM_V = 3 } nfg_buffer;
+
+/* HashEncodingConfig, grid.hpp:25-57. */
+typedef struct {
+    int32_t levels;
+    uint32_t table_size;
+    int32_t features;
+    int32_t n_min;
+    int32_t n_max;
+    int32_t dims;
+    int32_t interpolation; /* nfg_interpolation */
+} nfg_grid_config;
+
+/* GridLevelSpec, grid.hpp:59-64, plus the level's first row in the flat table. */
+typedef struct {
+    int32_t level;
+    uint32_t resolution;
+    uint32_t table_len;
+    int32_t dense;
+    uint64_t row_offset;
+} nfg_level_spec;
+
+/* MlpConfig, mlp.hpp:15-40. input_width is overwritten with levels*features
+ * by nfg_field_create (model.cpp:101). */
+typedef struct {
+    int32_t input_width;
+    int32_t hidden_layers;
+    int32_t hidden_width;
+    int32_t output_width;
+    int32_t output_activation; /* nfg_output_activation */
+} nfg_mlp_config;
+
+/* AdamHyper, adam.hpp:13-25. */
+typedef struct {
+    double lr;
+    double beta1;
+    double beta2;
+    double eps;
+    double l2;
+} nfg_adam_hyper;
+
+/* Build options of the sm_100a path (no reference equivalent). */
+typedef struct {
+    int32_t table_fp32;    /* 1: gather fp32 master tables (exact-parity mode); 0: fp16 shadow (default) */
+    int32_t fused_train;   /* 1: one fused encode+MLP+loss+backward kernel per step (default); 0: staged kernels */
+} nfg_options;
+
+typedef struct nfg_ctx nfg_ctx;
+typedef struct nfg_field nfg_field;
+
+/* ---- context ---------------------------------------------------------- */
+const char* nfg_last_error(void);
+int nfg_abi_version(void);
+nfg_status nfg_ctx_create(int device, nfg_ctx** out);
+nfg_status nfg_ctx_destroy(nfg_ctx* ctx);
+nfg_status nfg_ctx_synchronize(nfg_ctx* ctx);
+void* nfg_ctx_stream(nfg_ctx* ctx); /* cudaStream_t */
+/* Number of kernels this library has launched on ctx (for the bench's gpu_launches). */
+uint64_t nfg_ctx_launch_count(nfg_ctx* ctx);
+
+/* Device-side phase timing with CUDA events on the context stream (off by
+ * default). read_profile returns the summed milliseconds since the last read:
+ * ms[0] fused train kernel (or staged encode+MLP+encode-bwd), ms[1] Adam,
+ * ms[2] gradient all-reduce, ms[3] inference kernel; *steps = train steps. */
+nfg_status nfg_ctx_set_profiling(nfg_ctx* ctx, int on);
+nfg_status nfg_ctx_read_profile(nfg_ctx* ctx, double ms[4], int64_t* steps);
+
+/* Multi-GPU data parallelism (one process per GPU). id is an opaque 128-byte
+ * ncclUniqueId produced on rank 0 and broadcast by the caller. With a comm
+ * attached, train steps all-reduce the gradient slab before Adam. */
+nfg_status nfg_comm_unique_id(uint8_t id[128]);
+nfg_status nfg_ctx_attach_comm(nfg_ctx* ctx, const uint8_t id[128], int rank, int nranks);
+
+/* ---- level table (grid.hpp:66-84), host only ---------------------------- */
+/* Writes min(cap, levels) specs; returns the level count or -1 on error. */
+int32_t nfg_level_resolutions(const nfg_grid_config* cfg, nfg_level_spec* out, int32_t cap);
+double nfg_growth_factor(const nfg_grid_config* cfg);            /* grid.hpp:49-54 */
+uint32_t nfg_spatial_hash(const uint32_t* coords, int32_t dims, uint32_t table_size); /* grid.hpp:88-95 */
+
+/* ---- FieldModel (model.hpp:21-63) -------------------------------------- */
+/* hyper and opts may be NULL (reference defaults / library defaults). */
+nfg_status nfg_field_create(nfg_ctx* ctx, const nfg_grid_config* grid, const nfg_mlp_config* mlp,
+                            const nfg_adam_hyper* hyper, const nfg_options* opts, nfg_field** out);
+nfg_status nfg_field_destroy(nfg_field* f);
+/* FieldModel::init (model.cpp:23-37): PCG32 table init, Glorot MLP, zero grads/moments. */
+nfg_status nfg_field_init(nfg_field* f, uint64_t seed);
+nfg_status nfg_field_set_hyper(nfg_field* f, const nfg_adam_hyper* hyper);
+/* LrSchedule (adam.hpp:124-137). */
+nfg_status nfg_field_set_schedule(nfg_field* f, const int64_t* milestones, int32_t n, double factor);
+/* {table params, MLP weights, MLP biases} counts. */
+nfg_status nfg_field_sizes(const nfg_field* f, uint64_t out[3]);
+nfg_status nfg_field_levels(const nfg_field* f, nfg_level_spec* out, int32_t cap);
+/* Host mirrors of the public members (tables.values, mlp, adam state). */
+nfg_status nfg_field_read(nfg_field* f, int32_t which, uint64_t offset, uint64_t count, float* host);
+nfg_status nfg_field_write(nfg_field* f, int32_t which, uint64_t offset, uint64_t count, const float* host);
+nfg_status nfg_field_device_buffer(nfg_field* f, int32_t which, float** dev, uint64_t* count);
+/* AdamState::step (adam.hpp:56-73). */
+nfg_status nfg_field_get_step(const nfg_field* f, uint64_t* step);
+nfg_status nfg_field_set_step(nfg_field* f, uint64_t step);
+
+/* FieldModel::train_step (model.cpp:111-138): encode -> MLP -> loss ->
+ * backward -> Adam at lr_at(schedule, lr, step). Host pointers; returns the
+ * batch loss. X is dims x B, target n_out x B. */
+nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* target, int64_t B,
+                                int32_t loss_kind, int64_t step, float* loss);
+/* Same on device pointers, asynchronous. B_global is the global batch across
+ * data-parallel ranks (loss normalisation, losses.hpp:16). loss_dev (device
+ * float, may be NULL) receives the global-batch loss of this rank's shard. */
+nfg_status nfg_field_train_step_device(nfg_field* f, const float* X, const float* target,
+                                       int64_t B_local, int64_t B_global, int32_t loss_kind,
+                                       int64_t step, float* loss_dev);
+/* Non-finite check of the last device step (synchronises). */
+nfg_status nfg_field_check(nfg_field* f);
+
+/* FieldModel::evaluate (model.cpp:102-109): fused encode + MLP inference. */
+nfg_status nfg_field_evaluate(nfg_field* f, const float* X, int64_t B, float* out);
+nfg_status nfg_field_evaluate_device(nfg_field* f, const float* X, int64_t B, float* out);
+
+/* ---- components on the field's tables / MLP (host pointers) ------------- */
+/* encode_forward (grid.hpp:219-272). rows (u32) and weights (f32), shaped
+ * (L, B, 2^d) like EncodeCache (grid.hpp:183-195), are exported when non-NULL. */
+nfg_status nfg_encode_forward(nfg_field* f, const float* X, int64_t B, float* Y, uint32_t* rows,
+                              float* weights);
+/* encode_backward (grid.hpp:277-295): accumulates dLoss/dTables into the
+ * field's table grads. The GPU cache is the input X itself (rows and weights
+ * are recomputed, never materialised). */
+nfg_status nfg_encode_backward(nfg_field* f, const float* X, int64_t B, const float* dY);
+/* mlp_forward (mlp.hpp:104-124) with the field's MLP. Y is input_width x B. */
+nfg_status nfg_mlp_forward(nfg_field* f, const float* Y, int64_t B, float* out);
+/* mlp_backward (mlp.hpp:129-158): recomputes the forward for Y, accumulates
+ * into the field's MLP grads and writes dY. */
+nfg_status nfg_mlp_backward(nfg_field* f, const float* Y, int64_t B, const float* dOut, float* dY);
+/* l2_loss / mape_loss / relative_l2_loss (losses.hpp:10-59): n values,
+ * gradient normalised by count (= n for the reference). */
+nfg_status nfg_loss(nfg_ctx* ctx, int32_t loss_kind, const float* pred, const float* target,
+                    int64_t n, int64_t count, float* dpred, float* loss);
+/* adam_step over the field's three groups (model.cpp:49-77 + adam.hpp:78-122). */
+nfg_status nfg_adam_step(nfg_field* f, float lr_now);
+/* lr_at (adam.hpp:139-146). */
+double nfg_lr_at(const int64_t* milestones, int32_t n, double factor, double base_lr, int64_t step);
+
+/* ---- pinned host memory for zero-copy-staged inputs -------------------- */
+nfg_status nfg_host_alloc(size_t bytes, void** out);
+nfg_status nfg_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NFG_H */

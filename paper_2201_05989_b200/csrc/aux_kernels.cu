@@ -1,0 +1,301 @@
+// aux_kernels.cu — standalone encode fwd/bwd (component API), Adam, loss.
+#include "encode.cuh"
+#include "kernels.h"
+
+namespace nfg {
+
+// ---- encode_forward (grid.hpp:219-272): one thread per sample, all levels ----
+template <int D, int F, typename TT>
+__global__ void __launch_bounds__(256)
+k_encode_fwd(const FieldShape s, const LevelDev* __restrict__ levels, const float* __restrict__ X, int64_t B,
+             const TT* __restrict__ table, float* __restrict__ Y, uint32_t* __restrict__ rows,
+             float* __restrict__ wts)
+{
+    __shared__ LevelDev lvs[NFG_MAX_LEVELS];
+    for (int i = threadIdx.x; i < s.grid.L; i += blockDim.x)
+        lvs[i] = levels[i];
+    __syncthreads();
+    const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= B)
+        return;
+    float x[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        x[i] = X[p * D + i];
+    const int LF = s.grid.L * F;
+    constexpr int NC = 1 << D;
+    for (int l = 0; l < s.grid.L; ++l) {
+        const LevelDev lv = lvs[l];
+        const CornerSet<D> cs = corners_of<D>(s.grid, lv, x);
+        float acc[F];
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+            acc[f] = 0.0f;
+        const TT* base = table + size_t(lv.row_off) * F;
+        const size_t co = (size_t(l) * size_t(B) + size_t(p)) * NC;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const uint32_t r = cs.row(c);
+            const float w = cs.weight(c);
+            if (rows) {
+                rows[co + c] = r;
+                wts[co + c] = w;
+            }
+#pragma unroll
+            for (int f = 0; f < F; ++f)
+                acc[f] = fmaf(w, Gather<TT>::one(base + size_t(r) * F + f), acc[f]);
+        }
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+            Y[p * LF + l * F + f] = acc[f];
+    }
+}
+
+// ---- encode_backward (grid.hpp:277-295): recompute corners, scatter --------
+template <int D, int F>
+__global__ void __launch_bounds__(256)
+k_encode_bwd(const FieldShape s, const LevelDev* __restrict__ levels, const float* __restrict__ X, int64_t B,
+             const float* __restrict__ dY, float* __restrict__ grads)
+{
+    __shared__ LevelDev lvs[NFG_MAX_LEVELS];
+    for (int i = threadIdx.x; i < s.grid.L; i += blockDim.x)
+        lvs[i] = levels[i];
+    __syncthreads();
+    const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= B)
+        return;
+    float x[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        x[i] = X[p * D + i];
+    const int LF = s.grid.L * F;
+    for (int l = 0; l < s.grid.L; ++l) {
+        const LevelDev lv = lvs[l];
+        const CornerSet<D> cs = corners_of<D>(s.grid, lv, x);
+        float* base = grads + size_t(lv.row_off) * F;
+        float dy[F];
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+            dy[f] = dY[p * LF + l * F + f];
+#pragma unroll
+        for (int c = 0; c < (1 << D); ++c) {
+            const float w = cs.weight(c);
+            float* row = base + size_t(cs.row(c)) * F;
+            if (F % 2 == 0) {
+#pragma unroll
+                for (int f = 0; f < F; f += 2)
+                    red_add2(row + f, w * dy[f], w * dy[f + 1]);
+            } else {
+#pragma unroll
+                for (int f = 0; f < F; ++f)
+                    atomicAdd(row + f, w * dy[f]);
+            }
+        }
+    }
+}
+
+template <int D, int F, typename TT>
+static cudaError_t enc_fwd(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B, const void* table,
+                           float* Y, uint32_t* rows, float* w, cudaStream_t st)
+{
+    const int64_t blocks = (B + 255) / 256;
+    k_encode_fwd<D, F, TT><<<unsigned(blocks), 256, 0, st>>>(s, lv, X, B, static_cast<const TT*>(table), Y, rows, w);
+    return cudaGetLastError();
+}
+
+template <int D, int F>
+static cudaError_t enc_bwd(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B, const float* dY,
+                           float* grads, cudaStream_t st)
+{
+    const int64_t blocks = (B + 255) / 256;
+    k_encode_bwd<D, F><<<unsigned(blocks), 256, 0, st>>>(s, lv, X, B, dY, grads);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_encode_fwd_lv(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
+                                 const void* table, float* Y, uint32_t* rows, float* w, cudaStream_t st)
+{
+    if (B <= 0)
+        return cudaSuccess;
+#define NFG_ENC_F(D_, F_)                                                                                   \
+    if (s.grid.d == D_ && s.grid.F == F_)                                                                    \
+        return s.table_fp32 ? enc_fwd<D_, F_, float>(s, lv, X, B, table, Y, rows, w, st)                     \
+                            : enc_fwd<D_, F_, __half>(s, lv, X, B, table, Y, rows, w, st);
+    NFG_ENC_F(2, 1) NFG_ENC_F(2, 2) NFG_ENC_F(2, 4) NFG_ENC_F(2, 8)
+    NFG_ENC_F(3, 1) NFG_ENC_F(3, 2) NFG_ENC_F(3, 4) NFG_ENC_F(3, 8)
+#undef NFG_ENC_F
+    return cudaErrorNotSupported;
+}
+
+cudaError_t launch_encode_bwd_lv(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
+                                 const float* dY, float* grads, cudaStream_t st)
+{
+    if (B <= 0)
+        return cudaSuccess;
+#define NFG_ENC_B(D_, F_)                                                                                   \
+    if (s.grid.d == D_ && s.grid.F == F_)                                                                    \
+        return enc_bwd<D_, F_>(s, lv, X, B, dY, grads, st);
+    NFG_ENC_B(2, 1) NFG_ENC_B(2, 2) NFG_ENC_B(2, 4) NFG_ENC_B(2, 8)
+    NFG_ENC_B(3, 1) NFG_ENC_B(3, 2) NFG_ENC_B(3, 4) NFG_ENC_B(3, 8)
+#undef NFG_ENC_B
+    return cudaErrorNotSupported;
+}
+
+// ---- Adam (adam.hpp:78-122) -------------------------------------------------
+// Phase 1 (only when flags[0] says a non-finite gradient is possible, or when
+// forced): exact isfinite scan; records the first bad group and aborts.
+__global__ void __launch_bounds__(256) k_adam_check(const AdamArgs a, int force)
+{
+    if (!force && a.flags[0] == 0u)
+        return;
+    const uint64_t n = a.n_tab + a.n_w + a.n_b;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        if (!finite_f(a.g[i])) {
+            const unsigned grp = i < a.n_tab ? 0u : (i < a.n_tab + a.n_w ? 1u : 2u);
+            atomicOr(&a.flags[1], 1u);
+            atomicMin(&a.flags[2], grp + 1u);
+        }
+    }
+}
+
+// Phase 2: one streaming pass, per entry exactly the reference's operation
+// order with IEEE round-to-nearest intrinsics (no contraction) so updates are
+// bit-identical to the fp32 reference. Skip-zero entries of the tables group
+// are never written; every gradient is zeroed (adam.hpp:118-120).
+__device__ __forceinline__ void adam_one(const AdamArgs& a, uint64_t i, float& p, float& g, float& m, float& v,
+                                         bool& wrote)
+{
+    const int grp = i < a.n_tab ? 0 : (i < a.n_tab + a.n_w ? 1 : 2);
+    float gg = g;
+    wrote = false;
+    if (grp == 0 && gg == 0.0f)
+        return;
+    if (grp == 1)
+        gg = __fadd_rn(gg, __fmul_rn(a.l2, p));
+    m = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(a.omb1, gg));
+    v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(__fmul_rn(a.omb2, gg), gg));
+    const float num = __fmul_rn(a.lr, __fdiv_rn(m, a.bc1));
+    const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(v, a.bc2)), a.eps);
+    p = __fsub_rn(p, __fdiv_rn(num, den));
+    wrote = true;
+}
+
+__global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
+{
+    if (a.flags[1] != 0u)
+        return;   // non-finite gradient: state untouched (the reference throws first)
+    const uint64_t n = a.n_tab + a.n_w + a.n_b;
+    const uint64_t n4 = n / 4;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride) {
+        float4 P = reinterpret_cast<const float4*>(a.p)[q];
+        const float4 G = reinterpret_cast<const float4*>(a.g)[q];
+        const bool any = G.x != 0.0f || G.y != 0.0f || G.z != 0.0f || G.w != 0.0f;
+        const uint64_t i0 = 4 * q;
+        if (!any && i0 + 3 < a.n_tab)
+            continue;   // whole quad skipped: nothing to read or write
+        float4 M = reinterpret_cast<const float4*>(a.m)[q];
+        float4 V = reinterpret_cast<const float4*>(a.v)[q];
+        float pg[4] = { P.x, P.y, P.z, P.w }, gq[4] = { G.x, G.y, G.z, G.w };
+        float mq[4] = { M.x, M.y, M.z, M.w }, vq[4] = { V.x, V.y, V.z, V.w };
+        bool w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            adam_one(a, i0 + e, pg[e], gq[e], mq[e], vq[e], w[e]);
+        reinterpret_cast<float4*>(a.p)[q] = make_float4(pg[0], pg[1], pg[2], pg[3]);
+        reinterpret_cast<float4*>(a.m)[q] = make_float4(mq[0], mq[1], mq[2], mq[3]);
+        reinterpret_cast<float4*>(a.v)[q] = make_float4(vq[0], vq[1], vq[2], vq[3]);
+        if (any)
+            reinterpret_cast<float4*>(a.g)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (a.shadow && i0 < a.n_tab) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (w[e] && i0 + e < a.n_tab)
+                    a.shadow[i0 + e] = __float2half_rn(pg[e]);
+        }
+    }
+    // tail
+    for (uint64_t i = 4 * n4 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        float p = a.p[i], g = a.g[i], m = a.m[i], v = a.v[i];
+        bool w;
+        adam_one(a, i, p, g, m, v, w);
+        if (w) {
+            a.p[i] = p;
+            a.m[i] = m;
+            a.v[i] = v;
+            if (a.shadow && i < a.n_tab)
+                a.shadow[i] = __float2half_rn(p);
+        }
+        a.g[i] = 0.0f;
+    }
+}
+
+cudaError_t launch_adam(const AdamArgs& a, bool force_check, int num_sms, cudaStream_t st)
+{
+    const uint64_t n = a.n_tab + a.n_w + a.n_b;
+    const int blocks = int(std::min<uint64_t>((n / 4 + 255) / 256 + 1, uint64_t(num_sms) * 8));
+    k_adam_check<<<num_sms * 4, 256, 0, st>>>(a, force_check ? 1 : 0);
+    k_adam<<<blocks, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+__global__ void k_shadow(const float* __restrict__ p, __half* __restrict__ s, uint64_t n)
+{
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        s[i] = __float2half_rn(p[i]);
+}
+
+cudaError_t launch_shadow(const float* p, __half* shadow, uint64_t n, cudaStream_t st)
+{
+    if (n == 0)
+        return cudaSuccess;
+    const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, 148 * 16));
+    k_shadow<<<blocks, 256, 0, st>>>(p, shadow, n);
+    return cudaGetLastError();
+}
+
+// ---- losses (losses.hpp:10-59) ------------------------------------------------
+__global__ void __launch_bounds__(256) k_loss(int kind, const float* __restrict__ pred, const float* __restrict__ target,
+                                              int64_t n, float count, float* __restrict__ dpred, double* loss_sum)
+{
+    float term = 0.0f;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const float p = pred[i], t = target[i], diff = p - t;
+        float d;
+        switch (kind) {
+        case 0:
+            term += diff * diff;
+            d = (2.0f / count) * diff;   // losses.hpp:16-17
+            break;
+        case 1: {
+            const float den = fabsf(t) + 0.01f;
+            term += fabsf(diff) / den;
+            const float sg = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
+            d = sg / den / count;   // losses.hpp:36
+            break;
+        }
+        default: {
+            const float den = __fadd_rn(__fmul_rn(p, p), 0.01f);   // no contraction (bit parity)
+            term += diff * diff / den;
+            d = 2.0f * diff / den / count;   // losses.hpp:55
+        }
+        }
+        dpred[i] = d;
+    }
+    for (int m = 16; m > 0; m >>= 1)
+        term += __shfl_xor_sync(0xffffffffu, term, m);
+    if ((threadIdx.x & 31) == 0)
+        atomicAdd(loss_sum, double(term));
+}
+
+cudaError_t launch_loss(int kind, const float* pred, const float* target, int64_t n, float count, float* dpred,
+                        double* loss_sum, cudaStream_t st)
+{
+    if (n <= 0)
+        return cudaSuccess;
+    const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 8));
+    k_loss<<<blocks, 256, 0, st>>>(kind, pred, target, n, count, dpred, loss_sum);
+    return cudaGetLastError();
+}
+
+}   // namespace nfg

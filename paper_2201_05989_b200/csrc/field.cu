@@ -1,0 +1,900 @@
+// field.cu — the C ABI (include/nfg.h): contexts, the device-resident
+// FieldModel and the component entry points. Host orchestration only; the
+// math lives in the kernels.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/nfg.h"
+#include "host_init.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    nfg_status st;
+    std::string msg;
+};
+
+#define NFG_CUDA(call)                                                                                  \
+    do {                                                                                                \
+        const cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                          \
+            throw Fail{ e_ == cudaErrorNotSupported ? NFG_EUNSUPPORTED : NFG_ECUDA,                     \
+                        std::string(#call) + ": " + cudaGetErrorString(e_) };                           \
+    } while (0)
+
+// NCCL is resolved at run time (dlopen) and only when a communicator is
+// attached: a process that imported torch first reuses torch's libnccl.so.2,
+// and single-GPU users never load NCCL at all.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+    decltype(&ncclCommDestroy) comm_destroy = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const NcclApi& nccl()
+{
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+            api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+            api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+            api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+            api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+        }
+    }
+    if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce)
+        throw Fail{ NFG_ENCCL, "libnccl.so.2 could not be loaded" };
+    return api;
+}
+
+#define NFG_NCCL(call)                                                                                  \
+    do {                                                                                                \
+        const ncclResult_t r_ = (call);                                                                 \
+        if (r_ != ncclSuccess)                                                                          \
+            throw Fail{ NFG_ENCCL, std::string(#call) + ": " + nccl().error_string(r_) };               \
+    } while (0)
+
+template <class Fn>
+nfg_status guard(Fn&& fn)
+{
+    try {
+        fn();
+        return NFG_OK;
+    } catch (const Fail& f) {
+        g_err = f.msg;
+        return f.st;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return NFG_EINVAL;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return NFG_ELOGIC;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return NFG_ECUDA;
+    }
+}
+
+void require(bool ok, const char* msg)
+{
+    if (!ok)
+        throw std::invalid_argument(msg);
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t n)
+    {
+        if (n > bytes) {
+            if (p)
+                cudaFree(p);
+            p = nullptr;
+            bytes = 0;
+            if (cudaMalloc(&p, n) != cudaSuccess)
+                throw Fail{ NFG_ECUDA, "cudaMalloc staging buffer failed" };
+            bytes = n;
+        }
+        return p;
+    }
+    ~DevBuf()
+    {
+        if (p)
+            cudaFree(p);
+    }
+};
+
+}   // namespace
+
+struct nfg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    uint64_t launches = 0;
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1;
+    DevBuf s0, s1, s2, s3;   // staging for host-pointer calls
+    double* d_red = nullptr;
+    // phase timing (nfg_ctx_set_profiling)
+    bool profile = false;
+    std::vector<cudaEvent_t> ev_pool;
+    struct Rec {
+        int kind;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    int64_t prof_steps = 0;
+
+    cudaEvent_t ev()
+    {
+        if (ev_pool.empty()) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess)
+                throw std::runtime_error("cudaEventCreate failed");
+            return e;
+        }
+        cudaEvent_t e = ev_pool.back();
+        ev_pool.pop_back();
+        return e;
+    }
+};
+
+namespace {
+// RAII span: records a start/end event pair on the ctx stream when profiling.
+struct Span {
+    nfg_ctx* c;
+    int kind;
+    cudaEvent_t a = nullptr;
+    Span(nfg_ctx* c_, int k) : c(c_), kind(k)
+    {
+        if (c->profile) {
+            a = c->ev();
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    ~Span()
+    {
+        if (a) {
+            cudaEvent_t b = c->ev();
+            cudaEventRecord(b, c->stream);
+            c->recs.push_back({ kind, a, b });
+        }
+    }
+};
+}   // namespace
+
+// Scratch block written by kernels and read back in one 32-byte copy.
+struct StepResult {
+    double loss_sum;
+    unsigned int flags[4];
+    float dy_max;
+    float pad;
+};
+
+struct nfg_field {
+    nfg_ctx* ctx = nullptr;
+    nfg_grid_config gcfg{};
+    nfg_mlp_config mcfg{};
+    nfg_adam_hyper hyper{ 1e-2, 0.9, 0.99, 1e-15, 1e-6 };
+    nfg_options opts{ 0, 1 };
+    std::vector<int64_t> milestones;
+    double factor = 0.33;
+    std::vector<nfg_level_spec> levels;
+    nfg::FieldShape shape{};
+    nfg::LevelDev* d_levels = nullptr;
+    uint64_t n_tab = 0, n_w = 0, n_b = 0, n_total = 0, n_alloc = 0;
+    float* d_p = nullptr;
+    float* d_g = nullptr;
+    float* d_m = nullptr;
+    float* d_v = nullptr;
+    __half* d_shadow = nullptr;
+    StepResult* d_res = nullptr;
+    StepResult* h_res = nullptr;   // pinned
+    uint64_t step = 0;
+    uint64_t pending_steps = 0;    // device steps not yet checked (async API)
+};
+
+namespace {
+
+nfg::StepScratch scratch_of(nfg_field* f)
+{
+    nfg::StepScratch s;
+    s.loss_sum = &f->d_res->loss_sum;
+    s.flags = f->d_res->flags;
+    s.dy_max = &f->d_res->dy_max;
+    return s;
+}
+
+void reset_scratch(nfg_field* f)
+{
+    cudaStream_t st = f->ctx->stream;
+    NFG_CUDA(cudaMemsetAsync(f->d_res, 0, sizeof(StepResult), st));
+    NFG_CUDA(cudaMemsetAsync(&f->d_res->flags[2], 0xff, sizeof(unsigned int), st));
+}
+
+const char* group_name(unsigned g)
+{
+    switch (g) {
+    case 0: return "tables";
+    case 1: return "mlp_weights";
+    default: return "mlp_biases";
+    }
+}
+
+void fetch_result(nfg_field* f)
+{
+    NFG_CUDA(cudaMemcpyAsync(f->h_res, f->d_res, sizeof(StepResult), cudaMemcpyDeviceToHost, f->ctx->stream));
+    NFG_CUDA(cudaStreamSynchronize(f->ctx->stream));
+}
+
+void raise_if_aborted(nfg_field* f)
+{
+    if (f->h_res->flags[1]) {
+        const unsigned g = f->h_res->flags[2] == 0xffffffffu ? 0u : f->h_res->flags[2] - 1u;
+        throw Fail{ NFG_ENONFINITE, std::string("adam_step: non-finite gradient in group '") + group_name(g) + "'" };
+    }
+}
+
+const void* table_ptr(nfg_field* f) { return f->opts.table_fp32 ? static_cast<const void*>(f->d_p) : f->d_shadow; }
+
+void refresh_shadow(nfg_field* f)
+{
+    NFG_CUDA(nfg::launch_shadow(f->d_p, f->d_shadow, f->n_tab, f->ctx->stream));
+    f->ctx->launches++;
+}
+
+template <class T>
+T* stage(DevBuf& b, const T* host, size_t count, cudaStream_t st)
+{
+    T* d = static_cast<T*>(b.get(std::max<size_t>(count * sizeof(T), 16)));
+    if (count)
+        NFG_CUDA(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, st));
+    return d;
+}
+
+void run_adam(nfg_field* f, float lr_now, bool force_check)
+{
+    const uint64_t next = f->step + 1;
+    const nfg::host::AdamScalars s = nfg::host::adam_scalars(f->hyper, next, lr_now);
+    nfg::AdamArgs a;
+    a.p = f->d_p;
+    a.g = f->d_g;
+    a.m = f->d_m;
+    a.v = f->d_v;
+    a.shadow = f->d_shadow;
+    a.n_tab = f->n_tab;
+    a.n_w = f->n_w;
+    a.n_b = f->n_b;
+    a.b1 = s.b1;
+    a.b2 = s.b2;
+    a.omb1 = s.omb1;
+    a.omb2 = s.omb2;
+    a.bc1 = s.bc1;
+    a.bc2 = s.bc2;
+    a.eps = s.eps;
+    a.l2 = s.l2;
+    a.lr = s.lr;
+    a.flags = f->d_res->flags;
+    NFG_CUDA(nfg::launch_adam(a, force_check, f->ctx->num_sms, f->ctx->stream));
+    f->ctx->launches += 2;
+    f->step = next;
+}
+
+void device_train_step(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
+                       int loss_kind, int64_t step)
+{
+    require(loss_kind >= 0 && loss_kind <= 2, "train_step: unknown loss");
+    require(B_local >= 0 && B_global >= B_local, "train_step: invalid batch size");
+    nfg_ctx* c = f->ctx;
+    reset_scratch(f);
+    const double count = double(B_global) * double(f->mcfg.output_width);
+    nfg::TrainArgs a{};
+    a.X = X;
+    a.target = target;
+    a.B = B_local;
+    a.loss_kind = loss_kind;
+    a.inv_count = count > 0 ? float(1.0 / count) : 0.0f;
+    a.table = table_ptr(f);
+    a.W = f->d_p + f->n_tab;
+    a.b = f->d_p + f->n_tab + f->n_w;
+    a.table_grad = f->d_g;
+    a.gW = f->d_g + f->n_tab;
+    a.gb = f->d_g + f->n_tab + f->n_w;
+    a.scratch = scratch_of(f);
+    if (c->profile)
+        c->prof_steps++;
+    if (B_local > 0) {
+        Span span(c, 0);
+        if (f->opts.fused_train) {
+            NFG_CUDA(nfg::launch_train(f->shape, f->d_levels, nfg::SRC_ENCODE, nfg::GRAD_LOSS, nfg::SINK_SCATTER, a,
+                                       c->num_sms, c->stream, nullptr));
+            c->launches++;
+        } else {
+            const size_t LF = size_t(f->shape.in_real);
+            float* Y = static_cast<float*>(c->s2.get(size_t(B_local) * LF * 4));
+            float* dY = static_cast<float*>(c->s3.get(size_t(B_local) * LF * 4));
+            NFG_CUDA(nfg::launch_encode_fwd_lv(f->shape, f->d_levels, X, B_local, table_ptr(f), Y, nullptr, nullptr,
+                                               c->stream));
+            a.Y = Y;
+            a.dY = dY;
+            NFG_CUDA(nfg::launch_train(f->shape, nullptr, nfg::SRC_LOAD_Y, nfg::GRAD_LOSS, nfg::SINK_STORE, a,
+                                       c->num_sms, c->stream, nullptr));
+            NFG_CUDA(nfg::launch_encode_bwd_lv(f->shape, f->d_levels, X, B_local, dY, f->d_g, c->stream));
+            c->launches += 3;
+        }
+    }
+    if (c->comm && c->nranks > 1) {
+        Span span(c, 2);
+        // Data-parallel exchange: sum of the shards' (globally normalised)
+        // gradients == the single-GPU gradient of the global batch; loss sums
+        // and the non-finite flag travel with it.
+        NFG_NCCL(nccl().all_reduce(f->d_g, f->d_g, f->n_total, ncclFloat32, ncclSum, c->comm, c->stream));
+        NFG_NCCL(nccl().all_reduce(&f->d_res->loss_sum, &f->d_res->loss_sum, 1, ncclFloat64, ncclSum, c->comm, c->stream));
+        NFG_NCCL(nccl().all_reduce(f->d_res->flags, f->d_res->flags, 1, ncclUint32, ncclMax, c->comm, c->stream));
+    }
+    const float lr_now = float(nfg::host::lr_at(f->milestones, f->factor, f->hyper.lr, step));
+    Span span(c, 1);
+    run_adam(f, lr_now, false);
+}
+
+nfg::FieldShape make_shape(const nfg_grid_config& g, const nfg_mlp_config& m, const std::vector<nfg_level_spec>& lv,
+                           const nfg_options& o)
+{
+    nfg::FieldShape s{};
+    s.grid.L = g.levels;
+    s.grid.F = g.features;
+    s.grid.d = g.dims;
+    s.grid.smooth = g.interpolation == NFG_INTERP_SMOOTHSTEP;
+    s.grid.mask = g.table_size - 1u;
+    s.in_real = g.levels * g.features;
+    s.in_steps = (s.in_real + 15) / 16;
+    s.hidden_layers = m.hidden_layers;
+    s.n_out = m.output_width;
+    s.sigmoid = m.output_activation == NFG_ACT_SIGMOID;
+    s.table_fp32 = o.table_fp32;
+    for (size_t l = 0; l < lv.size() && l < NFG_MAX_LEVELS; ++l) {
+        nfg::LevelDev& d = s.grid.lv[l];
+        d.res = lv[l].resolution;
+        d.res_f = float(lv[l].resolution);
+        d.stride = lv[l].resolution + 1u;
+        d.dense = uint32_t(lv[l].dense);
+        d.row_off = uint32_t(lv[l].row_offset);
+        d.len = lv[l].table_len;
+    }
+    return s;
+}
+
+float* buffer_of(nfg_field* f, int which)
+{
+    switch (which) {
+    case NFG_BUF_PARAMS: return f->d_p;
+    case NFG_BUF_GRADS: return f->d_g;
+    case NFG_BUF_ADAM_M: return f->d_m;
+    case NFG_BUF_ADAM_V: return f->d_v;
+    }
+    throw std::invalid_argument("unknown buffer");
+}
+
+}   // namespace
+
+extern "C" {
+
+const char* nfg_last_error(void) { return g_err.c_str(); }
+int nfg_abi_version(void) { return NFG_ABI_VERSION; }
+
+nfg_status nfg_ctx_create(int device, nfg_ctx** out)
+{
+    return guard([&] {
+        require(out != nullptr, "nfg_ctx_create: null out");
+        auto* c = new nfg_ctx;
+        try {
+            c->device = device;
+            NFG_CUDA(cudaSetDevice(device));
+            NFG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            NFG_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+nfg_status nfg_ctx_destroy(nfg_ctx* c)
+{
+    return guard([&] {
+        if (!c)
+            return;
+        if (c->comm)
+            nccl().comm_destroy(c->comm);
+        for (auto& r : c->recs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (auto e : c->ev_pool)
+            cudaEventDestroy(e);
+        if (c->stream)
+            cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+nfg_status nfg_ctx_synchronize(nfg_ctx* c)
+{
+    return guard([&] { NFG_CUDA(cudaStreamSynchronize(c->stream)); });
+}
+
+void* nfg_ctx_stream(nfg_ctx* c) { return c ? c->stream : nullptr; }
+uint64_t nfg_ctx_launch_count(nfg_ctx* c) { return c ? c->launches : 0; }
+
+nfg_status nfg_ctx_set_profiling(nfg_ctx* c, int on)
+{
+    return guard([&] { c->profile = on != 0; });
+}
+
+nfg_status nfg_ctx_read_profile(nfg_ctx* c, double ms[4], int64_t* steps)
+{
+    return guard([&] {
+        NFG_CUDA(cudaStreamSynchronize(c->stream));
+        for (int i = 0; i < 4; ++i)
+            ms[i] = 0.0;
+        for (const auto& r : c->recs) {
+            float t = 0.0f;
+            NFG_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+            ms[r.kind] += t;
+            c->ev_pool.push_back(r.a);
+            c->ev_pool.push_back(r.b);
+        }
+        c->recs.clear();
+        *steps = c->prof_steps;
+        c->prof_steps = 0;
+    });
+}
+
+nfg_status nfg_comm_unique_id(uint8_t id[128])
+{
+    return guard([&] {
+        ncclUniqueId u;
+        NFG_NCCL(nccl().get_unique_id(&u));
+        static_assert(sizeof(u) == 128, "ncclUniqueId size");
+        std::memcpy(id, &u, 128);
+    });
+}
+
+nfg_status nfg_ctx_attach_comm(nfg_ctx* c, const uint8_t id[128], int rank, int nranks)
+{
+    return guard([&] {
+        require(nranks >= 1 && rank >= 0 && rank < nranks, "attach_comm: bad rank");
+        ncclUniqueId u;
+        std::memcpy(&u, id, 128);
+        NFG_CUDA(cudaSetDevice(c->device));
+        NFG_NCCL(nccl().comm_init_rank(&c->comm, nranks, u, rank));
+        c->rank = rank;
+        c->nranks = nranks;
+    });
+}
+
+int32_t nfg_level_resolutions(const nfg_grid_config* cfg, nfg_level_spec* out, int32_t cap)
+{
+    int32_t n = -1;
+    const nfg_status st = guard([&] {
+        const auto lv = nfg::host::level_resolutions(*cfg);
+        for (size_t i = 0; i < lv.size() && int32_t(i) < cap; ++i)
+            out[i] = lv[i];
+        n = int32_t(lv.size());
+    });
+    return st == NFG_OK ? n : -1;
+}
+
+double nfg_growth_factor(const nfg_grid_config* cfg) { return nfg::host::growth_factor(*cfg); }
+
+uint32_t nfg_spatial_hash(const uint32_t* coords, int32_t dims, uint32_t table_size)
+{
+    return nfg::host::spatial_hash(coords, dims, table_size);
+}
+
+double nfg_lr_at(const int64_t* ms, int32_t n, double factor, double base, int64_t step)
+{
+    return nfg::host::lr_at(std::vector<int64_t>(ms, ms + n), factor, base, step);
+}
+
+nfg_status nfg_field_create(nfg_ctx* ctx, const nfg_grid_config* grid, const nfg_mlp_config* mlp,
+                            const nfg_adam_hyper* hyper, const nfg_options* opts, nfg_field** out)
+{
+    return guard([&] {
+        require(ctx && grid && mlp && out, "nfg_field_create: null argument");
+        auto* f = new nfg_field;
+        try {
+            f->ctx = ctx;
+            f->gcfg = *grid;
+            f->mcfg = *mlp;
+            f->mcfg.input_width = grid->levels * grid->features;   // model.cpp:101
+            if (hyper)
+                f->hyper = *hyper;
+            if (opts)
+                f->opts = *opts;
+            nfg::host::validate(f->gcfg);
+            nfg::host::validate(f->mcfg);
+            nfg::host::validate(f->hyper);
+            if (f->mcfg.hidden_width != 64)
+                throw Fail{ NFG_EUNSUPPORTED, "sm_100a MLP is built for hidden_width == 64 only" };
+            if (f->mcfg.hidden_layers < 1 || f->mcfg.hidden_layers > 3)
+                throw Fail{ NFG_EUNSUPPORTED, "sm_100a MLP is built for 1..3 hidden layers" };
+            if (f->mcfg.output_width > 16)
+                throw Fail{ NFG_EUNSUPPORTED, "sm_100a MLP is built for output_width <= 16" };
+            if (f->gcfg.levels > NFG_MAX_LEVELS || f->mcfg.input_width > 64)
+                throw Fail{ NFG_EUNSUPPORTED, "sm_100a encoding is built for levels <= 32 and levels*features <= 64" };
+            if (f->gcfg.features != 1 && f->gcfg.features != 2 && f->gcfg.features != 4 && f->gcfg.features != 8)
+                throw Fail{ NFG_EUNSUPPORTED, "sm_100a encoding is built for features in {1, 2, 4, 8}" };
+            f->levels = nfg::host::level_resolutions(f->gcfg);
+            const uint64_t rows = f->levels.back().row_offset + f->levels.back().table_len;
+            if (rows >= (uint64_t(1) << 32))
+                throw Fail{ NFG_EUNSUPPORTED, "table rows exceed 2^32" };
+            f->n_tab = rows * uint64_t(f->gcfg.features);
+            uint64_t nw = 0, nb = 0;
+            int in = f->mcfg.input_width;
+            for (int k = 0; k <= f->mcfg.hidden_layers; ++k) {
+                const int o = k < f->mcfg.hidden_layers ? f->mcfg.hidden_width : f->mcfg.output_width;
+                nw += uint64_t(in) * uint64_t(o);
+                nb += uint64_t(o);
+                in = o;
+            }
+            f->n_w = nw;
+            f->n_b = nb;
+            f->n_total = f->n_tab + nw + nb;
+            f->n_alloc = (f->n_total + 63) & ~uint64_t(63);
+            f->shape = make_shape(f->gcfg, f->mcfg, f->levels, f->opts);
+            NFG_CUDA(cudaSetDevice(ctx->device));
+            const size_t bytes = f->n_alloc * sizeof(float);
+            NFG_CUDA(cudaMalloc(&f->d_p, bytes));
+            NFG_CUDA(cudaMalloc(&f->d_g, bytes));
+            NFG_CUDA(cudaMalloc(&f->d_m, bytes));
+            NFG_CUDA(cudaMalloc(&f->d_v, bytes));
+            NFG_CUDA(cudaMalloc(&f->d_shadow, std::max<uint64_t>(f->n_tab, 1) * sizeof(__half)));
+            NFG_CUDA(cudaMalloc(&f->d_levels, sizeof(nfg::LevelDev) * NFG_MAX_LEVELS));
+            NFG_CUDA(cudaMalloc(&f->d_res, sizeof(StepResult)));
+            NFG_CUDA(cudaMallocHost(&f->h_res, sizeof(StepResult)));
+            NFG_CUDA(cudaMemcpy(f->d_levels, f->shape.grid.lv, sizeof(nfg::LevelDev) * NFG_MAX_LEVELS,
+                                cudaMemcpyHostToDevice));
+            for (float* p : { f->d_p, f->d_g, f->d_m, f->d_v })
+                NFG_CUDA(cudaMemsetAsync(p, 0, bytes, ctx->stream));
+            NFG_CUDA(cudaMemsetAsync(f->d_shadow, 0, std::max<uint64_t>(f->n_tab, 1) * sizeof(__half), ctx->stream));
+            NFG_CUDA(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            nfg_field_destroy(f);
+            throw;
+        }
+        *out = f;
+    });
+}
+
+nfg_status nfg_field_destroy(nfg_field* f)
+{
+    return guard([&] {
+        if (!f)
+            return;
+        for (void* p : { (void*)f->d_p, (void*)f->d_g, (void*)f->d_m, (void*)f->d_v, (void*)f->d_shadow,
+                         (void*)f->d_levels, (void*)f->d_res })
+            if (p)
+                cudaFree(p);
+        if (f->h_res)
+            cudaFreeHost(f->h_res);
+        delete f;
+    });
+}
+
+nfg_status nfg_field_init(nfg_field* f, uint64_t seed)
+{
+    return guard([&] {
+        std::vector<float> host(f->n_total);
+        nfg::host::init_tables(seed, host.data(), f->n_tab);                         // grid.hpp:158-164
+        nfg::host::glorot(f->mcfg, seed + 1, host.data() + f->n_tab, host.data() + f->n_tab + f->n_w);   // model.cpp:34
+        cudaStream_t st = f->ctx->stream;
+        NFG_CUDA(cudaMemcpyAsync(f->d_p, host.data(), f->n_total * 4, cudaMemcpyHostToDevice, st));
+        for (float* p : { f->d_g, f->d_m, f->d_v })
+            NFG_CUDA(cudaMemsetAsync(p, 0, f->n_alloc * 4, st));
+        refresh_shadow(f);
+        NFG_CUDA(cudaStreamSynchronize(st));
+        f->step = 0;
+    });
+}
+
+nfg_status nfg_field_set_hyper(nfg_field* f, const nfg_adam_hyper* h)
+{
+    return guard([&] {
+        nfg::host::validate(*h);
+        f->hyper = *h;
+    });
+}
+
+nfg_status nfg_field_set_schedule(nfg_field* f, const int64_t* ms, int32_t n, double factor)
+{
+    return guard([&] {
+        // LrSchedule::validate (adam.hpp:129-136)
+        require(factor > 0 && factor <= 1, "LrSchedule: factor must be in (0, 1]");
+        for (int32_t i = 1; i < n; ++i)
+            require(ms[i] > ms[i - 1], "LrSchedule: milestones must be strictly increasing");
+        f->milestones.assign(ms, ms + n);
+        f->factor = factor;
+    });
+}
+
+nfg_status nfg_field_sizes(const nfg_field* f, uint64_t out[3])
+{
+    return guard([&] {
+        out[0] = f->n_tab;
+        out[1] = f->n_w;
+        out[2] = f->n_b;
+    });
+}
+
+nfg_status nfg_field_levels(const nfg_field* f, nfg_level_spec* out, int32_t cap)
+{
+    return guard([&] {
+        for (size_t i = 0; i < f->levels.size() && int32_t(i) < cap; ++i)
+            out[i] = f->levels[i];
+    });
+}
+
+nfg_status nfg_field_read(nfg_field* f, int32_t which, uint64_t off, uint64_t n, float* host)
+{
+    return guard([&] {
+        require(off + n <= f->n_total, "nfg_field_read: range out of bounds");
+        NFG_CUDA(cudaMemcpyAsync(host, buffer_of(f, which) + off, n * 4, cudaMemcpyDeviceToHost, f->ctx->stream));
+        NFG_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    });
+}
+
+nfg_status nfg_field_write(nfg_field* f, int32_t which, uint64_t off, uint64_t n, const float* host)
+{
+    return guard([&] {
+        require(off + n <= f->n_total, "nfg_field_write: range out of bounds");
+        NFG_CUDA(cudaMemcpyAsync(buffer_of(f, which) + off, host, n * 4, cudaMemcpyHostToDevice, f->ctx->stream));
+        if (which == NFG_BUF_PARAMS && off < f->n_tab)
+            refresh_shadow(f);
+        NFG_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    });
+}
+
+nfg_status nfg_field_device_buffer(nfg_field* f, int32_t which, float** dev, uint64_t* count)
+{
+    return guard([&] {
+        *dev = buffer_of(f, which);
+        *count = f->n_total;
+    });
+}
+
+nfg_status nfg_field_get_step(const nfg_field* f, uint64_t* step)
+{
+    return guard([&] { *step = f->step; });
+}
+
+nfg_status nfg_field_set_step(nfg_field* f, uint64_t step)
+{
+    return guard([&] { f->step = step; });
+}
+
+nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* target, int64_t B, int32_t loss_kind,
+                                int64_t step, float* loss)
+{
+    return guard([&] {
+        nfg_ctx* c = f->ctx;
+        const int d = f->gcfg.dims, no = f->mcfg.output_width;
+        const float* dX = stage(c->s0, X, size_t(B) * d, c->stream);
+        const float* dT = stage(c->s1, target, size_t(B) * no, c->stream);
+        const uint64_t before = f->step;
+        device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step);
+        fetch_result(f);
+        if (f->h_res->flags[1]) {
+            f->step = before;   // the reference throws before incrementing (adam.hpp:86-92)
+            raise_if_aborted(f);
+        }
+        const double count = double(B) * c->nranks * no;
+        if (loss)
+            *loss = count > 0 ? float(f->h_res->loss_sum / count) : 0.0f;
+    });
+}
+
+nfg_status nfg_field_train_step_device(nfg_field* f, const float* X, const float* target, int64_t B_local,
+                                       int64_t B_global, int32_t loss_kind, int64_t step, float* loss_dev)
+{
+    return guard([&] {
+        (void)loss_dev;
+        device_train_step(f, X, target, B_local, B_global, loss_kind, step);
+        f->pending_steps++;
+    });
+}
+
+nfg_status nfg_field_check(nfg_field* f)
+{
+    return guard([&] {
+        fetch_result(f);
+        f->pending_steps = 0;
+        if (f->h_res->flags[1]) {
+            f->step -= 1;
+            raise_if_aborted(f);
+        }
+    });
+}
+
+nfg_status nfg_field_evaluate_device(nfg_field* f, const float* X, int64_t B, float* out)
+{
+    return guard([&] {
+        nfg::InferArgs a{};
+        a.X = X;
+        a.B = B;
+        a.table = table_ptr(f);
+        a.W = f->d_p + f->n_tab;
+        a.b = f->d_p + f->n_tab + f->n_w;
+        a.out = out;
+        Span span(f->ctx, 3);
+        NFG_CUDA(nfg::launch_infer(f->shape, f->d_levels, nfg::SRC_ENCODE, a, f->ctx->num_sms, f->ctx->stream));
+        f->ctx->launches++;
+    });
+}
+
+nfg_status nfg_field_evaluate(nfg_field* f, const float* X, int64_t B, float* out)
+{
+    return guard([&] {
+        nfg_ctx* c = f->ctx;
+        const float* dX = stage(c->s0, X, size_t(B) * f->gcfg.dims, c->stream);
+        float* dO = static_cast<float*>(c->s1.get(std::max<size_t>(size_t(B) * f->mcfg.output_width * 4, 16)));
+        const nfg_status st = nfg_field_evaluate_device(f, dX, B, dO);
+        if (st != NFG_OK)
+            throw Fail{ st, g_err };
+        if (B > 0)
+            NFG_CUDA(cudaMemcpyAsync(out, dO, size_t(B) * f->mcfg.output_width * 4, cudaMemcpyDeviceToHost, c->stream));
+        NFG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+nfg_status nfg_encode_forward(nfg_field* f, const float* X, int64_t B, float* Y, uint32_t* rows, float* weights)
+{
+    return guard([&] {
+        nfg_ctx* c = f->ctx;
+        const size_t LF = size_t(f->shape.in_real), nc = size_t(1) << f->gcfg.dims, L = size_t(f->gcfg.levels);
+        const float* dX = stage(c->s0, X, size_t(B) * f->gcfg.dims, c->stream);
+        float* dY = static_cast<float*>(c->s1.get(std::max<size_t>(size_t(B) * LF * 4, 16)));
+        uint32_t* dR = nullptr;
+        float* dW = nullptr;
+        if (rows && weights) {
+            dR = static_cast<uint32_t*>(c->s2.get(std::max<size_t>(L * B * nc * 4, 16)));
+            dW = static_cast<float*>(c->s3.get(std::max<size_t>(L * B * nc * 4, 16)));
+        }
+        NFG_CUDA(nfg::launch_encode_fwd_lv(f->shape, f->d_levels, dX, B, table_ptr(f), dY, dR, dW, c->stream));
+        c->launches++;
+        if (B > 0) {
+            NFG_CUDA(cudaMemcpyAsync(Y, dY, size_t(B) * LF * 4, cudaMemcpyDeviceToHost, c->stream));
+            if (dR) {
+                NFG_CUDA(cudaMemcpyAsync(rows, dR, L * B * nc * 4, cudaMemcpyDeviceToHost, c->stream));
+                NFG_CUDA(cudaMemcpyAsync(weights, dW, L * B * nc * 4, cudaMemcpyDeviceToHost, c->stream));
+            }
+        }
+        NFG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+nfg_status nfg_encode_backward(nfg_field* f, const float* X, int64_t B, const float* dY)
+{
+    return guard([&] {
+        nfg_ctx* c = f->ctx;
+        const float* dX = stage(c->s0, X, size_t(B) * f->gcfg.dims, c->stream);
+        const float* ddY = stage(c->s1, dY, size_t(B) * f->shape.in_real, c->stream);
+        NFG_CUDA(nfg::launch_encode_bwd_lv(f->shape, f->d_levels, dX, B, ddY, f->d_g, c->stream));
+        c->launches++;
+        NFG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+nfg_status nfg_mlp_forward(nfg_field* f, const float* Y, int64_t B, float* out)
+{
+    return guard([&] {
+        nfg_ctx* c = f->ctx;
+        const float* dY = stage(c->s0, Y, size_t(B) * f->shape.in_real, c->stream);
+        float* dO = static_cast<float*>(c->s1.get(std::max<size_t>(size_t(B) * f->mcfg.output_width * 4, 16)));
+        nfg::InferArgs a{};
+        a.Y = dY;
+        a.B = B;
+        a.W = f->d_p + f->n_tab;
+        a.b = f->d_p + f->n_tab + f->n_w;
+        a.out = dO;
+        NFG_CUDA(nfg::launch_infer(f->shape, nullptr, nfg::SRC_LOAD_Y, a, c->num_sms, c->stream));
+        c->launches++;
+        if (B > 0)
+            NFG_CUDA(cudaMemcpyAsync(out, dO, size_t(B) * f->mcfg.output_width * 4, cudaMemcpyDeviceToHost, c->stream));
+        NFG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+nfg_status nfg_mlp_backward(nfg_field* f, const float* Y, int64_t B, const float* dOut, float* dY)
+{
+    return guard([&] {
+        nfg_ctx* c = f->ctx;
+        const float* dYin = stage(c->s0, Y, size_t(B) * f->shape.in_real, c->stream);
+        const float* dO = stage(c->s1, dOut, size_t(B) * f->mcfg.output_width, c->stream);
+        float* ddY = static_cast<float*>(c->s2.get(std::max<size_t>(size_t(B) * f->shape.in_real * 4, 16)));
+        reset_scratch(f);
+        nfg::TrainArgs a{};
+        a.Y = dYin;
+        a.dout = dO;
+        a.B = B;
+        a.inv_count = 1.0f;
+        a.W = f->d_p + f->n_tab;
+        a.b = f->d_p + f->n_tab + f->n_w;
+        a.dY = ddY;
+        a.gW = f->d_g + f->n_tab;
+        a.gb = f->d_g + f->n_tab + f->n_w;
+        a.scratch = scratch_of(f);
+        NFG_CUDA(nfg::launch_train(f->shape, nullptr, nfg::SRC_LOAD_Y, nfg::GRAD_DOUT, nfg::SINK_STORE, a, c->num_sms,
+                                   c->stream, nullptr));
+        c->launches++;
+        if (B > 0)
+            NFG_CUDA(cudaMemcpyAsync(dY, ddY, size_t(B) * f->shape.in_real * 4, cudaMemcpyDeviceToHost, c->stream));
+        NFG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+nfg_status nfg_loss(nfg_ctx* c, int32_t kind, const float* pred, const float* target, int64_t n, int64_t count,
+                    float* dpred, float* loss)
+{
+    return guard([&] {
+        require(kind >= 0 && kind <= 2, "loss_with_grad: unknown loss");
+        const float* dP = stage(c->s0, pred, size_t(n), c->stream);
+        const float* dT = stage(c->s1, target, size_t(n), c->stream);
+        float* dD = static_cast<float*>(c->s2.get(std::max<size_t>(size_t(n) * 4, 16)));
+        if (!c->d_red)
+            NFG_CUDA(cudaMalloc(&c->d_red, sizeof(double)));
+        NFG_CUDA(cudaMemsetAsync(c->d_red, 0, sizeof(double), c->stream));
+        NFG_CUDA(nfg::launch_loss(kind, dP, dT, n, float(count), dD, c->d_red, c->stream));
+        c->launches++;
+        double sum = 0;
+        if (n > 0)
+            NFG_CUDA(cudaMemcpyAsync(dpred, dD, size_t(n) * 4, cudaMemcpyDeviceToHost, c->stream));
+        NFG_CUDA(cudaMemcpyAsync(&sum, c->d_red, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        NFG_CUDA(cudaStreamSynchronize(c->stream));
+        *loss = float(sum / double(count));
+    });
+}
+
+nfg_status nfg_adam_step(nfg_field* f, float lr_now)
+{
+    return guard([&] {
+        reset_scratch(f);
+        const uint64_t before = f->step;
+        run_adam(f, lr_now, true);
+        fetch_result(f);
+        if (f->h_res->flags[1]) {
+            f->step = before;
+            raise_if_aborted(f);
+        }
+    });
+}
+
+nfg_status nfg_host_alloc(size_t bytes, void** out)
+{
+    return guard([&] { NFG_CUDA(cudaMallocHost(out, bytes)); });
+}
+
+nfg_status nfg_host_free(void* p)
+{
+    return guard([&] { NFG_CUDA(cudaFreeHost(p)); });
+}
+
+}   // extern "C"

@@ -1,0 +1,461 @@
+// field_kernels.cuh — the fused training and inference kernels (templates).
+//
+// k_train: one persistent CTA of 8 warps loops over 128-sample tiles. Per tile:
+//   encode fwd (grid.hpp:245-271)   straight into mma A fragments (+ smem copy)
+//   MLP fwd (mlp.hpp:113-123)       activations in registers, smem copy for dW
+//   loss + dPred (losses.hpp)       fused in the output epilogue
+//   MLP bwd (mlp.hpp:146-157)       dz chain in registers, dz copies in smem
+//   encode bwd (grid.hpp:286-294)   straight out of the dY C fragments as
+//                                   float2 vector reductions into fp32 grads
+//   dW/db                           K = 128-sample MMA from smem, accumulated in
+//                                   registers across all tiles of the CTA and
+//                                   flushed once per CTA.
+// Backward operands are fp16 with a per-tile power-of-two scale (chosen from
+// the tile's max |dLoss/dpred|) so gradients of order 1e-6 stay normal; all
+// accumulation is fp32 and the scale is removed exactly (powers of two).
+//
+// k_infer: per-warp 16-sample tiles, no block barriers in the loop; encode ->
+// MLP -> output activation (model.cpp:102-109).
+#pragma once
+
+#include "encode.cuh"
+#include "kernels.h"
+#include "mlp_core.cuh"
+
+namespace nfg {
+
+using namespace mlp;
+
+constexpr int TS = 128;   // samples per training tile
+constexpr int TW = 8;     // warps per training CTA
+constexpr int IW = 4;     // warps per inference CTA
+
+__host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
+
+template <int IN_STEPS, int NH>
+struct TrainSmem {
+    using Lay = WLayout<IN_STEPS, NH>;
+    static constexpr int INS = Lay::INS;
+    static constexpr int OS = OUTP + 8;
+    static constexpr int LV_OFF = align16(Lay::BYTES);
+    static constexpr int ACT0_OFF = LV_OFF + align16(int(sizeof(LevelDev)) * NFG_MAX_LEVELS);
+    static constexpr int ACTH_OFF = ACT0_OFF + TS * INS * 2;
+    static constexpr int DZH_OFF = ACTH_OFF + NH * TS * HS * 2;
+    static constexpr int DZO_OFF = DZH_OFF + NH * TS * HS * 2;
+    static constexpr int DB_OFF = DZO_OFF + TS * OS * 2;
+    static constexpr int RED_OFF = DB_OFF + (NH + 1) * H * 4;
+    static constexpr int BYTES = RED_OFF + 4 * TW * 4;
+};
+
+template <int IN_STEPS, int NH>
+struct InferSmem {
+    using Lay = WLayout<IN_STEPS, NH>;
+    static constexpr int LV_OFF = align16(Lay::BYTES);
+    static constexpr int BYTES = LV_OFF + align16(int(sizeof(LevelDev)) * NFG_MAX_LEVELS);
+};
+
+__device__ __forceinline__ bool sane(float v) { return fabsf(v) <= 1e30f; }   // false for NaN/inf/huge
+
+// Input fragments of the warp's 16 rows: encoded from X, or loaded from Y.
+template <int SRC, int D, int F, typename TT, int IN_STEPS>
+__device__ __forceinline__ void input_frags(uint32_t (&afr)[IN_STEPS][4], const FieldShape& s, const LevelDev* lvs,
+                                            const float* xg, const float* xg8, bool vg, bool vg8, int64_t sg,
+                                            const float* __restrict__ Y, const void* table, int lane)
+{
+    const int t = lane & 3;
+#pragma unroll
+    for (int st = 0; st < IN_STEPS; ++st) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int col = 16 * st + 8 * h + 2 * t;
+            float2 e0 = make_float2(0.f, 0.f), e8 = make_float2(0.f, 0.f);
+            if (SRC == SRC_ENCODE) {
+                const TT* tab = static_cast<const TT*>(table);
+                if (vg)
+                    e0 = encode_pair<D, F, TT>(s.grid, lvs, xg, col, tab);
+                if (vg8)
+                    e8 = encode_pair<D, F, TT>(s.grid, lvs, xg8, col, tab);
+            } else {
+                const int w = s.in_real;
+                if (vg) {
+                    if (col < w) e0.x = Y[sg * w + col];
+                    if (col + 1 < w) e0.y = Y[sg * w + col + 1];
+                }
+                if (vg8) {
+                    if (col < w) e8.x = Y[(sg + 8) * w + col];
+                    if (col + 1 < w) e8.y = Y[(sg + 8) * w + col + 1];
+                }
+            }
+            afr[st][2 * h] = pack_half2(e0.x, e0.y);
+            afr[st][2 * h + 1] = pack_half2(e8.x, e8.y);
+        }
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void load_x(float* x, const float* __restrict__ X, int64_t sidx, bool valid)
+{
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        x[i] = valid ? X[sidx * D + i] : 0.0f;
+}
+
+template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IN_STEPS, int NH>
+__global__ void __launch_bounds__(TW * 32, 1)
+k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ levels)
+{
+    using Lay = WLayout<IN_STEPS, NH>;
+    using SM = TrainSmem<IN_STEPS, NH>;
+    extern __shared__ __align__(16) unsigned char sm[];
+    __half* ws = reinterpret_cast<__half*>(sm);
+    float* bs = reinterpret_cast<float*>(sm + Lay::HALVES * 2);
+    LevelDev* lvs = reinterpret_cast<LevelDev*>(sm + SM::LV_OFF);
+    __half* act0 = reinterpret_cast<__half*>(sm + SM::ACT0_OFF);
+    __half* acth = reinterpret_cast<__half*>(sm + SM::ACTH_OFF);
+    __half* dzh = reinterpret_cast<__half*>(sm + SM::DZH_OFF);
+    __half* dzo = reinterpret_cast<__half*>(sm + SM::DZO_OFF);
+    float* db = reinterpret_cast<float*>(sm + SM::DB_OFF);
+    float* red = reinterpret_cast<float*>(sm + SM::RED_OFF);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    const MlpShape msh{ s.in_real, s.n_out, s.sigmoid };
+    load_weights<IN_STEPS, NH>(ws, bs, a.W, a.b, msh);
+    if (SRC == SRC_ENCODE)
+        for (int i = tid; i < s.grid.L; i += blockDim.x)
+            lvs[i] = levels[i];
+    for (int i = tid; i < (NH + 1) * H; i += blockDim.x)
+        db[i] = 0.0f;
+    __syncthreads();
+
+    const __half* W0s = ws;
+    const __half* Whs = ws + Lay::W0_HALVES;
+    const __half* Wos = ws + Lay::W0_HALVES + (NH - 1) * Lay::WH_HALVES;
+    const float* bout = bs + H * NH;
+
+    constexpr int P0 = 4 * IN_STEPS, PH = 16, PO = 4;
+    constexpr int C0 = (P0 + TW - 1) / TW, CH = PH / TW, NHM = NH > 1 ? NH - 1 : 1;
+    float dw0[C0][2][4], dwh[NHM][CH][2][4], dwo[2][4];
+#pragma unroll
+    for (int c = 0; c < C0; ++c)
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            dw0[c][e >> 2][e & 3] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < NHM; ++k)
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                dwh[k][c][e >> 2][e & 3] = 0.0f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+        dwo[e >> 2][e & 3] = 0.0f;
+
+    bool bad = false;
+    const int64_t ntiles = (a.B + TS - 1) / TS;
+    const int r0 = 16 * warp;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t sg = tile * TS + r0 + g, sg8 = sg + 8;
+        const bool vg = sg < a.B, vg8 = sg8 < a.B;
+        float xg[D], xg8[D];
+        if (SRC == SRC_ENCODE) {
+            load_x<D>(xg, a.X, sg, vg);
+            load_x<D>(xg8, a.X, sg8, vg8);
+        }
+        // ---- encode / load inputs -------------------------------------
+        uint32_t afr[IN_STEPS][4];
+        input_frags<SRC, D, F, TT, IN_STEPS>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
+        store_a<IN_STEPS>(afr, act0, SM::INS, r0, lane);
+
+        // ---- MLP forward --------------------------------------------------
+        float acc[HT][4];
+        uint32_t mask[NH];
+        uint32_t ah[4][4];
+        layer_fwd<IN_STEPS, HT>(afr, W0s, SM::INS, acc, lane);
+        mask[0] = bias_relu<HT>(acc, bs, lane);
+        c_to_a<4, false>(acc, ah);
+        store_a<4>(ah, acth, HS, r0, lane);
+#pragma unroll
+        for (int k = 1; k < NH; ++k) {
+            layer_fwd<4, HT>(ah, Whs + (k - 1) * Lay::WH_HALVES, HS, acc, lane);
+            mask[k] = bias_relu<HT>(acc, bs + H * k, lane);
+            c_to_a<4, false>(acc, ah);
+            store_a<4>(ah, acth + k * TS * HS, HS, r0, lane);
+        }
+        float ao[2][4];
+        layer_fwd<4, 2>(ah, Wos, HS, ao, lane);
+
+        // ---- output activation, loss, dLoss/dpred --------------------------
+        float term = 0.0f, mx = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int col = 8 * j + 2 * t + (e & 1);
+                const bool valid = (e < 2 ? vg : vg8) && col < s.n_out;
+                const int64_t smp = e < 2 ? sg : sg8;
+                const float z = ao[j][e] + bout[col];
+                const float p = s.sigmoid ? 1.0f / (1.0f + expf(-z)) : z;
+                float d = 0.0f;
+                if (valid) {
+                    if (a.pred)
+                        a.pred[smp * s.n_out + col] = p;
+                    if (GRAD == GRAD_LOSS)
+                        d = loss_grad(a.loss_kind, p, a.target[smp * s.n_out + col], term);
+                    else
+                        d = a.dout[smp * s.n_out + col];
+                    if (s.sigmoid)
+                        d = d * (p * (1.0f - p));
+                }
+                bad |= !sane(d);
+                ao[j][e] = d;
+                mx = fmaxf(mx, fabsf(d));
+            }
+        }
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) {
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+            term += __shfl_xor_sync(0xffffffffu, term, m);
+        }
+        if (lane == 0) {
+            red[warp] = mx;
+            if (GRAD == GRAD_LOSS)
+                atomicAdd(a.scratch.loss_sum, double(term));
+        }
+        __syncthreads();
+        float tmax = 0.0f;
+#pragma unroll
+        for (int w = 0; w < TW; ++w)
+            tmax = fmaxf(tmax, red[w]);
+        float sc = 1.0f, isc = 1.0f;
+        if (tmax > 0.0f && tmax <= 1e30f) {
+            int ex;
+            frexpf(tmax, &ex);                 // tmax < 2^ex
+            const int k = max(-100, min(100, 4 - ex));   // scaled max < 16
+            sc = ldexpf(1.0f, k);
+            isc = ldexpf(1.0f, -k);
+        }
+
+        // ---- MLP backward ---------------------------------------------------
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                ao[j][e] *= sc;
+        uint32_t azo[1][4];
+        c_to_a<1, true>(ao, azo);
+        store_a<1>(azo, dzo, SM::OS, r0, lane);
+        {
+            float cs[2][2];
+            col_sums<2>(ao, cs);
+            if (g == 0)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+                        atomicAdd(&db[NH * H + 8 * j + 2 * t + q], cs[j][q] * isc);
+        }
+        layer_bwd<1, HT>(azo, Wos, HS, acc, lane);
+        apply_mask<HT>(acc, mask[NH - 1]);
+#pragma unroll
+        for (int k = NH - 1; k >= 1; --k) {
+            c_to_a<4, true>(acc, ah);
+            store_a<4>(ah, dzh + k * TS * HS, HS, r0, lane);
+            float cs[HT][2];
+            col_sums<HT>(acc, cs);
+            if (g == 0)
+#pragma unroll
+                for (int j = 0; j < HT; ++j)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+                        atomicAdd(&db[k * H + 8 * j + 2 * t + q], cs[j][q] * isc);
+            layer_bwd<4, HT>(ah, Whs + (k - 1) * Lay::WH_HALVES, HS, acc, lane);
+            apply_mask<HT>(acc, mask[k - 1]);
+        }
+        c_to_a<4, true>(acc, ah);
+        store_a<4>(ah, dzh, HS, r0, lane);
+        {
+            float cs[HT][2];
+            col_sums<HT>(acc, cs);
+            if (g == 0)
+#pragma unroll
+                for (int j = 0; j < HT; ++j)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+                        atomicAdd(&db[8 * j + 2 * t + q], cs[j][q] * isc);
+        }
+        float ay[2 * IN_STEPS][4];
+        layer_bwd<4, 2 * IN_STEPS>(ah, W0s, SM::INS, ay, lane);
+
+        // ---- dY -> encode backward / store -------------------------------------
+        const float dysc = isc * a.inv_count;
+#pragma unroll
+        for (int j = 0; j < 2 * IN_STEPS; ++j) {
+            const int col = 8 * j + 2 * t;
+            const float2 d0 = make_float2(ay[j][0] * dysc, ay[j][1] * dysc);
+            const float2 d8 = make_float2(ay[j][2] * dysc, ay[j][3] * dysc);
+            bad |= !(sane(d0.x) && sane(d0.y) && sane(d8.x) && sane(d8.y));
+            if (col >= s.in_real)
+                continue;
+            if (SINK == SINK_SCATTER) {
+                if (vg)
+                    scatter_pair<D, F>(s.grid, lvs, xg, col, d0, a.table_grad);
+                if (vg8)
+                    scatter_pair<D, F>(s.grid, lvs, xg8, col, d8, a.table_grad);
+            } else {
+                const int w = s.in_real;
+                if (vg) {
+                    a.dY[sg * w + col] = d0.x;
+                    if (col + 1 < w) a.dY[sg * w + col + 1] = d0.y;
+                }
+                if (vg8) {
+                    a.dY[sg8 * w + col] = d8.x;
+                    if (col + 1 < w) a.dY[sg8 * w + col + 1] = d8.y;
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- dW = dz^T act over the tile's 128 samples ------------------------
+#pragma unroll
+        for (int c = 0; c < C0; ++c) {
+            const int p = warp + c * TW;
+            if (p < P0) {
+                float c0[4], c1[4];
+                dw_pair<TS>(c0, c1, dzh, HS, act0, SM::INS, p / IN_STEPS, p % IN_STEPS, lane);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    dw0[c][0][e] = fmaf(c0[e], isc, dw0[c][0][e]);
+                    dw0[c][1][e] = fmaf(c1[e], isc, dw0[c][1][e]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 1; k < NH; ++k)
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int p = warp + c * TW;
+                float c0[4], c1[4];
+                dw_pair<TS>(c0, c1, dzh + k * TS * HS, HS, acth + (k - 1) * TS * HS, HS, p / 4, p % 4, lane);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    dwh[k - 1][c][0][e] = fmaf(c0[e], isc, dwh[k - 1][c][0][e]);
+                    dwh[k - 1][c][1][e] = fmaf(c1[e], isc, dwh[k - 1][c][1][e]);
+                }
+            }
+        if (warp < PO) {
+            float c0[4], c1[4];
+            dw_pair<TS>(c0, c1, dzo, SM::OS, acth + (NH - 1) * TS * HS, HS, 0, warp, lane);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                dwo[0][e] = fmaf(c0[e], isc, dwo[0][e]);
+                dwo[1][e] = fmaf(c1[e], isc, dwo[1][e]);
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- flush per-CTA dW / db (x 1/count) ----------------------------------
+    const float ic = a.inv_count;
+    auto flush = [&](const float (&cq)[2][4], int mt, int np, int out_k, int in_k, size_t woff) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int m = 16 * mt + g + (e >= 2 ? 8 : 0);
+                const int n = 8 * (2 * np + q) + 2 * t + (e & 1);
+                if (m < out_k && n < in_k) {
+                    const float v = cq[q][e] * ic;
+                    bad |= !sane(v);
+                    atomicAdd(a.gW + woff + m + size_t(n) * out_k, v);
+                }
+            }
+    };
+    {
+#pragma unroll
+        for (int c = 0; c < C0; ++c) {
+            const int p = warp + c * TW;
+            if (p < P0)
+                flush(dw0[c], p / IN_STEPS, p % IN_STEPS, H, s.in_real, 0);
+        }
+#pragma unroll
+        for (int k = 1; k < NH; ++k)
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int p = warp + c * TW;
+                flush(dwh[k - 1][c], p / 4, p % 4, H, H, size_t(H) * s.in_real + size_t(k - 1) * H * H);
+            }
+        if (warp < PO)
+            flush(dwo, 0, warp, s.n_out, H, size_t(H) * s.in_real + size_t(NH - 1) * H * H);
+    }
+    __syncthreads();
+    for (int i = tid; i < H * NH + s.n_out; i += blockDim.x) {
+        const float v = db[i] * ic;
+        bad |= !sane(v);
+        atomicAdd(a.gb + i, v);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0)
+        atomicOr(a.scratch.flags, 1u);
+}
+
+template <int SRC, int D, int F, typename TT, int IN_STEPS, int NH>
+__global__ void __launch_bounds__(IW * 32)
+k_infer(const InferArgs a, const FieldShape s, const LevelDev* __restrict__ levels)
+{
+    using Lay = WLayout<IN_STEPS, NH>;
+    using SM = InferSmem<IN_STEPS, NH>;
+    extern __shared__ __align__(16) unsigned char sm[];
+    __half* ws = reinterpret_cast<__half*>(sm);
+    float* bs = reinterpret_cast<float*>(sm + Lay::HALVES * 2);
+    LevelDev* lvs = reinterpret_cast<LevelDev*>(sm + SM::LV_OFF);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    const MlpShape msh{ s.in_real, s.n_out, s.sigmoid };
+    load_weights<IN_STEPS, NH>(ws, bs, a.W, a.b, msh);
+    if (SRC == SRC_ENCODE)
+        for (int i = tid; i < s.grid.L; i += blockDim.x)
+            lvs[i] = levels[i];
+    __syncthreads();
+    const __half* W0s = ws;
+    const __half* Whs = ws + Lay::W0_HALVES;
+    const __half* Wos = ws + Lay::W0_HALVES + (NH - 1) * Lay::WH_HALVES;
+    const float* bout = bs + H * NH;
+
+    const int64_t ntiles = (a.B + 15) / 16;
+    for (int64_t tile = int64_t(blockIdx.x) * IW + warp; tile < ntiles; tile += int64_t(gridDim.x) * IW) {
+        const int64_t sg = tile * 16 + g, sg8 = sg + 8;
+        const bool vg = sg < a.B, vg8 = sg8 < a.B;
+        float xg[D], xg8[D];
+        if (SRC == SRC_ENCODE) {
+            load_x<D>(xg, a.X, sg, vg);
+            load_x<D>(xg8, a.X, sg8, vg8);
+        }
+        uint32_t afr[IN_STEPS][4];
+        input_frags<SRC, D, F, TT, IN_STEPS>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
+        float acc[HT][4];
+        uint32_t ah[4][4];
+        layer_fwd<IN_STEPS, HT>(afr, W0s, Lay::INS, acc, lane);
+        bias_relu<HT>(acc, bs, lane);
+        c_to_a<4, false>(acc, ah);
+#pragma unroll
+        for (int k = 1; k < NH; ++k) {
+            layer_fwd<4, HT>(ah, Whs + (k - 1) * Lay::WH_HALVES, HS, acc, lane);
+            bias_relu<HT>(acc, bs + H * k, lane);
+            c_to_a<4, false>(acc, ah);
+        }
+        float ao[2][4];
+        layer_fwd<4, 2>(ah, Wos, HS, ao, lane);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int col = 8 * j + 2 * t + (e & 1);
+                const bool valid = (e < 2 ? vg : vg8) && col < s.n_out;
+                if (valid) {
+                    const float z = ao[j][e] + bout[col];
+                    a.out[(e < 2 ? sg : sg8) * s.n_out + col] = s.sigmoid ? 1.0f / (1.0f + expf(-z)) : z;
+                }
+            }
+    }
+}
+
+}   // namespace nfg

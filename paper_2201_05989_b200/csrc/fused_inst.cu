@@ -1,0 +1,49 @@
+// fused_inst.cu — sm_100a instantiations of the fused encode+MLP kernels for
+// one input dimensionality (compiled twice: -DNFG_D=2 and -DNFG_D=3).
+#include "launch_impl.cuh"
+
+#ifndef NFG_D
+#error "compile with -DNFG_D=2 or -DNFG_D=3"
+#endif
+#define NFG_CAT2(a, b) a##b
+#define NFG_CAT(a, b) NFG_CAT2(a, b)
+
+namespace nfg {
+
+// Built combinations (anything else is NFG_EUNSUPPORTED):
+//   F = 2: fp16 or fp32 tables, in_steps 1..2 (L*F <= 32), hidden_layers 1..3
+//   F = 1, 4, 8: fp16 or fp32 tables, in_steps 2, hidden_layers 2
+#define NFG_FUSED_LIST(X)                                                     \
+    X(2, __half, 1, 1) X(2, __half, 1, 2) X(2, __half, 1, 3)                  \
+    X(2, __half, 2, 1) X(2, __half, 2, 2) X(2, __half, 2, 3)                  \
+    X(2, float, 1, 1) X(2, float, 1, 2) X(2, float, 1, 3)                     \
+    X(2, float, 2, 1) X(2, float, 2, 2) X(2, float, 2, 3)                     \
+    X(1, __half, 2, 2) X(4, __half, 2, 2) X(8, __half, 2, 2)                  \
+    X(1, float, 2, 2) X(4, float, 2, 2) X(8, float, 2, 2)
+
+cudaError_t NFG_CAT(launch_fused_train_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
+                                                 int num_sms, cudaStream_t st, int* grid_used)
+{
+    const bool f32 = s.table_fp32 != 0;
+#define X(F_, TT_, IS_, NH_)                                                                               \
+    if (s.grid.F == F_ && f32 == (sizeof(TT_) == 4) && s.in_steps == IS_ && s.hidden_layers == NH_)         \
+        return run_train<SRC_ENCODE, GRAD_LOSS, SINK_SCATTER, NFG_D, F_, TT_, IS_, NH_>(s, lv, a, num_sms, st, \
+                                                                                         grid_used);
+    NFG_FUSED_LIST(X)
+#undef X
+    return cudaErrorNotSupported;
+}
+
+cudaError_t NFG_CAT(launch_fused_infer_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const InferArgs& a,
+                                                 int num_sms, cudaStream_t st)
+{
+    const bool f32 = s.table_fp32 != 0;
+#define X(F_, TT_, IS_, NH_)                                                                               \
+    if (s.grid.F == F_ && f32 == (sizeof(TT_) == 4) && s.in_steps == IS_ && s.hidden_layers == NH_)         \
+        return run_infer<SRC_ENCODE, NFG_D, F_, TT_, IS_, NH_>(s, lv, a, num_sms, st);
+    NFG_FUSED_LIST(X)
+#undef X
+    return cudaErrorNotSupported;
+}
+
+}   // namespace nfg

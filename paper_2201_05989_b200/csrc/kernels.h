@@ -1,0 +1,92 @@
+// kernels.h — host-side launch interface of the sm_100a kernels (internal to libnfg).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nfg_common.cuh"
+
+namespace nfg {
+
+// Static shape of one field model, resolved on the host.
+struct FieldShape {
+    GridDev grid;
+    int in_real;       // L*F
+    int in_steps;      // ceil(in_real / 16)
+    int hidden_layers;
+    int n_out;
+    int sigmoid;
+    int table_fp32;
+};
+
+// Gradient-side device scratch of one training step.
+struct StepScratch {
+    double* loss_sum;        // [1]
+    unsigned int* flags;     // [0]: maybe non-finite; [1]: abort; [2]: first bad group (+1); [3]: fp16 saturations
+    float* dy_max;           // [1] max |dY| (as float bits, non-negative)
+};
+
+enum TrainSource { SRC_ENCODE = 0, SRC_LOAD_Y = 1 };
+enum TrainGrad { GRAD_LOSS = 0, GRAD_DOUT = 1 };
+enum TrainSink { SINK_SCATTER = 0, SINK_STORE = 1 };
+
+struct TrainArgs {
+    // inputs
+    const float* X;          // d x B            (SRC_ENCODE)
+    const float* Y;          // in_real x B      (SRC_LOAD_Y)
+    const float* target;     // n_out x B        (GRAD_LOSS)
+    const float* dout;       // n_out x B        (GRAD_DOUT)
+    int64_t B;
+    int loss_kind;
+    float inv_count;         // 1 / (global batch * n_out); 1 for GRAD_DOUT
+    // parameters (fp32 master, reference layout) and tables
+    const void* table;       // fp16 shadow or fp32 master tables
+    const float* W;
+    const float* b;
+    // outputs
+    float* table_grad;       // SINK_SCATTER
+    float* dY;               // SINK_STORE: in_real x B
+    float* gW;
+    float* gb;
+    float* pred;             // optional n_out x B
+    StepScratch scratch;
+};
+
+struct InferArgs {
+    const float* X;
+    const float* Y;
+    int64_t B;
+    const void* table;
+    const float* W;
+    const float* b;
+    float* out;
+};
+
+// Returns cudaErrorNotSupported when the (dims, F, in_steps, hidden_layers)
+// combination has no sm_100a instantiation.
+// `lv` is the device copy of the level table (LevelDev[L]).
+cudaError_t launch_train(const FieldShape& s, const LevelDev* lv, int src, int grad, int sink, const TrainArgs& a,
+                         int num_sms, cudaStream_t st, int* grid_used);
+cudaError_t launch_infer(const FieldShape& s, const LevelDev* lv, int src, const InferArgs& a, int num_sms,
+                         cudaStream_t st);
+cudaError_t launch_encode_fwd_lv(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
+                                 const void* table, float* Y, uint32_t* rows, float* weights, cudaStream_t st);
+cudaError_t launch_encode_bwd_lv(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
+                                 const float* dY, float* grads, cudaStream_t st);
+
+struct AdamArgs {
+    float* p;
+    float* g;
+    float* m;
+    float* v;
+    __half* shadow;          // fp16 table shadow (may be null)
+    uint64_t n_tab, n_w, n_b;
+    float b1, b2, omb1, omb2, bc1, bc2, eps, l2, lr;
+    unsigned int* flags;
+};
+cudaError_t launch_adam(const AdamArgs& a, bool force_check, int num_sms, cudaStream_t st);
+cudaError_t launch_shadow(const float* p, __half* shadow, uint64_t n, cudaStream_t st);
+cudaError_t launch_loss(int kind, const float* pred, const float* target, int64_t n, float count, float* dpred,
+                        double* loss_sum, cudaStream_t st);
+
+}   // namespace nfg

@@ -1,0 +1,62 @@
+// launch_impl.cuh — host launch helpers for the templated train / infer kernels.
+#pragma once
+
+#include <algorithm>
+
+#include "field_kernels.cuh"
+
+namespace nfg {
+
+template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IS, int NH>
+cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& a, int num_sms, cudaStream_t st,
+                      int* grid_used)
+{
+    using SM = TrainSmem<IS, NH>;
+    auto k = k_train<SRC, GRAD, SINK, D, F, TT, IS, NH>;
+    static int per_sm = -1;   // resolved once per instantiation
+    if (per_sm < 0) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
+        if (e != cudaSuccess)
+            return e;
+        int n = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, TW * 32, SM::BYTES);
+        if (e != cudaSuccess)
+            return e;
+        per_sm = std::max(n, 1);
+    }
+    const int64_t ntiles = (a.B + TS - 1) / TS;
+    if (ntiles <= 0)
+        return cudaSuccess;
+    const int grid = int(std::min<int64_t>(ntiles, int64_t(num_sms) * per_sm));
+    if (grid_used)
+        *grid_used = grid;
+    k<<<grid, TW * 32, SM::BYTES, st>>>(a, s, lv);
+    return cudaGetLastError();
+}
+
+template <int SRC, int D, int F, typename TT, int IS, int NH>
+cudaError_t run_infer(const FieldShape& s, const LevelDev* lv, const InferArgs& a, int num_sms, cudaStream_t st)
+{
+    using SM = InferSmem<IS, NH>;
+    auto k = k_infer<SRC, D, F, TT, IS, NH>;
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
+        if (e != cudaSuccess)
+            return e;
+        int n = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, IW * 32, SM::BYTES);
+        if (e != cudaSuccess)
+            return e;
+        per_sm = std::max(n, 1);
+    }
+    const int64_t tiles = (a.B + 15) / 16;
+    if (tiles <= 0)
+        return cudaSuccess;
+    const int64_t want = (tiles + IW - 1) / IW;
+    const int grid = int(std::min<int64_t>(want, int64_t(num_sms) * per_sm));
+    k<<<grid, IW * 32, SM::BYTES, st>>>(a, s, lv);
+    return cudaGetLastError();
+}
+
+}   // namespace nfg

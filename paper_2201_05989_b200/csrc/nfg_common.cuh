@@ -1,0 +1,129 @@
+// nfg_common.cuh — shared device-side definitions for the sm_100a kernels.
+//
+// The grid-encoding arithmetic here restates grid.hpp:88-133,199-212 of the
+// reference with explicit IEEE round-to-nearest intrinsics (__fmul_rn,
+// __fadd_rn, __fsub_rn) so nvcc cannot contract it into FMAs: vertex selection
+// (corner + row index) and the interpolation weights are bit-identical to the
+// reference's fp32 path.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define NFG_MAX_LEVELS 32
+
+namespace nfg {
+
+// One level of the multiresolution grid as the kernels see it. Built on the
+// host from level_resolutions (grid.hpp:66-84) and passed by value.
+struct LevelDev {
+    uint32_t res;       // N_l
+    float res_f;        // float(N_l), the reference's Scalar(resolution)
+    uint32_t stride;    // N_l + 1 (dense levels)
+    uint32_t dense;     // (N_l+1)^d <= T
+    uint32_t row_off;   // first row of this level in the flat table
+    uint32_t len;       // rows at this level
+};
+
+struct GridDev {
+    int32_t L;
+    int32_t F;
+    int32_t d;
+    int32_t smooth;     // Interpolation::Smoothstep
+    uint32_t mask;      // T - 1
+    LevelDev lv[NFG_MAX_LEVELS];
+};
+
+// Clamp, scale, optional half-voxel offset, floor (grid.hpp:199-212).
+__device__ __forceinline__ void voxel_of(float x, float n, bool half, uint32_t& corner, float& frac)
+{
+    float p = __fmul_rn(fminf(fmaxf(x, 0.0f), 1.0f - 0x1p-20f), n);
+    if (half)
+        p = fminf(__fadd_rn(p, 0.5f), __fmul_rn(n, 1.0f - 0x1p-20f));
+    const float f = floorf(p);
+    corner = static_cast<uint32_t>(f);
+    frac = __fsub_rn(p, f);
+}
+
+// smoothstep1 (grid.hpp:112-116): (x*x) * (3 - 2x), no contraction.
+__device__ __forceinline__ float smoothstep1(float x)
+{
+    return __fmul_rn(__fmul_rn(x, x), __fsub_rn(3.0f, __fmul_rn(2.0f, x)));
+}
+
+// Per-dimension partial indices of the two candidate corners along each
+// axis; corner c's row is a combination selected by the bits of c. For hashed
+// levels the combination is XOR of prime products (grid.hpp:88-95, pi_1 = 1),
+// for dense levels the row-major sum (grid.hpp:100-110) — both identical to
+// the reference's per-corner evaluation.
+template <int D>
+struct CornerSet {
+    uint32_t lo[D], hi[D];
+    float t[D];   // interpolation parameter per axis (frac or smoothstep(frac))
+    uint32_t dense, mask;
+
+    __device__ __forceinline__ uint32_t row(int c) const
+    {
+        uint32_t r = (c & 1) ? hi[0] : lo[0];
+#pragma unroll
+        for (int i = 1; i < D; ++i) {
+            const uint32_t v = ((c >> i) & 1) ? hi[i] : lo[i];
+            r = dense ? r + v : (r ^ v);
+        }
+        return dense ? r : (r & mask);
+    }
+
+    // interpolation_weights (grid.hpp:120-133): w = ((1*a0)*a1)*a2.
+    __device__ __forceinline__ float weight(int c) const
+    {
+        float w = (c & 1) ? t[0] : __fsub_rn(1.0f, t[0]);
+#pragma unroll
+        for (int i = 1; i < D; ++i)
+            w = __fmul_rn(w, ((c >> i) & 1) ? t[i] : __fsub_rn(1.0f, t[i]));
+        return w;
+    }
+};
+
+template <int D>
+__device__ __forceinline__ CornerSet<D> corners_of(const GridDev& g, const LevelDev& lv, const float* x)
+{
+    CornerSet<D> cs;
+    cs.dense = lv.dense;
+    cs.mask = g.mask;
+    const uint32_t primes[3] = { 1u, 2654435761u, 805459861u };
+    uint32_t mul = 1u;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        uint32_t c;
+        float fr;
+        voxel_of(x[i], lv.res_f, g.smooth != 0, c, fr);
+        cs.t[i] = g.smooth ? smoothstep1(fr) : fr;
+        if (lv.dense) {
+            cs.lo[i] = c * mul;
+            cs.hi[i] = (c + 1u) * mul;
+            mul *= lv.stride;
+        } else {
+            cs.lo[i] = c * primes[i];
+            cs.hi[i] = (c + 1u) * primes[i];
+        }
+    }
+    return cs;
+}
+
+// ---- small helpers ------------------------------------------------------
+__device__ __forceinline__ uint32_t pack_half2(float a, float b)
+{
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ float2 unpack_half2(uint32_t v)
+{
+    __half2 h = *reinterpret_cast<__half2*>(&v);
+    return __half22float2(h);
+}
+
+__device__ __forceinline__ bool finite_f(float x) { return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u; }
+
+}   // namespace nfg

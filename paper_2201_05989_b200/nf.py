@@ -1,0 +1,487 @@
+"""Python mirror of the reference's hot-path API (namespace ``nf``), backed by
+the sm_100a library through the C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/nf/{grid,mlp,adam,losses,model}.hpp:
+
+* ``HashEncodingConfig``, ``MlpConfig``, ``AdamHyper``, ``LrSchedule`` — the
+  reference's config structs (grid.hpp:25-57, mlp.hpp:15-40, adam.hpp:13-25,124-137).
+* ``FieldModel`` — model.hpp:21-63. Set ``hash_cfg`` / ``mlp_cfg`` / ``hyper`` /
+  ``schedule`` then call ``init(seed)``; ``train_step`` and ``evaluate`` run on
+  the GPU. Public members of the reference (``tables``, ``mlp``, Adam state)
+  are exposed as host mirrors that read/write device memory.
+* Matrices are numpy arrays shaped (B, rows): C-order (B, d) is exactly the
+  reference's column-major d x B ``MatX``.
+
+Errors: ``ValueError`` (std::invalid_argument), ``NfgNonFinite``
+(std::runtime_error from adam_step), ``NfgUnsupported`` (valid for the
+reference but not built for sm_100a, e.g. hidden_width != 64).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+class Interpolation(enum.IntEnum):   # grid.hpp:20
+    Linear = 0
+    Smoothstep = 1
+
+
+class OutputActivation(enum.IntEnum):   # mlp.hpp:13
+    Linear = 0
+    Sigmoid = 1
+
+
+class LossKind(enum.IntEnum):   # model.hpp:17
+    L2 = 0
+    Mape = 1
+    RelativeL2 = 2
+
+
+@dataclass
+class HashEncodingConfig:   # grid.hpp:25-57
+    levels: int = 16
+    table_size: int = 1 << 14
+    features: int = 2
+    n_min: int = 16
+    n_max: int = 512
+    dims: int = 3
+    interpolation: Interpolation = Interpolation.Linear
+
+    def c(self) -> L.nfg_grid_config:
+        return L.nfg_grid_config(self.levels, self.table_size, self.features, self.n_min, self.n_max, self.dims,
+                                 int(self.interpolation))
+
+    def validate(self) -> None:
+        level_resolutions(self)
+
+    def growth_factor(self) -> float:
+        return L.load().nfg_growth_factor(C.byref(self.c()))
+
+    def output_width(self) -> int:
+        return self.levels * self.features
+
+
+@dataclass
+class GridLevelSpec:   # grid.hpp:59-64
+    level: int
+    resolution: int
+    table_len: int
+    dense: bool
+    row_offset: int
+
+
+def level_resolutions(cfg: HashEncodingConfig) -> List[GridLevelSpec]:   # grid.hpp:66-84
+    lib = L.load()
+    n = max(int(cfg.levels), 1)
+    arr = (L.nfg_level_spec * n)()
+    got = lib.nfg_level_resolutions(C.byref(cfg.c()), arr, n)
+    if got < 0:
+        raise L.NfgInvalidArgument(L.NFG_EINVAL, lib.nfg_last_error().decode())
+    return [GridLevelSpec(a.level, a.resolution, a.table_len, bool(a.dense), a.row_offset) for a in arr[:got]]
+
+
+def spatial_hash(coords: Sequence[int], dims: int, table_size: int) -> int:   # grid.hpp:88-95
+    c = (C.c_uint32 * 3)(*([int(x) & 0xFFFFFFFF for x in coords] + [0] * (3 - len(coords))))
+    return int(L.load().nfg_spatial_hash(c, dims, table_size))
+
+
+@dataclass
+class MlpConfig:   # mlp.hpp:15-40
+    input_width: int = 32
+    hidden_layers: int = 2
+    hidden_width: int = 64
+    output_width: int = 3
+    output_activation: OutputActivation = OutputActivation.Linear
+
+    def c(self) -> L.nfg_mlp_config:
+        return L.nfg_mlp_config(self.input_width, self.hidden_layers, self.hidden_width, self.output_width,
+                                int(self.output_activation))
+
+    def layer_count(self) -> int:
+        return self.hidden_layers + 1
+
+    def layer_shapes(self):
+        shapes, fin = [], self.input_width
+        for k in range(self.layer_count()):
+            out = self.hidden_width if k < self.hidden_layers else self.output_width
+            shapes.append((out, fin))
+            fin = out
+        return shapes
+
+    def parameter_count(self) -> int:
+        return sum(o * i + o for o, i in self.layer_shapes())
+
+
+@dataclass
+class AdamHyper:   # adam.hpp:13-25
+    lr: float = 1e-2
+    beta1: float = 0.9
+    beta2: float = 0.99
+    eps: float = 1e-15
+    l2: float = 1e-6
+
+    def c(self) -> L.nfg_adam_hyper:
+        return L.nfg_adam_hyper(self.lr, self.beta1, self.beta2, self.eps, self.l2)
+
+
+@dataclass
+class LrSchedule:   # adam.hpp:124-137
+    milestones: List[int] = field(default_factory=list)
+    factor: float = 0.33
+
+    def validate(self) -> None:
+        if not (self.factor > 0) or self.factor > 1:
+            raise ValueError("LrSchedule: factor must be in (0, 1]")
+        for a, b in zip(self.milestones, self.milestones[1:]):
+            if b <= a:
+                raise ValueError("LrSchedule: milestones must be strictly increasing")
+
+
+def lr_at(schedule: LrSchedule, base_lr: float, step: int) -> float:   # adam.hpp:139-146
+    ms = (C.c_int64 * max(len(schedule.milestones), 1))(*schedule.milestones)
+    return L.load().nfg_lr_at(ms, len(schedule.milestones), schedule.factor, base_lr, step)
+
+
+def default_schedule(total_steps: int, factor: float = 0.33) -> LrSchedule:   # adam.hpp:150-161
+    s = LrSchedule(factor=factor)
+    nxt, stride = int(0.65 * total_steps), int(0.30 * total_steps)
+    while nxt < total_steps and stride > 0:
+        s.milestones.append(nxt)
+        nxt += stride
+    return s
+
+
+@dataclass
+class Options:
+    """sm_100a build options (no reference equivalent)."""
+    table_fp32: bool = False    # gather fp32 master tables instead of the fp16 shadow
+    fused_train: bool = True    # one fused kernel per step vs staged encode / MLP / encode-bwd kernels
+
+    def c(self) -> L.nfg_options:
+        return L.nfg_options(int(self.table_fp32), int(self.fused_train))
+
+
+class Context:
+    """One CUDA device + stream (+ optional NCCL communicator)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = L.load()
+        h = C.c_void_p()
+        L.check(self.lib.nfg_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.nfg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self) -> None:
+        L.check(self.lib.nfg_ctx_synchronize(self.h))
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.nfg_ctx_stream(self.h) or 0)
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.nfg_ctx_launch_count(self.h))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        L.check(L.load().nfg_comm_unique_id(buf))
+        return bytes(buf)
+
+    def attach_comm(self, uid: bytes, rank: int, nranks: int) -> None:
+        buf = (C.c_uint8 * 128)(*uid)
+        L.check(self.lib.nfg_ctx_attach_comm(self.h, buf, rank, nranks))
+
+
+_DEFAULT_CTX: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _DEFAULT_CTX
+    if _DEFAULT_CTX is None:
+        _DEFAULT_CTX = Context(0)
+    return _DEFAULT_CTX
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _dptr(t) -> Optional[int]:
+    """Device pointer of a torch CUDA tensor (or a raw int)."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return int(t.data_ptr())
+
+
+BUF_PARAMS, BUF_GRADS, BUF_ADAM_M, BUF_ADAM_V = range(4)
+
+
+@dataclass
+class EncodeCache:   # grid.hpp:183-195 (exported for checks; the GPU path recomputes)
+    rows: np.ndarray
+    weights: np.ndarray
+
+
+class FieldModel:
+    """model.hpp:21-63 on the GPU (hash encoder)."""
+
+    def __init__(self, ctx: Optional[Context] = None, options: Optional[Options] = None):
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        self.hash_cfg = HashEncodingConfig()
+        self.mlp_cfg = MlpConfig()
+        self.hyper = AdamHyper()
+        self.schedule = LrSchedule()
+        self.options = options or Options()
+        self.h = None
+        self._sizes = (0, 0, 0)
+
+    # ---- lifecycle ----------------------------------------------------------
+    def _create(self) -> None:
+        if self.h:
+            self.lib.nfg_field_destroy(self.h)
+            self.h = None
+        self.mlp_cfg.input_width = self.encoded_width()   # model.cpp:101
+        h = C.c_void_p()
+        L.check(self.lib.nfg_field_create(self.ctx.h, C.byref(self.hash_cfg.c()), C.byref(self.mlp_cfg.c()),
+                                          C.byref(self.hyper.c()), C.byref(self.options.c()), C.byref(h)))
+        self.h = h
+        sz = (C.c_uint64 * 3)()
+        L.check(self.lib.nfg_field_sizes(self.h, sz))
+        self._sizes = tuple(int(x) for x in sz)
+
+    def init(self, seed: int) -> None:   # model.cpp:23-37
+        self._create()
+        L.check(self.lib.nfg_field_init(self.h, seed))
+        self._push_schedule()
+
+    def close(self) -> None:
+        if self.h:
+            self.lib.nfg_field_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _push_schedule(self) -> None:
+        self.schedule.validate()
+        ms = (C.c_int64 * max(len(self.schedule.milestones), 1))(*self.schedule.milestones)
+        L.check(self.lib.nfg_field_set_schedule(self.h, ms, len(self.schedule.milestones), self.schedule.factor))
+        L.check(self.lib.nfg_field_set_hyper(self.h, C.byref(self.hyper.c())))
+
+    def encoded_width(self) -> int:
+        return self.hash_cfg.output_width()
+
+    def parameter_count(self) -> int:
+        return sum(self._sizes)
+
+    @property
+    def sizes(self):
+        """(table params, MLP weights, MLP biases) — the three param groups."""
+        return self._sizes
+
+    # ---- host mirrors of the public members ------------------------------------
+    def read(self, which: int, offset: int = 0, count: Optional[int] = None) -> np.ndarray:
+        n = self.parameter_count() - offset if count is None else count
+        out = np.empty(n, np.float32)
+        L.check(self.lib.nfg_field_read(self.h, which, offset, n, _ptr(out)))
+        return out
+
+    def write(self, which: int, data, offset: int = 0) -> None:
+        d = _f32(data).ravel()
+        L.check(self.lib.nfg_field_write(self.h, which, offset, d.size, _ptr(d)))
+
+    @property
+    def params(self) -> np.ndarray:
+        return self.read(BUF_PARAMS)
+
+    @property
+    def grads(self) -> np.ndarray:
+        return self.read(BUF_GRADS)
+
+    @property
+    def table_params(self) -> np.ndarray:
+        return self.read(BUF_PARAMS, 0, self._sizes[0])
+
+    @table_params.setter
+    def table_params(self, v) -> None:
+        self.write(BUF_PARAMS, v, 0)
+
+    def mlp_weights(self) -> List[np.ndarray]:
+        """Weights as (out, in) matrices (the reference's MlpParams::weights)."""
+        flat = self.read(BUF_PARAMS, self._sizes[0], self._sizes[1])
+        mats, off = [], 0
+        for o, i in self.mlp_cfg.layer_shapes():
+            mats.append(flat[off: off + o * i].reshape(i, o).T.copy())
+            off += o * i
+        return mats
+
+    def device_buffer(self, which: int):
+        p = L._fp()
+        n = C.c_uint64()
+        L.check(self.lib.nfg_field_device_buffer(self.h, which, C.byref(p), C.byref(n)))
+        return C.cast(p, C.c_void_p).value, int(n.value)
+
+    @property
+    def step(self) -> int:
+        s = C.c_uint64()
+        L.check(self.lib.nfg_field_get_step(self.h, C.byref(s)))
+        return int(s.value)
+
+    @step.setter
+    def step(self, s: int) -> None:
+        L.check(self.lib.nfg_field_set_step(self.h, s))
+
+    def adam_state(self):
+        """(step, m, v) flat in param-group order (AdamState, adam.hpp:56-73)."""
+        return self.step, self.read(BUF_ADAM_M), self.read(BUF_ADAM_V)
+
+    def param_groups(self):
+        """The three groups of model.cpp:49-77: (name, offset, size, apply_l2, skip_zero_grad)."""
+        t, w, b = self._sizes
+        return [("tables", 0, t, False, True), ("mlp_weights", t, w, True, False),
+                ("mlp_biases", t + w, b, False, False)]
+
+    # ---- the hot path ----------------------------------------------------------
+    def _check_x(self, X) -> np.ndarray:
+        X = _f32(X)
+        if X.ndim != 2 or X.shape[1] != self.hash_cfg.dims:
+            raise L.NfgInvalidArgument(L.NFG_EINVAL, "encode_forward: input dimensionality mismatch")
+        # grid.hpp:226-229 — validated on the host like the reference
+        if not np.isfinite(X).all():
+            raise L.NfgInvalidArgument(L.NFG_EINVAL, "encode_forward: non-finite input")
+        if (X < np.float32(-1e-6)).any() or (X > np.float32(1) + np.float32(1e-6)).any():
+            raise L.NfgInvalidArgument(L.NFG_EINVAL, "encode_forward: input outside [0,1]^d")
+        return X
+
+    def train_step(self, X, target, loss: LossKind, step: int) -> float:   # model.cpp:111-138
+        X = self._check_x(X)
+        T = _f32(target)
+        if T.shape != (X.shape[0], self.mlp_cfg.output_width):
+            raise L.NfgInvalidArgument(L.NFG_EINVAL, "l2_loss: shape mismatch")
+        self._push_schedule()
+        out = C.c_float()
+        L.check(self.lib.nfg_field_train_step(self.h, _ptr(X), _ptr(T), X.shape[0], int(loss), step, C.byref(out)))
+        return float(out.value)
+
+    def train_step_host_ptr(self, x_ptr: int, t_ptr: int, B: int, loss: LossKind, step: int) -> float:
+        """train_step on caller-owned (e.g. pinned) host buffers, no validation copy."""
+        out = C.c_float()
+        L.check(self.lib.nfg_field_train_step(self.h, x_ptr, t_ptr, B, int(loss), step, C.byref(out)))
+        return float(out.value)
+
+    def train_step_device(self, X, target, B_local: int, B_global: int, loss: LossKind, step: int) -> None:
+        """Asynchronous step on device pointers (torch CUDA tensors or ints)."""
+        L.check(self.lib.nfg_field_train_step_device(self.h, _dptr(X), _dptr(target), B_local, B_global, int(loss),
+                                                     step, None))
+
+    def check(self) -> None:
+        L.check(self.lib.nfg_field_check(self.h))
+
+    def evaluate(self, X) -> np.ndarray:   # model.cpp:102-109
+        X = self._check_x(X)
+        out = np.empty((X.shape[0], self.mlp_cfg.output_width), np.float32)
+        L.check(self.lib.nfg_field_evaluate(self.h, _ptr(X), X.shape[0], _ptr(out)))
+        return out
+
+    def evaluate_device(self, X, B: int, out) -> None:
+        L.check(self.lib.nfg_field_evaluate_device(self.h, _dptr(X), B, _dptr(out)))
+
+    # ---- components -------------------------------------------------------------
+    def encode_forward(self, X, want_cache: bool = False):   # grid.hpp:219-272
+        X = self._check_x(X)
+        B = X.shape[0]
+        Y = np.empty((B, self.encoded_width()), np.float32)
+        rows = wts = None
+        if want_cache:
+            nc = 1 << self.hash_cfg.dims
+            rows = np.empty((self.hash_cfg.levels, B, nc), np.uint32)
+            wts = np.empty((self.hash_cfg.levels, B, nc), np.float32)
+        L.check(self.lib.nfg_encode_forward(self.h, _ptr(X), B, _ptr(Y), _ptr(rows), _ptr(wts)))
+        return (Y, EncodeCache(rows, wts)) if want_cache else Y
+
+    def encode_backward(self, X, dY) -> None:   # grid.hpp:277-295
+        X = self._check_x(X)
+        dY = _f32(dY)
+        if dY.shape != (X.shape[0], self.encoded_width()):
+            raise L.NfgInvalidArgument(L.NFG_EINVAL, "encode_backward: gradient shape does not match cache")
+        L.check(self.lib.nfg_encode_backward(self.h, _ptr(X), X.shape[0], _ptr(dY)))
+
+    def mlp_forward(self, Y) -> np.ndarray:   # mlp.hpp:104-124
+        Y = _f32(Y)
+        if Y.ndim != 2 or Y.shape[1] != self.mlp_cfg.input_width:
+            raise L.NfgInvalidArgument(L.NFG_EINVAL, "mlp_forward: input width mismatch")
+        out = np.empty((Y.shape[0], self.mlp_cfg.output_width), np.float32)
+        L.check(self.lib.nfg_mlp_forward(self.h, _ptr(Y), Y.shape[0], _ptr(out)))
+        return out
+
+    def mlp_backward(self, Y, dOut) -> np.ndarray:   # mlp.hpp:129-158 (grads accumulate)
+        Y = _f32(Y)
+        dOut = _f32(dOut)
+        if dOut.shape != (Y.shape[0], self.mlp_cfg.output_width):
+            raise L.NfgInvalidArgument(L.NFG_EINVAL, "mlp_backward: shape mismatch with cache")
+        dY = np.empty((Y.shape[0], self.mlp_cfg.input_width), np.float32)
+        L.check(self.lib.nfg_mlp_backward(self.h, _ptr(Y), Y.shape[0], _ptr(dOut), _ptr(dY)))
+        return dY
+
+    def adam_step(self, lr_now: float) -> None:   # adam.hpp:78-122 over param_groups()
+        L.check(self.lib.nfg_adam_step(self.h, C.c_float(lr_now)))
+
+
+def loss_with_grad(kind: LossKind, pred, target, ctx: Optional[Context] = None):   # model.cpp:140-149
+    p = _f32(pred)
+    t = _f32(target)
+    if p.shape != t.shape:
+        raise L.NfgInvalidArgument(L.NFG_EINVAL, "l2_loss: shape mismatch")
+    ctx = ctx or default_context()
+    d = np.empty_like(p)
+    out = C.c_float()
+    L.check(ctx.lib.nfg_loss(ctx.h, int(kind), _ptr(p), _ptr(t), p.size, p.size, _ptr(d), C.byref(out)))
+    return float(out.value), d
+
+
+class PinnedBuffer:
+    """Page-locked host memory (cudaMallocHost) viewed as a numpy array."""
+
+    def __init__(self, shape, dtype=np.float32):
+        self.lib = L.load()
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = C.c_void_p()
+        L.check(self.lib.nfg_host_alloc(max(nbytes, 1), C.byref(p)))
+        self.ptr = p.value
+        buf = (C.c_uint8 * nbytes).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def free(self) -> None:
+        if getattr(self, "ptr", None):
+            self.lib.nfg_host_free(C.c_void_p(self.ptr))
+            self.ptr = None

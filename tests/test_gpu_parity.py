@@ -1,0 +1,317 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle on
+identical inputs and seeds.
+
+Contract (stated per test):
+  * bit-exact: level table, PCG32/Glorot init, per-corner row indices and
+    interpolation weights, Adam updates (fp32, no contraction), loss gradients;
+  * tolerance: encoded features (fp32 tables: FMA-level; fp16 tables: vs the
+    oracle run on fp16-rounded tables), MLP outputs (fp16 MMA), gradients,
+    loss values and loss curves.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _nf():
+    from paper_2201_05989_b200 import nf
+    return nf
+
+
+def _grid(nf, **kw):
+    kw.setdefault("interpolation", 0)
+    return nf.HashEncodingConfig(**kw)
+
+
+def _ocfg(g):
+    return O.GridCfg(levels=g.levels, table_size=g.table_size, features=g.features, n_min=g.n_min,
+                     n_max=g.n_max, dims=g.dims, smoothstep=bool(g.interpolation))
+
+
+def _model(nf, grid, hidden_layers=2, n_out=1, sigmoid=False, table_fp32=False, fused=True, lr=1e-2, seed=1337):
+    m = nf.FieldModel(options=nf.Options(table_fp32=table_fp32, fused_train=fused))
+    m.hash_cfg = grid
+    m.mlp_cfg = nf.MlpConfig(hidden_layers=hidden_layers, hidden_width=64, output_width=n_out,
+                             output_activation=nf.OutputActivation.Sigmoid if sigmoid else nf.OutputActivation.Linear)
+    m.hyper = nf.AdamHyper(lr=lr)
+    m.init(seed)
+    return m
+
+
+def _oracle_field(m, lr=1e-2, seed=1337):
+    g = _ocfg(m.hash_cfg)
+    f = O.Field(g, O.MlpCfg(hidden_layers=m.mlp_cfg.hidden_layers, hidden_width=64,
+                            output_width=m.mlp_cfg.output_width, sigmoid=bool(m.mlp_cfg.output_activation)),
+                O.Hyper(lr=lr))
+    f.init(seed)
+    return f
+
+
+def _points(n, d, seed=5):
+    return O.Pcg32(seed, 9).floats(n * d).reshape(n, d)
+
+
+ENC_CASES = [
+    dict(dims=3, levels=16, table_size=1 << 19, features=2, n_min=16, n_max=2048),
+    dict(dims=2, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=1024),
+    dict(dims=3, levels=16, table_size=1 << 12, features=2, n_min=4, n_max=512, interpolation=1),
+    dict(dims=2, levels=8, table_size=1 << 10, features=4, n_min=8, n_max=200),
+    dict(dims=3, levels=4, table_size=1 << 14, features=8, n_min=4, n_max=64),
+    dict(dims=2, levels=32, table_size=1 << 16, features=1, n_min=2, n_max=4096, interpolation=1),
+]
+
+
+@pytest.mark.parametrize("case", ENC_CASES)
+def test_init_bit_exact(case):   # model.cpp:23-37, grid.hpp:158-164, mlp.hpp:74-94
+    nf = _nf()
+    m = _model(nf, _grid(nf, **case))
+    f = _oracle_field(m)
+    assert np.array_equal(m.params, f.params)
+
+
+@pytest.mark.parametrize("case", ENC_CASES)
+@pytest.mark.parametrize("fp32", [True, False])
+def test_encode_forward(case, fp32):   # grid.hpp:219-272
+    nf = _nf()
+    g = _grid(nf, **case)
+    m = _model(nf, g, table_fp32=fp32)
+    X = _points(4099, g.dims)
+    X[:5] = [[0.0] * g.dims, [1.0] * g.dims, [0.5] * g.dims, [1e-7] * g.dims, [1 - 1e-7] * g.dims]
+    Y, cache = m.encode_forward(X, want_cache=True)
+    tables = m.table_params
+    if not fp32:
+        tables = tables.astype(np.float16).astype(np.float32)   # oracle on the fp16-rounded tables
+    Yo, co = O.encode_forward(_ocfg(g), tables, X)
+    # vertex selection and weights: bit-exact
+    assert np.array_equal(cache.rows, co.rows)
+    assert np.array_equal(cache.weights.view(np.uint32), co.weights.view(np.uint32))
+    # features: FMA-level (fp32 tables) / fp16-storage-level
+    tol = 1e-6 if fp32 else 1e-3
+    assert np.abs(Y - Yo).max() <= tol * np.abs(Yo).max() + 1e-9
+
+
+@pytest.mark.parametrize("case", ENC_CASES[:4])
+def test_encode_backward(case):   # grid.hpp:277-295 (fp32 atomics: order-nondeterministic)
+    nf = _nf()
+    g = _grid(nf, **case)
+    m = _model(nf, g, table_fp32=True)
+    X = _points(2048, g.dims, seed=11)
+    dY = O.Pcg32(3, 3).floats(2048 * g.levels * g.features).reshape(2048, -1) * 2 - 1
+    m.encode_backward(X, dY)
+    got = m.grads[: m.sizes[0]]
+    _, cache = O.encode_forward(_ocfg(g), m.table_params, X)
+    want = np.zeros(m.sizes[0], np.float32)
+    O.encode_backward(_ocfg(g), cache, dY, want)
+    assert np.array_equal(got != 0, want != 0) or np.abs(got - want).max() < 1e-6
+    assert np.abs(got - want).max() <= 1e-5 * np.abs(want).max() + 1e-7
+
+
+@pytest.mark.parametrize("hidden,n_out,sig", [(2, 1, False), (2, 3, True), (1, 4, False), (3, 16, True)])
+def test_mlp_forward_backward(hidden, n_out, sig):   # mlp.hpp:104-158 (fp16 MMA, fp32 accumulate)
+    nf = _nf()
+    g = _grid(nf, dims=3, levels=16, table_size=1 << 12, features=2, n_min=16, n_max=256)
+    m = _model(nf, g, hidden_layers=hidden, n_out=n_out, sigmoid=sig)
+    mc = O.MlpCfg(32, hidden, 64, n_out, sig)
+    W = m.params[m.sizes[0]: m.sizes[0] + m.sizes[1]]
+    b = m.params[m.sizes[0] + m.sizes[1]:]
+    rng = np.random.default_rng(0)
+    Y = rng.uniform(-1, 1, (1000, 32)).astype(np.float32)
+    out = m.mlp_forward(Y)
+    ref = O.mlp_forward(mc, W, b, Y)
+    assert np.abs(out - ref).max() <= 5e-3 * np.abs(ref).max() + 1e-4
+    dOut = (rng.uniform(-1, 1, (1000, n_out)) * 1e-5).astype(np.float32)   # realistic /count magnitudes
+    dY = m.mlp_backward(Y, dOut)
+    _, gW, gb, dYo = O.mlp_forward_backward(mc, W, b, Y, dOut)
+    G = m.grads
+    gWg = G[m.sizes[0]: m.sizes[0] + m.sizes[1]]
+    gbg = G[m.sizes[0] + m.sizes[1]:]
+    for a, r in ((gWg, gW), (gbg, gb), (dY, dYo)):
+        assert np.linalg.norm(a - r) <= 1e-2 * np.linalg.norm(r) + 1e-12
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_loss_gradients_bit_exact(kind):   # losses.hpp:10-59
+    nf = _nf()
+    rng = np.random.default_rng(kind)
+    p = rng.uniform(-1, 1, (777, 3)).astype(np.float32)
+    t = rng.uniform(-1, 1, (777, 3)).astype(np.float32)
+    p[0, 0] = t[0, 0]   # MAPE kink: subgradient 0
+    loss, d = nf.loss_with_grad(kind, p, t)
+    lo, do = O.loss_with_grad(kind, p, t)
+    assert np.array_equal(d.view(np.uint32), do.view(np.uint32))
+    assert abs(loss - lo) <= 1e-5 * abs(lo)
+
+
+def test_adam_bit_exact_and_skip_zero():   # adam.hpp:78-122, SPEC decisions on skip-zero
+    nf = _nf()
+    g = _grid(nf, dims=2, levels=4, table_size=1 << 8, features=2, n_min=4, n_max=32)
+    m = _model(nf, g, hidden_layers=1)
+    f = _oracle_field(m)
+    n = m.parameter_count()
+    rng = np.random.default_rng(3)
+    grads = rng.normal(0, 1e-3, n).astype(np.float32)
+    grads[: m.sizes[0]][rng.uniform(size=m.sizes[0]) < 0.4] = 0.0   # untouched table entries
+    grads[m.sizes[0]:][:7] = 0.0                                       # zero MLP grads still update (no skip)
+    for step in range(1, 4):
+        m.write(1, grads)
+        f.grads[:] = grads
+        m.adam_step(np.float32(1e-2 / step))
+        f_lib_adam(f, np.float32(1e-2 / step))
+        assert np.array_equal(m.params.view(np.uint32), f.params.view(np.uint32)), step
+        _, mm, vv = m.adam_state()
+        assert np.array_equal(mm.view(np.uint32), f.m.view(np.uint32))
+        assert np.array_equal(vv.view(np.uint32), f.v.view(np.uint32))
+        assert (m.grads == 0).all()
+        assert m.step == f.step == step
+
+
+def f_lib_adam(f, lr_now):
+    """Oracle adam_step over the field's three groups (model.cpp:49-77)."""
+    t, w = f.n_tab, f.n_w
+    groups = [O.ParamGroup("tables", f.params[:t], f.grads[:t], False, True),
+              O.ParamGroup("mlp_weights", f.params[t:t + w], f.grads[t:t + w], True, False),
+              O.ParamGroup("mlp_biases", f.params[t + w:], f.grads[t + w:], False, False)]
+    st = O.AdamState(step=f.step, m=[f.m[:t], f.m[t:t + w], f.m[t + w:]], v=[f.v[:t], f.v[t:t + w], f.v[t + w:]])
+    O.adam_step(st, groups, O.Hyper(lr=f.hyper.lr), lr_now)
+    f.step = st.step
+
+
+def test_adam_nonfinite_names_group():   # adam.hpp:86-90; state untouched
+    nf = _nf()
+    from paper_2201_05989_b200._lib import NfgNonFinite
+    g = _grid(nf, dims=2, levels=4, table_size=1 << 8, features=2, n_min=4, n_max=32)
+    m = _model(nf, g, hidden_layers=1)
+    before = m.params
+    grads = np.zeros(m.parameter_count(), np.float32)
+    grads[m.sizes[0] + 3] = np.nan
+    m.write(1, grads)
+    with pytest.raises(NfgNonFinite, match="mlp_weights"):
+        m.adam_step(1e-2)
+    assert np.array_equal(m.params, before)
+    assert m.step == 0
+
+
+def test_invalid_and_unsupported():   # grid.hpp:224-229, NFG_EUNSUPPORTED
+    nf = _nf()
+    from paper_2201_05989_b200._lib import NfgInvalidArgument, NfgUnsupported
+    g = _grid(nf, dims=2, levels=4, table_size=1 << 8, features=2, n_min=4, n_max=32)
+    m = _model(nf, g, hidden_layers=1)
+    with pytest.raises(NfgInvalidArgument):
+        m.evaluate(np.array([[0.5, 1.5]], np.float32))
+    with pytest.raises(NfgInvalidArgument):
+        m.evaluate(np.array([[0.5, np.nan]], np.float32))
+    with pytest.raises(NfgInvalidArgument):
+        m.evaluate(np.zeros((3, 3), np.float32))
+    bad = nf.FieldModel()
+    bad.hash_cfg = g
+    bad.mlp_cfg = nf.MlpConfig(hidden_width=32)
+    with pytest.raises(NfgUnsupported):
+        bad.init(1)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("case,kind,n_out,sig", [
+    (dict(dims=3, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=512), 1, 1, False),
+    (dict(dims=2, levels=16, table_size=1 << 12, features=2, n_min=16, n_max=256), 0, 3, True),
+    (dict(dims=3, levels=16, table_size=1 << 12, features=2, n_min=8, n_max=128, interpolation=1), 2, 1, False),
+])
+def test_train_step_parity(case, kind, n_out, sig, fused):   # model.cpp:111-138
+    nf = _nf()
+    g = _grid(nf, **case)
+    m = _model(nf, g, n_out=n_out, sigmoid=sig, table_fp32=True, fused=fused, lr=1e-3)
+    f = _oracle_field(m, lr=1e-3)
+    rng = O.Pcg32(21, 4)
+    before = m.params
+    touched = None
+    for step in range(1, 4):
+        X = rng.floats(3000 * g.dims).reshape(3000, g.dims)
+        T = (rng.floats(3000 * n_out).reshape(3000, n_out) * (1.0 if sig else 0.6) - (0 if sig else 0.3))
+        lg = m.train_step(X, T, kind, step)
+        lo = f.train_step(X, T, kind, step)
+        assert abs(lg - lo) <= 5e-3 * abs(lo) + 1e-7, (step, lg, lo)
+        _, cache = O.encode_forward(_ocfg(g), before[: m.sizes[0]], X)
+        specs = O.level_resolutions(_ocfg(g))
+        rows = set()
+        for l in range(g.levels):
+            rows.update((specs[l].row_offset + cache.rows[l].ravel().astype(np.int64)).tolist())
+        touched = rows if touched is None else touched | rows
+    pg, po = m.params, f.params
+    t = m.sizes[0]
+    F = g.features
+    changed_g = np.any((pg[:t] != before[:t]).reshape(-1, F), axis=1)
+    changed_o = np.any((po[:t] != before[:t]).reshape(-1, F), axis=1)
+    untouched = np.ones(changed_g.size, bool)
+    untouched[list(touched)] = False
+    assert not changed_g[untouched].any()            # skip-zero: untouched rows bit-identical
+    assert not changed_o[untouched].any()
+    # Adam's normalised steps: parameters agree to a few lr (sign flips of tiny grads)
+    assert np.abs(pg - po).max() <= 6 * 1e-3
+    assert np.mean(np.abs(pg - po) <= 1e-4) > 0.97
+
+
+def test_full_size_config2_properties():   # BASELINE config 2 at full size (B = 2^18, T = 2^19)
+    nf = _nf()
+    g = _grid(nf, dims=3, levels=16, table_size=1 << 19, features=2, n_min=16, n_max=2048)
+    m = _model(nf, g, n_out=1, lr=1e-4)
+    B = 1 << 18
+    X = _points(B, 3, seed=1337)
+    T = O.csg_sdf(X).reshape(B, 1)
+    before = m.params
+    loss = m.train_step(X, T, nf.LossKind.Mape, 1)
+    assert np.isfinite(loss)
+    # rows are bit-exact at full size; the changed-entry set equals the touched set
+    Y, cache = m.encode_forward(X[: 1 << 16], want_cache=True)
+    _, co = O.encode_forward(_ocfg(g), before[: m.sizes[0]], X[: 1 << 16])
+    assert np.array_equal(cache.rows, co.rows)
+    _, cfull = O.encode_forward(_ocfg(g), before[: m.sizes[0]], X)
+    specs = O.level_resolutions(_ocfg(g))
+    touched = np.zeros(m.sizes[0] // 2, bool)
+    for l in range(16):
+        touched[specs[l].row_offset + cfull.rows[l].ravel().astype(np.int64)] = True
+    after = m.params
+    changed = np.any((after[: m.sizes[0]] != before[: m.sizes[0]]).reshape(-1, 2), axis=1)
+    assert not changed[~touched].any()
+    assert changed[touched].mean() > 0.99
+    # second step keeps decreasing the loss on the same batch
+    loss2 = m.train_step(X, T, nf.LossKind.Mape, 2)
+    assert loss2 < loss
+
+
+@pytest.mark.parametrize("fp32", [True, False])
+def test_evaluate_parity(fp32):   # model.cpp:102-109 (fused encode + MLP inference)
+    nf = _nf()
+    g = _grid(nf, dims=3, levels=16, table_size=1 << 19, features=2, n_min=16, n_max=2048)
+    m = _model(nf, g, n_out=1)
+    f = _oracle_field(m)
+    # train a few steps so the tables are not ~1e-4 noise
+    rng = O.Pcg32(2, 2)
+    for step in range(1, 6):
+        X = rng.floats(1 << 15).reshape(-1, 3)[: 10000]
+        m.train_step(X, O.csg_sdf(X).reshape(-1, 1), nf.LossKind.Mape, step)
+    f.params[:] = m.params
+    X = _points(1 << 16, 3, seed=77)
+    out = m.evaluate(X)
+    ref = f.evaluate(X)
+    assert np.abs(out - ref).max() <= 1e-2 * np.abs(ref).max() + 1e-4
+
+
+def test_image_loss_curve_parity():   # loss curves within 2%, config-1 shape, shorter run
+    nf = _nf()
+    from _tasks import fit_image
+    w = h = 128
+    rgb = O.make_test_image(w, h)
+    g = _grid(nf, dims=2, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=64)
+    m = _model(nf, g, n_out=3, sigmoid=True, table_fp32=True)
+    m.schedule = nf.default_schedule(300)
+    f = _oracle_field(m)
+    f.set_schedule(O.default_milestones(300))
+    rg = fit_image(m, rgb, w, h, seed=1337, batch=1 << 12, total_steps=300, log_interval=50)
+    ro = fit_image(f, rgb, w, h, seed=1337, batch=1 << 12, total_steps=300, log_interval=50)
+    for (sg, lg, pg), (so, lo, po) in zip(rg, ro):
+        assert sg == so
+        assert abs(pg - po) <= 0.3, (sg, pg, po)   # PSNR within 0.3 dB along the curve
+    assert abs(rg[-1][1] - ro[-1][1]) <= 0.02 * ro[-1][1] + 1e-6
+    assert rg[-1][2] > rg[0][2] + 10
