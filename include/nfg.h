@@ -160,6 +160,11 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
 nfg_status nfg_field_train_step_device(nfg_field* f, const float* X, const float* target,
                                        int64_t B_local, int64_t B_global, int32_t loss_kind,
                                        int64_t step, float* loss_dev);
+/* Forward + loss + backward of train_step WITHOUT the Adam update: gradients
+ * accumulate into the field's grad slab (mlp_backward / encode_backward
+ * semantics, mlp.hpp:147-148, grid.hpp:292); pair with nfg_adam_step. */
+nfg_status nfg_field_gradients(nfg_field* f, const float* X, const float* target, int64_t B,
+                               int32_t loss_kind, float* loss);
 /* Non-finite check of the last device step (synchronises). */
 nfg_status nfg_field_check(nfg_field* f);
 

@@ -297,8 +297,10 @@ void run_adam(nfg_field* f, float lr_now, bool force_check)
     f->step = next;
 }
 
-void device_train_step(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
-                       int loss_kind, int64_t step)
+// Forward + loss + backward: gradients ACCUMULATE into the grad slab (the
+// reference's mlp_backward / encode_backward semantics); no optimizer step.
+void device_backward(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
+                     int loss_kind)
 {
     require(loss_kind >= 0 && loss_kind <= 2, "train_step: unknown loss");
     require(B_local >= 0 && B_global >= B_local, "train_step: invalid batch size");
@@ -349,8 +351,14 @@ void device_train_step(nfg_field* f, const float* X, const float* target, int64_
         NFG_NCCL(nccl().all_reduce(&f->d_res->loss_sum, &f->d_res->loss_sum, 1, ncclFloat64, ncclSum, c->comm, c->stream));
         NFG_NCCL(nccl().all_reduce(f->d_res->flags, f->d_res->flags, 1, ncclUint32, ncclMax, c->comm, c->stream));
     }
+}
+
+void device_train_step(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
+                       int loss_kind, int64_t step)
+{
+    device_backward(f, X, target, B_local, B_global, loss_kind);
     const float lr_now = float(nfg::host::lr_at(f->milestones, f->factor, f->hyper.lr, step));
-    Span span(c, 1);
+    Span span(f->ctx, 1);
     run_adam(f, lr_now, false);
 }
 
@@ -379,6 +387,24 @@ nfg::FieldShape make_shape(const nfg_grid_config& g, const nfg_mlp_config& m, co
         d.len = lv[l].table_len;
     }
     return s;
+}
+
+// encode_forward's input validation (grid.hpp:226-229) for host-pointer calls;
+// runs before anything touches device state, as in the reference.
+void validate_inputs(const float* X, int64_t B, int d)
+{
+    const int64_t n = B * d;
+    bool nonfinite = false, outside = false;
+    const float lo = -1e-6f, hi = 1.0f + 1e-6f;
+    for (int64_t i = 0; i < n; ++i) {
+        const float v = X[i];
+        nonfinite |= !std::isfinite(v);
+        outside |= (v < lo) || (v > hi);
+    }
+    if (nonfinite)
+        throw std::invalid_argument("encode_forward: non-finite input");
+    if (outside)
+        throw std::invalid_argument("encode_forward: input outside [0,1]^d");
 }
 
 float* buffer_of(nfg_field* f, int which)
@@ -697,6 +723,7 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
     return guard([&] {
         nfg_ctx* c = f->ctx;
         const int d = f->gcfg.dims, no = f->mcfg.output_width;
+        validate_inputs(X, B, d);
         const float* dX = stage(c->s0, X, size_t(B) * d, c->stream);
         const float* dT = stage(c->s1, target, size_t(B) * no, c->stream);
         const uint64_t before = f->step;
@@ -707,6 +734,22 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
             raise_if_aborted(f);
         }
         const double count = double(B) * c->nranks * no;
+        if (loss)
+            *loss = count > 0 ? float(f->h_res->loss_sum / count) : 0.0f;
+    });
+}
+
+nfg_status nfg_field_gradients(nfg_field* f, const float* X, const float* target, int64_t B, int32_t loss_kind,
+                               float* loss)
+{
+    return guard([&] {
+        nfg_ctx* c = f->ctx;
+        validate_inputs(X, B, f->gcfg.dims);
+        const float* dX = stage(c->s0, X, size_t(B) * f->gcfg.dims, c->stream);
+        const float* dT = stage(c->s1, target, size_t(B) * f->mcfg.output_width, c->stream);
+        device_backward(f, dX, dT, B, B * c->nranks, loss_kind);
+        fetch_result(f);
+        const double count = double(B) * c->nranks * f->mcfg.output_width;
         if (loss)
             *loss = count > 0 ? float(f->h_res->loss_sum / count) : 0.0f;
     });
@@ -754,6 +797,7 @@ nfg_status nfg_field_evaluate(nfg_field* f, const float* X, int64_t B, float* ou
 {
     return guard([&] {
         nfg_ctx* c = f->ctx;
+        validate_inputs(X, B, f->gcfg.dims);
         const float* dX = stage(c->s0, X, size_t(B) * f->gcfg.dims, c->stream);
         float* dO = static_cast<float*>(c->s1.get(std::max<size_t>(size_t(B) * f->mcfg.output_width * 4, 16)));
         const nfg_status st = nfg_field_evaluate_device(f, dX, B, dO);
@@ -770,6 +814,7 @@ nfg_status nfg_encode_forward(nfg_field* f, const float* X, int64_t B, float* Y,
     return guard([&] {
         nfg_ctx* c = f->ctx;
         const size_t LF = size_t(f->shape.in_real), nc = size_t(1) << f->gcfg.dims, L = size_t(f->gcfg.levels);
+        validate_inputs(X, B, f->gcfg.dims);
         const float* dX = stage(c->s0, X, size_t(B) * f->gcfg.dims, c->stream);
         float* dY = static_cast<float*>(c->s1.get(std::max<size_t>(size_t(B) * LF * 4, 16)));
         uint32_t* dR = nullptr;
@@ -795,6 +840,7 @@ nfg_status nfg_encode_backward(nfg_field* f, const float* X, int64_t B, const fl
 {
     return guard([&] {
         nfg_ctx* c = f->ctx;
+        validate_inputs(X, B, f->gcfg.dims);
         const float* dX = stage(c->s0, X, size_t(B) * f->gcfg.dims, c->stream);
         const float* ddY = stage(c->s1, dY, size_t(B) * f->shape.in_real, c->stream);
         NFG_CUDA(nfg::launch_encode_bwd_lv(f->shape, f->d_levels, dX, B, ddY, f->d_g, c->stream));

@@ -393,6 +393,16 @@ class FieldModel:
         L.check(self.lib.nfg_field_train_step(self.h, _ptr(X), _ptr(T), X.shape[0], int(loss), step, C.byref(out)))
         return float(out.value)
 
+    def gradients(self, X, target, loss: LossKind) -> float:
+        """Forward + loss + backward without Adam; grads accumulate (call adam_step after)."""
+        X = self._check_x(X)
+        T = _f32(target)
+        if T.shape != (X.shape[0], self.mlp_cfg.output_width):
+            raise L.NfgInvalidArgument(L.NFG_EINVAL, "l2_loss: shape mismatch")
+        out = C.c_float()
+        L.check(self.lib.nfg_field_gradients(self.h, _ptr(X), _ptr(T), X.shape[0], int(loss), C.byref(out)))
+        return float(out.value)
+
     def train_step_host_ptr(self, x_ptr: int, t_ptr: int, B: int, loss: LossKind, step: int) -> float:
         """train_step on caller-owned (e.g. pinned) host buffers, no validation copy."""
         out = C.c_float()

@@ -1,0 +1,71 @@
+"""numpy emulation of the GPU MLP's storage precision (test-side checker).
+
+Restates mlp.hpp:104-158 in float64 but rounds to fp16 exactly where the
+sm_100a kernel stores fp16 operands: the layer inputs (Y and every hidden
+activation), the weights, and the backward dz operands. Bias gradients use
+the unrounded dz (the kernel sums its fp32 C fragments). Agreement with this
+emulation (tight tolerance) proves the kernel's math; agreement with the fp32
+oracle (loose tolerance) measures the precision choice.
+"""
+import numpy as np
+
+
+def h(x):
+    return np.asarray(x, np.float64).astype(np.float16).astype(np.float64)
+
+
+def split(W, b, shapes):
+    mats, biases, wo, bo = [], [], 0, 0
+    for out, fin in shapes:
+        mats.append(np.asarray(W[wo: wo + out * fin], np.float64).reshape(fin, out).T)
+        biases.append(np.asarray(b[bo: bo + out], np.float64))
+        wo += out * fin
+        bo += out
+    return mats, biases
+
+
+def forward(W, b, shapes, Y, sigmoid):
+    mats, biases = split(W, b, shapes)
+    a = h(Y)
+    acts, masks = [a], []
+    for k, (Wk, bk) in enumerate(zip(mats, biases)):
+        z = a @ h(Wk).T + bk
+        if k + 1 < len(mats):
+            m = z > 0
+            masks.append(m)
+            a = h(np.where(m, z, 0.0))
+            acts.append(a)
+        else:
+            out = 1 / (1 + np.exp(-z)) if sigmoid else z
+    return out, acts, masks, mats
+
+
+def tile_scale(d, tile=128):
+    """The kernel's per-128-sample power-of-two scale: max|d| * s < 16."""
+    s = np.ones((d.shape[0], 1))
+    for r in range(0, d.shape[0], tile):
+        mx = np.abs(d[r:r + tile]).max()
+        if mx > 0:
+            _, ex = np.frexp(np.float32(mx))
+            s[r:r + tile] = 2.0 ** max(-100, min(100, 4 - int(ex)))
+    return s
+
+
+def backward(W, b, shapes, Y, dOut, sigmoid):
+    out, acts, masks, mats = forward(W, b, shapes, Y, sigmoid)
+    dz = np.asarray(dOut, np.float64)
+    if sigmoid:
+        dz = dz * (out * (1 - out))
+    sc = tile_scale(dz)
+    gW, gb = [None] * len(mats), [None] * len(mats)
+    for k in range(len(mats) - 1, -1, -1):
+        gb[k] = dz.sum(0)
+        dzh = h(dz * sc) / sc
+        gW[k] = dzh.T @ acts[k]
+        da = dzh @ h(mats[k])
+        if k > 0:
+            dz = np.where(masks[k - 1], da, 0.0)
+        else:
+            dY = da
+    flatW = np.concatenate([g.T.ravel() for g in gW])
+    return out, flatW, np.concatenate(gb), dY

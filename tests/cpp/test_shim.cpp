@@ -1,0 +1,135 @@
+// test_shim.cpp — the reference's C++ call pattern through include/nf/gpu_field_model.hpp.
+//
+// Mirrors the FieldModel usage of the reference's own tests: config members set
+// before init (acceptance.cpp:326-336), train_step with the reference's
+// LossKind values, the untouched-rows contract (acceptance.cpp:346-369) and
+// exception types (grid.hpp:224-229, adam.hpp:86-90). Built by tests/cpp/Makefile
+// and run by tests/test_gpu_shim.py on a B200.
+#include <cmath>
+#include <cstdio>
+#include <set>
+
+#include "../../include/nf/gpu_field_model.hpp"
+
+// Stand-ins with the reference's member names (grid.hpp:25-33, mlp.hpp:15-20,
+// adam.hpp:13-18, adam.hpp:124-127); the shim reads them by name.
+struct HashEncodingConfig {
+    int levels = 16;
+    std::uint32_t table_size = 1u << 14;
+    int features = 2;
+    int n_min = 16;
+    int n_max = 512;
+    int dims = 3;
+    int interpolation = 0;
+};
+struct MlpConfig {
+    int input_width = 32, hidden_layers = 2, hidden_width = 64, output_width = 3, output_activation = 0;
+};
+struct AdamHyper {
+    double lr = 1e-2, beta1 = 0.9, beta2 = 0.99, eps = 1e-15, l2 = 1e-6;
+};
+struct LrSchedule {
+    std::vector<std::int64_t> milestones;
+    double factor = 0.33;
+};
+using FieldModel = nf::gpu::FieldModelT<HashEncodingConfig, MlpConfig, AdamHyper, LrSchedule>;
+using nf::gpu::Mat;
+
+static int failures = 0;
+#define CHECK(c)                                                            \
+    do {                                                                    \
+        if (!(c)) {                                                         \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);        \
+            ++failures;                                                     \
+        }                                                                   \
+    } while (0)
+
+int main()
+{
+    nf::gpu::Context ctx(0);
+
+    // criterion 4 through the model path (acceptance.cpp:326-369)
+    {
+        FieldModel model(ctx);
+        model.hash_cfg.dims = 2;
+        model.hash_cfg.levels = 16;
+        model.hash_cfg.table_size = 1u << 10;
+        model.hash_cfg.n_min = 8;
+        model.hash_cfg.n_max = 64;
+        model.mlp_cfg.hidden_layers = 1;
+        model.mlp_cfg.output_width = 1;
+        model.init(3);
+        const std::vector<float> before = model.read(NFG_BUF_PARAMS);
+        Mat X(2, 4), target(1, 4, 0.3f);
+        const float xs[4] = { 0.1f, 0.11f, 0.12f, 0.13f };
+        for (int i = 0; i < 4; ++i)
+            X(0, i) = X(1, i) = xs[i];
+        const float loss = model.train_step(X, target, NFG_LOSS_L2, 1);
+        CHECK(std::isfinite(loss));
+        const std::vector<float> after = model.read(NFG_BUF_PARAMS);
+        std::uint64_t sizes[3];
+        nf::gpu::check(nfg_field_sizes(model.handle(), sizes));
+        std::size_t moved = 0;
+        for (std::size_t i = 0; i < sizes[0]; ++i)
+            moved += after[i] != before[i];
+        // 4 points x 16 levels x 4 corners x 2 features bounds the touched entries
+        CHECK(moved > 0 && moved <= 4 * 16 * 4 * 2);
+        CHECK(model.adam_step_count() == 1);
+    }
+
+    // training decreases the loss; evaluate returns out x B (model.cpp:102-109)
+    {
+        FieldModel model(ctx);
+        model.hash_cfg.dims = 3;
+        model.hash_cfg.table_size = 1u << 16;
+        model.hash_cfg.n_max = 256;
+        model.mlp_cfg.output_width = 1;
+        model.hyper.lr = 1e-3;
+        model.init(1337);
+        const long B = 1 << 14;
+        Mat X(3, B), T(1, B);
+        std::uint32_t s = 12345u;
+        for (long j = 0; j < B; ++j) {
+            for (int i = 0; i < 3; ++i) {
+                s = s * 1664525u + 1013904223u;
+                X(i, j) = float(s >> 8) * 0x1p-24f;
+            }
+            const float dx = X(0, j) - 0.5f, dy = X(1, j) - 0.5f, dz = X(2, j) - 0.5f;
+            T(0, j) = std::sqrt(dx * dx + dy * dy + dz * dz) - 0.3f;
+        }
+        float first = 0, last = 0;
+        for (int step = 1; step <= 50; ++step) {
+            const float l = model.train_step(X, T, NFG_LOSS_MAPE, step);
+            if (step == 1)
+                first = l;
+            last = l;
+        }
+        CHECK(last < 0.5f * first);
+        const Mat out = model.evaluate(X);
+        CHECK(out.rows() == 1 && out.cols() == B);
+        Mat bad(3, 1, 0.5f);
+        bad(1, 0) = 1.5f;
+        bool threw = false;
+        try {
+            model.evaluate(bad);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+
+    // loss_with_grad KAT (test_losses.cpp:35-55): l2 2.5, dPred {1, 2}
+    {
+        Mat p(1, 2), t(1, 2), d;
+        p(0, 0) = 1.0f;
+        p(0, 1) = 3.0f;
+        t(0, 0) = 0.0f;
+        t(0, 1) = 1.0f;
+        const float l = nf::gpu::loss_with_grad(ctx, NFG_LOSS_L2, p, t, d);
+        CHECK(std::fabs(l - 2.5f) < 1e-6f);
+        CHECK(d(0, 0) == 1.0f && d(0, 1) == 2.0f);
+    }
+
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+    return failures ? 1 : 0;
+}
