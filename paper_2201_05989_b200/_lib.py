@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnfg.so")
+LIB_PATH = os.environ.get("NFG_LIB", os.path.join(_HERE, "libnfg.so"))   # NFG_LIB: A/B builds
 
 NFG_OK, NFG_EINVAL, NFG_ENONFINITE, NFG_EUNSUPPORTED, NFG_ECUDA, NFG_ENCCL, NFG_ELOGIC = range(7)
 

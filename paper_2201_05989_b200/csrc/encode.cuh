@@ -75,6 +75,104 @@ __device__ __forceinline__ float2 encode_pair(const GridDev& g, const LevelDev* 
     return acc;
 }
 
+// ---- asynchronous (cp.async) staged gathers --------------------------------
+// The fused training kernel runs one CTA per SM, so it cannot hide the L2
+// latency of its corner gathers with warps. Instead each thread issues ALL of
+// its corner loads for a tile as cp.async copies into private shared-memory
+// slots (no registers held while in flight), waits once, then blends.
+template <int F, typename TT>
+struct Stage {
+    // bytes per staged element: the (col, col+1) feature pair of one corner
+    // (F >= 2), or the aligned 4-byte word holding one feature (F == 1)
+    static constexpr int SB = (F == 1) ? 4 : 2 * int(sizeof(TT));
+};
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem)
+{
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
+}
+
+__device__ __forceinline__ void cp_async_wait_all()
+{
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Elements staged per (sample, col-pair): 2^D corners, times 2 levels for F == 1.
+template <int D, int F>
+struct PairElems {
+    static constexpr int NE = (F == 1 ? 2 : 1) << D;
+};
+
+template <int D, int F, typename TT>
+__device__ __forceinline__ void gather_issue(const GridDev& g, const LevelDev* lvs, const float* x, int col,
+                                             const TT* __restrict__ table, unsigned char* slot0, int slot_stride)
+{
+    constexpr int SB = Stage<F, TT>::SB;
+#pragma unroll
+    for (int h = 0; h < (F == 1 ? 2 : 1); ++h) {
+        const int l = F == 1 ? col + h : col / F;
+        if (l >= g.L)
+            continue;
+        const LevelDev lv = lvs[l];
+        const CornerSet<D> cs = corners_of<D>(g, lv, x);
+#pragma unroll
+        for (int c = 0; c < (1 << D); ++c) {
+            const size_t e = (size_t(lv.row_off) + cs.row(c)) * F + (F == 1 ? 0 : (col % F));
+            const TT* src = table + e;
+            if (F == 1 && sizeof(TT) == 2)   // aligned 4-byte word holding the half
+                src = table + (e & ~size_t(1));
+            cp_async<SB>(slot0 + (h * (1 << D) + c) * slot_stride, src);
+        }
+    }
+}
+
+template <int D, int F, typename TT>
+__device__ __forceinline__ float2 gather_blend(const GridDev& g, const LevelDev* lvs, const float* x, int col,
+                                               const unsigned char* slot0, int slot_stride)
+{
+    float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int h = 0; h < (F == 1 ? 2 : 1); ++h) {
+        const int l = F == 1 ? col + h : col / F;
+        if (l >= g.L)
+            continue;
+        const LevelDev lv = lvs[l];
+        const CornerSet<D> cs = corners_of<D>(g, lv, x);
+        float a = 0.0f, b = 0.0f;
+#pragma unroll
+        for (int c = 0; c < (1 << D); ++c) {
+            const unsigned char* s = slot0 + (h * (1 << D) + c) * slot_stride;
+            const float w = cs.weight(c);
+            if (F == 1) {
+                float v;
+                if (sizeof(TT) == 2) {
+                    const float2 two = unpack_half2(*reinterpret_cast<const uint32_t*>(s));
+                    v = (cs.row(c) + lv.row_off) & 1u ? two.y : two.x;
+                } else {
+                    v = *reinterpret_cast<const float*>(s);
+                }
+                a = fmaf(w, v, a);
+            } else {
+                const float2 v = sizeof(TT) == 2 ? unpack_half2(*reinterpret_cast<const uint32_t*>(s))
+                                                 : *reinterpret_cast<const float2*>(s);
+                a = fmaf(w, v.x, a);
+                b = fmaf(w, v.y, b);
+            }
+        }
+        if (F == 1) {
+            if (h == 0)
+                acc.x = a;
+            else
+                acc.y = a;
+        } else {
+            acc = make_float2(a, b);
+        }
+    }
+    return acc;
+}
+
 __device__ __forceinline__ void red_add2(float* p, float a, float b)
 {
     // vector reduction to global memory (sm_90+): one L2 atomic for both features
@@ -108,6 +206,30 @@ __device__ __forceinline__ void scatter_pair(const GridDev& g, const LevelDev* l
     const LevelDev lv = lvs[l];
     const CornerSet<D> cs = corners_of<D>(g, lv, x);
     float* base = grads + size_t(lv.row_off) * F + (col % F);
+#ifndef NFG_NO_PAIR_RED
+    if (F == 2) {
+        // x-adjacent corners (c, c+1) whose rows form an aligned pair {2k, 2k+1}
+        // (always at hashed levels with even x since pi_1 = 1, and at dense
+        // levels with an even row) share one 16-byte vector reduction.
+        const bool odd_base = (lv.row_off & 1u) != 0;
+#pragma unroll
+        for (int c = 0; c < (1 << D); c += 2) {
+            const uint32_t r0 = cs.row(c), r1 = cs.row(c + 1);
+            const float w0 = cs.weight(c), w1 = cs.weight(c + 1);
+            if (!odd_base && r1 == (r0 ^ 1u)) {
+                const bool lo0 = r0 < r1;
+                const uint32_t rl = lo0 ? r0 : r1;
+                const float wl = lo0 ? w0 : w1, wh = lo0 ? w1 : w0;
+                atomicAdd(reinterpret_cast<float4*>(base + size_t(rl) * 2),
+                          make_float4(wl * dy.x, wl * dy.y, wh * dy.x, wh * dy.y));
+            } else {
+                red_add2(base + size_t(r0) * 2, w0 * dy.x, w0 * dy.y);
+                red_add2(base + size_t(r1) * 2, w1 * dy.x, w1 * dy.y);
+            }
+        }
+        return;
+    }
+#endif
 #pragma unroll
     for (int c = 0; c < (1 << D); ++c) {
         const float w = cs.weight(c);

@@ -199,7 +199,9 @@ struct nfg_field {
     std::vector<nfg_level_spec> levels;
     nfg::FieldShape shape{};
     nfg::LevelDev* d_levels = nullptr;
-    uint64_t n_tab = 0, n_w = 0, n_b = 0, n_total = 0, n_alloc = 0;
+    uint64_t n_tab = 0, n_w = 0, n_b = 0, n_total = 0, n_alloc = 0;   // reference (API) layout counts
+    uint64_t n_tab_dev = 0, n_total_dev = 0;   // device layout: each level starts on an even row
+    std::vector<uint64_t> dev_row_off;        // per-level first row in the device layout
     float* d_p = nullptr;
     float* d_g = nullptr;
     float* d_m = nullptr;
@@ -256,7 +258,7 @@ const void* table_ptr(nfg_field* f) { return f->opts.table_fp32 ? static_cast<co
 
 void refresh_shadow(nfg_field* f)
 {
-    NFG_CUDA(nfg::launch_shadow(f->d_p, f->d_shadow, f->n_tab, f->ctx->stream));
+    NFG_CUDA(nfg::launch_shadow(f->d_p, f->d_shadow, f->n_tab_dev, f->ctx->stream));
     f->ctx->launches++;
 }
 
@@ -279,7 +281,7 @@ void run_adam(nfg_field* f, float lr_now, bool force_check)
     a.m = f->d_m;
     a.v = f->d_v;
     a.shadow = f->d_shadow;
-    a.n_tab = f->n_tab;
+    a.n_tab = f->n_tab_dev;
     a.n_w = f->n_w;
     a.n_b = f->n_b;
     a.b1 = s.b1;
@@ -314,11 +316,11 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
     a.loss_kind = loss_kind;
     a.inv_count = count > 0 ? float(1.0 / count) : 0.0f;
     a.table = table_ptr(f);
-    a.W = f->d_p + f->n_tab;
-    a.b = f->d_p + f->n_tab + f->n_w;
+    a.W = f->d_p + f->n_tab_dev;
+    a.b = f->d_p + f->n_tab_dev + f->n_w;
     a.table_grad = f->d_g;
-    a.gW = f->d_g + f->n_tab;
-    a.gb = f->d_g + f->n_tab + f->n_w;
+    a.gW = f->d_g + f->n_tab_dev;
+    a.gb = f->d_g + f->n_tab_dev + f->n_w;
     a.scratch = scratch_of(f);
     if (c->profile)
         c->prof_steps++;
@@ -347,7 +349,7 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
         // Data-parallel exchange: sum of the shards' (globally normalised)
         // gradients == the single-GPU gradient of the global batch; loss sums
         // and the non-finite flag travel with it.
-        NFG_NCCL(nccl().all_reduce(f->d_g, f->d_g, f->n_total, ncclFloat32, ncclSum, c->comm, c->stream));
+        NFG_NCCL(nccl().all_reduce(f->d_g, f->d_g, f->n_total_dev, ncclFloat32, ncclSum, c->comm, c->stream));
         NFG_NCCL(nccl().all_reduce(&f->d_res->loss_sum, &f->d_res->loss_sum, 1, ncclFloat64, ncclSum, c->comm, c->stream));
         NFG_NCCL(nccl().all_reduce(f->d_res->flags, f->d_res->flags, 1, ncclUint32, ncclMax, c->comm, c->stream));
     }
@@ -362,7 +364,7 @@ void device_train_step(nfg_field* f, const float* X, const float* target, int64_
     run_adam(f, lr_now, false);
 }
 
-nfg::FieldShape make_shape(const nfg_grid_config& g, const nfg_mlp_config& m, const std::vector<nfg_level_spec>& lv,
+nfg::FieldShape make_shape(const nfg_grid_config& g, const nfg_mlp_config& m, const std::vector<nfg_level_spec>& lv, const std::vector<uint64_t>& dev_off,
                            const nfg_options& o)
 {
     nfg::FieldShape s{};
@@ -383,10 +385,33 @@ nfg::FieldShape make_shape(const nfg_grid_config& g, const nfg_mlp_config& m, co
         d.res_f = float(lv[l].resolution);
         d.stride = lv[l].resolution + 1u;
         d.dense = uint32_t(lv[l].dense);
-        d.row_off = uint32_t(lv[l].row_offset);
+        d.row_off = uint32_t(dev_off[l]);
         d.len = lv[l].table_len;
     }
     return s;
+}
+
+// Copies a reference-layout range [off, off + n) of one flat buffer between the
+// host and the device layout (levels padded to even rows; see nfg_field_create).
+void copy_ref(nfg_field* f, float* dev, uint64_t off, uint64_t n, float* host, cudaMemcpyKind kind)
+{
+    const uint64_t F = uint64_t(f->gcfg.features), end = off + n;
+    auto seg = [&](uint64_t ref_lo, uint64_t ref_hi, uint64_t dev_lo) {
+        const uint64_t a = std::max(ref_lo, off), b = std::min(ref_hi, end);
+        if (a >= b)
+            return;
+        float* d = dev + dev_lo + (a - ref_lo);
+        float* h = host + (a - off);
+        if (kind == cudaMemcpyHostToDevice)
+            NFG_CUDA(cudaMemcpyAsync(d, h, (b - a) * 4, kind, f->ctx->stream));
+        else
+            NFG_CUDA(cudaMemcpyAsync(h, d, (b - a) * 4, kind, f->ctx->stream));
+    };
+    for (size_t l = 0; l < f->levels.size(); ++l) {
+        const uint64_t lo = f->levels[l].row_offset * F;
+        seg(lo, lo + uint64_t(f->levels[l].table_len) * F, f->dev_row_off[l] * F);
+    }
+    seg(f->n_tab, f->n_total, f->n_tab_dev);
 }
 
 // encode_forward's input validation (grid.hpp:226-229) for host-pointer calls;
@@ -585,15 +610,27 @@ nfg_status nfg_field_create(nfg_ctx* ctx, const nfg_grid_config* grid, const nfg
             f->n_w = nw;
             f->n_b = nb;
             f->n_total = f->n_tab + nw + nb;
-            f->n_alloc = (f->n_total + 63) & ~uint64_t(63);
-            f->shape = make_shape(f->gcfg, f->mcfg, f->levels, f->opts);
+            // Device layout: every level starts on an even row, so x-adjacent
+            // corner pairs {2k, 2k+1} are 16-byte aligned in the fp32 gradient
+            // slab (one vector reduction per pair). Padding rows carry zero
+            // gradients, which the skip-zero Adam group never touches.
+            uint64_t drow = 0;
+            f->dev_row_off.clear();
+            for (const auto& s : f->levels) {
+                f->dev_row_off.push_back(drow);
+                drow += (uint64_t(s.table_len) + 1u) & ~uint64_t(1);
+            }
+            f->n_tab_dev = drow * uint64_t(f->gcfg.features);
+            f->n_total_dev = f->n_tab_dev + nw + nb;
+            f->n_alloc = (f->n_total_dev + 63) & ~uint64_t(63);
+            f->shape = make_shape(f->gcfg, f->mcfg, f->levels, f->dev_row_off, f->opts);
             NFG_CUDA(cudaSetDevice(ctx->device));
             const size_t bytes = f->n_alloc * sizeof(float);
             NFG_CUDA(cudaMalloc(&f->d_p, bytes));
             NFG_CUDA(cudaMalloc(&f->d_g, bytes));
             NFG_CUDA(cudaMalloc(&f->d_m, bytes));
             NFG_CUDA(cudaMalloc(&f->d_v, bytes));
-            NFG_CUDA(cudaMalloc(&f->d_shadow, std::max<uint64_t>(f->n_tab, 1) * sizeof(__half)));
+            NFG_CUDA(cudaMalloc(&f->d_shadow, std::max<uint64_t>(f->n_tab_dev, 1) * sizeof(__half)));
             NFG_CUDA(cudaMalloc(&f->d_levels, sizeof(nfg::LevelDev) * NFG_MAX_LEVELS));
             NFG_CUDA(cudaMalloc(&f->d_res, sizeof(StepResult)));
             NFG_CUDA(cudaMallocHost(&f->h_res, sizeof(StepResult)));
@@ -601,7 +638,7 @@ nfg_status nfg_field_create(nfg_ctx* ctx, const nfg_grid_config* grid, const nfg
                                 cudaMemcpyHostToDevice));
             for (float* p : { f->d_p, f->d_g, f->d_m, f->d_v })
                 NFG_CUDA(cudaMemsetAsync(p, 0, bytes, ctx->stream));
-            NFG_CUDA(cudaMemsetAsync(f->d_shadow, 0, std::max<uint64_t>(f->n_tab, 1) * sizeof(__half), ctx->stream));
+            NFG_CUDA(cudaMemsetAsync(f->d_shadow, 0, std::max<uint64_t>(f->n_tab_dev, 1) * sizeof(__half), ctx->stream));
             NFG_CUDA(cudaStreamSynchronize(ctx->stream));
         } catch (...) {
             nfg_field_destroy(f);
@@ -633,9 +670,9 @@ nfg_status nfg_field_init(nfg_field* f, uint64_t seed)
         nfg::host::init_tables(seed, host.data(), f->n_tab);                         // grid.hpp:158-164
         nfg::host::glorot(f->mcfg, seed + 1, host.data() + f->n_tab, host.data() + f->n_tab + f->n_w);   // model.cpp:34
         cudaStream_t st = f->ctx->stream;
-        NFG_CUDA(cudaMemcpyAsync(f->d_p, host.data(), f->n_total * 4, cudaMemcpyHostToDevice, st));
-        for (float* p : { f->d_g, f->d_m, f->d_v })
+        for (float* p : { f->d_p, f->d_g, f->d_m, f->d_v })
             NFG_CUDA(cudaMemsetAsync(p, 0, f->n_alloc * 4, st));
+        copy_ref(f, f->d_p, 0, f->n_total, host.data(), cudaMemcpyHostToDevice);
         refresh_shadow(f);
         NFG_CUDA(cudaStreamSynchronize(st));
         f->step = 0;
@@ -683,7 +720,7 @@ nfg_status nfg_field_read(nfg_field* f, int32_t which, uint64_t off, uint64_t n,
 {
     return guard([&] {
         require(off + n <= f->n_total, "nfg_field_read: range out of bounds");
-        NFG_CUDA(cudaMemcpyAsync(host, buffer_of(f, which) + off, n * 4, cudaMemcpyDeviceToHost, f->ctx->stream));
+        copy_ref(f, buffer_of(f, which), off, n, host, cudaMemcpyDeviceToHost);
         NFG_CUDA(cudaStreamSynchronize(f->ctx->stream));
     });
 }
@@ -692,7 +729,7 @@ nfg_status nfg_field_write(nfg_field* f, int32_t which, uint64_t off, uint64_t n
 {
     return guard([&] {
         require(off + n <= f->n_total, "nfg_field_write: range out of bounds");
-        NFG_CUDA(cudaMemcpyAsync(buffer_of(f, which) + off, host, n * 4, cudaMemcpyHostToDevice, f->ctx->stream));
+        copy_ref(f, buffer_of(f, which), off, n, const_cast<float*>(host), cudaMemcpyHostToDevice);
         if (which == NFG_BUF_PARAMS && off < f->n_tab)
             refresh_shadow(f);
         NFG_CUDA(cudaStreamSynchronize(f->ctx->stream));
@@ -703,7 +740,7 @@ nfg_status nfg_field_device_buffer(nfg_field* f, int32_t which, float** dev, uin
 {
     return guard([&] {
         *dev = buffer_of(f, which);
-        *count = f->n_total;
+        *count = f->n_total_dev;   // device layout (levels start on even rows)
     });
 }
 
@@ -784,8 +821,8 @@ nfg_status nfg_field_evaluate_device(nfg_field* f, const float* X, int64_t B, fl
         a.X = X;
         a.B = B;
         a.table = table_ptr(f);
-        a.W = f->d_p + f->n_tab;
-        a.b = f->d_p + f->n_tab + f->n_w;
+        a.W = f->d_p + f->n_tab_dev;
+        a.b = f->d_p + f->n_tab_dev + f->n_w;
         a.out = out;
         Span span(f->ctx, 3);
         NFG_CUDA(nfg::launch_infer(f->shape, f->d_levels, nfg::SRC_ENCODE, a, f->ctx->num_sms, f->ctx->stream));
@@ -858,8 +895,8 @@ nfg_status nfg_mlp_forward(nfg_field* f, const float* Y, int64_t B, float* out)
         nfg::InferArgs a{};
         a.Y = dY;
         a.B = B;
-        a.W = f->d_p + f->n_tab;
-        a.b = f->d_p + f->n_tab + f->n_w;
+        a.W = f->d_p + f->n_tab_dev;
+        a.b = f->d_p + f->n_tab_dev + f->n_w;
         a.out = dO;
         NFG_CUDA(nfg::launch_infer(f->shape, nullptr, nfg::SRC_LOAD_Y, a, c->num_sms, c->stream));
         c->launches++;
@@ -882,11 +919,11 @@ nfg_status nfg_mlp_backward(nfg_field* f, const float* Y, int64_t B, const float
         a.dout = dO;
         a.B = B;
         a.inv_count = 1.0f;
-        a.W = f->d_p + f->n_tab;
-        a.b = f->d_p + f->n_tab + f->n_w;
+        a.W = f->d_p + f->n_tab_dev;
+        a.b = f->d_p + f->n_tab_dev + f->n_w;
         a.dY = ddY;
-        a.gW = f->d_g + f->n_tab;
-        a.gb = f->d_g + f->n_tab + f->n_w;
+        a.gW = f->d_g + f->n_tab_dev;
+        a.gb = f->d_g + f->n_tab_dev + f->n_w;
         a.scratch = scratch_of(f);
         NFG_CUDA(nfg::launch_train(f->shape, nullptr, nfg::SRC_LOAD_Y, nfg::GRAD_DOUT, nfg::SINK_STORE, a, c->num_sms,
                                    c->stream, nullptr));

@@ -32,7 +32,20 @@ constexpr int IW = 4;     // warps per inference CTA
 
 __host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
 
-template <int IN_STEPS, int NH>
+// Staged-gather geometry of the fused kernel: per pass, STS k16 steps of
+// input columns (4 (sample, col-pair) items per step per thread) with NE
+// corner elements of SB bytes each, at most 256 B of slots per thread.
+template <int SRC, int D, int F, typename TT, int IN_STEPS>
+struct StageGeo {
+    static constexpr int NE = PairElems<D, F>::NE;
+    static constexpr int SB = Stage<F, TT>::SB;
+    static constexpr int PER_STEP = 4 * NE * SB;
+    static constexpr int STS_RAW = 256 / PER_STEP;
+    static constexpr int STS = STS_RAW < 1 ? 1 : (STS_RAW > IN_STEPS ? IN_STEPS : STS_RAW);
+    static constexpr int BYTES = SRC == SRC_ENCODE ? TW * 32 * STS * PER_STEP : 0;
+};
+
+template <int IN_STEPS, int NH, int STAGE_BYTES = 0>
 struct TrainSmem {
     using Lay = WLayout<IN_STEPS, NH>;
     static constexpr int INS = Lay::INS;
@@ -44,7 +57,8 @@ struct TrainSmem {
     static constexpr int DZO_OFF = DZH_OFF + NH * TS * HS * 2;
     static constexpr int DB_OFF = DZO_OFF + TS * OS * 2;
     static constexpr int RED_OFF = DB_OFF + (NH + 1) * H * 4;
-    static constexpr int BYTES = RED_OFF + 4 * TW * 4;
+    static constexpr int STAGE_OFF = align16(RED_OFF + 4 * TW * 4);
+    static constexpr int BYTES = STAGE_OFF + STAGE_BYTES;
 };
 
 template <int IN_STEPS, int NH>
@@ -53,6 +67,29 @@ struct InferSmem {
     static constexpr int LV_OFF = align16(Lay::BYTES);
     static constexpr int BYTES = LV_OFF + align16(int(sizeof(LevelDev)) * NFG_MAX_LEVELS);
 };
+
+// Phase timing of k_train (build with -DNFG_PHASE_TIMING; a.phase_clk != null):
+// per-warp clock64 deltas of encode / fwd / loss+barrier / bwd / scatter /
+// barrier / dW / barrier, summed into a.phase_clk[8].
+#ifdef NFG_PHASE_TIMING
+#define NFG_PT_DECL unsigned long long pt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pt_t = 0;
+#define NFG_PT_START() pt_t = clock64();
+#define NFG_PT(i)                                  \
+    {                                              \
+        const unsigned long long n_ = clock64();   \
+        pt_acc[i] += n_ - pt_t;                    \
+        pt_t = n_;                                 \
+    }
+#define NFG_PT_FLUSH()                                                 \
+    if (a.phase_clk && lane == 0)                                      \
+        for (int i_ = 0; i_ < 8; ++i_)                                 \
+            atomicAdd(a.phase_clk + i_, pt_acc[i_]);
+#else
+#define NFG_PT_DECL
+#define NFG_PT_START()
+#define NFG_PT(i)
+#define NFG_PT_FLUSH()
+#endif
 
 __device__ __forceinline__ bool sane(float v) { return fabsf(v) <= 1e30f; }   // false for NaN/inf/huge
 
@@ -101,11 +138,15 @@ __device__ __forceinline__ void load_x(float* x, const float* __restrict__ X, in
 }
 
 template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IN_STEPS, int NH>
-__global__ void __launch_bounds__(TW * 32, 1)
+#ifndef NFG_TRAIN_MIN_BLOCKS
+#define NFG_TRAIN_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(TW * 32, NFG_TRAIN_MIN_BLOCKS)
 k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ levels)
 {
     using Lay = WLayout<IN_STEPS, NH>;
-    using SM = TrainSmem<IN_STEPS, NH>;
+    using SG = StageGeo<SRC, D, F, TT, IN_STEPS>;
+    using SM = TrainSmem<IN_STEPS, NH, SG::BYTES>;
     extern __shared__ __align__(16) unsigned char sm[];
     __half* ws = reinterpret_cast<__half*>(sm);
     float* bs = reinterpret_cast<float*>(sm + Lay::HALVES * 2);
@@ -152,9 +193,11 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         dwo[e >> 2][e & 3] = 0.0f;
 
     bool bad = false;
+    NFG_PT_DECL
     const int64_t ntiles = (a.B + TS - 1) / TS;
     const int r0 = 16 * warp;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        NFG_PT_START();
         const int64_t sg = tile * TS + r0 + g, sg8 = sg + 8;
         const bool vg = sg < a.B, vg8 = sg8 < a.B;
         float xg[D], xg8[D];
@@ -164,8 +207,49 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         }
         // ---- encode / load inputs -------------------------------------
         uint32_t afr[IN_STEPS][4];
-        input_frags<SRC, D, F, TT, IN_STEPS>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
+        if (SRC == SRC_ENCODE) {
+            // all corner loads of SG::STS k16 steps in flight at once (cp.async)
+            const TT* tab = static_cast<const TT*>(a.table);
+            unsigned char* stage = sm + SM::STAGE_OFF;
+            constexpr int SLOT = TW * 32 * SG::SB;   // stride between a thread's slots
+#pragma unroll
+            for (int s0 = 0; s0 < IN_STEPS; s0 += SG::STS) {
+#pragma unroll
+                for (int sl = 0; sl < SG::STS; ++sl)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
+                        const int p = (sl * 2 + h) * 2;
+                        unsigned char* base = stage + tid * SG::SB;
+                        if (s0 + sl < IN_STEPS && vg)
+                            gather_issue<D, F, TT>(s.grid, lvs, xg, col, tab, base + p * SG::NE * SLOT, SLOT);
+                        if (s0 + sl < IN_STEPS && vg8)
+                            gather_issue<D, F, TT>(s.grid, lvs, xg8, col, tab, base + (p + 1) * SG::NE * SLOT, SLOT);
+                    }
+                cp_async_wait_all();
+#pragma unroll
+                for (int sl = 0; sl < SG::STS; ++sl)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (s0 + sl >= IN_STEPS)
+                            continue;
+                        const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
+                        const int p = (sl * 2 + h) * 2;
+                        const unsigned char* base = stage + tid * SG::SB;
+                        const float2 e0 = vg ? gather_blend<D, F, TT>(s.grid, lvs, xg, col, base + p * SG::NE * SLOT, SLOT)
+                                             : make_float2(0.f, 0.f);
+                        const float2 e8 = vg8 ? gather_blend<D, F, TT>(s.grid, lvs, xg8, col,
+                                                                        base + (p + 1) * SG::NE * SLOT, SLOT)
+                                              : make_float2(0.f, 0.f);
+                        afr[s0 + sl][2 * h] = pack_half2(e0.x, e0.y);
+                        afr[s0 + sl][2 * h + 1] = pack_half2(e8.x, e8.y);
+                    }
+            }
+        } else {
+            input_frags<SRC, D, F, TT, IN_STEPS>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
+        }
         store_a<IN_STEPS>(afr, act0, SM::INS, r0, lane);
+        NFG_PT(0);
 
         // ---- MLP forward --------------------------------------------------
         float acc[HT][4];
@@ -184,6 +268,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         }
         float ao[2][4];
         layer_fwd<4, 2>(ah, Wos, HS, ao, lane);
+        NFG_PT(1);
 
         // ---- output activation, loss, dLoss/dpred --------------------------
         float term = 0.0f, mx = 0.0f;
@@ -223,6 +308,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 atomicAdd(a.scratch.loss_sum, double(term));
         }
         __syncthreads();
+        NFG_PT(2);
         float tmax = 0.0f;
 #pragma unroll
         for (int w = 0; w < TW; ++w)
@@ -287,6 +373,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         float ay[2 * IN_STEPS][4];
         layer_bwd<4, 2 * IN_STEPS>(ah, W0s, SM::INS, ay, lane);
 
+        NFG_PT(3);
         // ---- dY -> encode backward / store -------------------------------------
         const float dysc = isc * a.inv_count;
 #pragma unroll
@@ -314,7 +401,9 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 }
             }
         }
+        NFG_PT(4);
         __syncthreads();
+        NFG_PT(5);
 
         // ---- dW = dz^T act over the tile's 128 samples ------------------------
 #pragma unroll
@@ -352,9 +441,12 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 dwo[1][e] = fmaf(c1[e], isc, dwo[1][e]);
             }
         }
+        NFG_PT(6);
         __syncthreads();
+        NFG_PT(7);
     }
 
+    NFG_PT_FLUSH();
     // ---- flush per-CTA dW / db (x 1/count) ----------------------------------
     const float ic = a.inv_count;
     auto flush = [&](const float (&cq)[2][4], int mt, int np, int out_k, int in_k, size_t woff) {

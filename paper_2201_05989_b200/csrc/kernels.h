@@ -50,6 +50,7 @@ struct TrainArgs {
     float* gb;
     float* pred;             // optional n_out x B
     StepScratch scratch;
+    unsigned long long* phase_clk;   // NFG_PHASE_TIMING builds only
 };
 
 struct InferArgs {

@@ -11,7 +11,7 @@ template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IS, int NH
 cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& a, int num_sms, cudaStream_t st,
                       int* grid_used)
 {
-    using SM = TrainSmem<IS, NH>;
+    using SM = TrainSmem<IS, NH, StageGeo<SRC, D, F, TT, IS>::BYTES>;
     auto k = k_train<SRC, GRAD, SINK, D, F, TT, IS, NH>;
     static int per_sm = -1;   // resolved once per instantiation
     if (per_sm < 0) {
