@@ -55,8 +55,10 @@ k_encode_fwd(const FieldShape s, const LevelDev* __restrict__ levels, const floa
 template <int D, int F>
 __global__ void __launch_bounds__(256)
 k_encode_bwd(const FieldShape s, const LevelDev* __restrict__ levels, const float* __restrict__ X, int64_t B,
-             const float* __restrict__ dY, float* __restrict__ grads)
+             const float* __restrict__ dY, float* __restrict__ grads, const unsigned int* flags)
 {
+    if (flags && flags[3] != 0u)
+        return;   // invalid input of this step (k_validate)
     __shared__ LevelDev lvs[NFG_MAX_LEVELS];
     for (int i = threadIdx.x; i < s.grid.L; i += blockDim.x)
         lvs[i] = levels[i];
@@ -105,10 +107,10 @@ static cudaError_t enc_fwd(const FieldShape& s, const LevelDev* lv, const float*
 
 template <int D, int F>
 static cudaError_t enc_bwd(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B, const float* dY,
-                           float* grads, cudaStream_t st)
+                           float* grads, const unsigned int* flags, cudaStream_t st)
 {
     const int64_t blocks = (B + 255) / 256;
-    k_encode_bwd<D, F><<<unsigned(blocks), 256, 0, st>>>(s, lv, X, B, dY, grads);
+    k_encode_bwd<D, F><<<unsigned(blocks), 256, 0, st>>>(s, lv, X, B, dY, grads, flags);
     return cudaGetLastError();
 }
 
@@ -128,17 +130,55 @@ cudaError_t launch_encode_fwd_lv(const FieldShape& s, const LevelDev* lv, const 
 }
 
 cudaError_t launch_encode_bwd_lv(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
-                                 const float* dY, float* grads, cudaStream_t st)
+                                 const float* dY, float* grads, cudaStream_t st, const unsigned int* flags)
 {
     if (B <= 0)
         return cudaSuccess;
 #define NFG_ENC_B(D_, F_)                                                                                   \
     if (s.grid.d == D_ && s.grid.F == F_)                                                                    \
-        return enc_bwd<D_, F_>(s, lv, X, B, dY, grads, st);
+        return enc_bwd<D_, F_>(s, lv, X, B, dY, grads, flags, st);
     NFG_ENC_B(2, 1) NFG_ENC_B(2, 2) NFG_ENC_B(2, 4) NFG_ENC_B(2, 8)
     NFG_ENC_B(3, 1) NFG_ENC_B(3, 2) NFG_ENC_B(3, 4) NFG_ENC_B(3, 8)
 #undef NFG_ENC_B
     return cudaErrorNotSupported;
+}
+
+// ---- input validation (grid.hpp:226-229) on the device -------------------------
+// flags[3] |= 1 (non-finite) / 2 (outside [-1e-6, 1+1e-6]); flags[1] |= 1 so the
+// step aborts before any state changes (k_train and Adam test it first).
+__global__ void __launch_bounds__(256) k_validate(const float* __restrict__ X, int64_t n, unsigned int* flags)
+{
+    unsigned bad = 0;
+    const int64_t n4 = (reinterpret_cast<uintptr_t>(X) & 15u) ? 0 : n / 4;
+    const float lo = -1e-6f, hi = 1.0f + 1e-6f;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+        const float4 v = reinterpret_cast<const float4*>(X)[i];
+        const float e[4] = { v.x, v.y, v.z, v.w };
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            bad |= finite_f(e[k]) ? 0u : 1u;
+            bad |= (e[k] < lo || e[k] > hi) ? 2u : 0u;
+        }
+    }
+    for (int64_t i = 4 * n4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        bad |= finite_f(X[i]) ? 0u : 1u;
+        bad |= (X[i] < lo || X[i] > hi) ? 2u : 0u;
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && (threadIdx.x & 31) == 0) {
+        atomicOr(&flags[3], bad);
+        atomicOr(&flags[1], 1u);
+    }
+}
+
+cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cudaStream_t st)
+{
+    if (n <= 0)
+        return cudaSuccess;
+    const unsigned blocks = unsigned(std::min<int64_t>((n / 4 + 255) / 256 + 1, 148 * 4));
+    k_validate<<<blocks, 256, 0, st>>>(X, n, flags);
+    return cudaGetLastError();
 }
 
 // ---- Adam (adam.hpp:78-122) -------------------------------------------------

@@ -248,6 +248,10 @@ void fetch_result(nfg_field* f)
 
 void raise_if_aborted(nfg_field* f)
 {
+    if (f->h_res->flags[3] & 1u)
+        throw std::invalid_argument("encode_forward: non-finite input");
+    if (f->h_res->flags[3] & 2u)
+        throw std::invalid_argument("encode_forward: input outside [0,1]^d");
     if (f->h_res->flags[1]) {
         const unsigned g = f->h_res->flags[2] == 0xffffffffu ? 0u : f->h_res->flags[2] - 1u;
         throw Fail{ NFG_ENONFINITE, std::string("adam_step: non-finite gradient in group '") + group_name(g) + "'" };
@@ -308,6 +312,10 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
     require(B_local >= 0 && B_global >= B_local, "train_step: invalid batch size");
     nfg_ctx* c = f->ctx;
     reset_scratch(f);
+    // encode_forward's input checks (grid.hpp:226-229), on the device: an
+    // invalid batch aborts every later kernel of the step before any update
+    NFG_CUDA(nfg::launch_validate(X, B_local * f->gcfg.dims, f->d_res->flags, c->stream));
+    c->launches++;
     const double count = double(B_global) * double(f->mcfg.output_width);
     nfg::TrainArgs a{};
     a.X = X;
@@ -340,7 +348,8 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
             a.dY = dY;
             NFG_CUDA(nfg::launch_train(f->shape, nullptr, nfg::SRC_LOAD_Y, nfg::GRAD_LOSS, nfg::SINK_STORE, a,
                                        c->num_sms, c->stream, nullptr));
-            NFG_CUDA(nfg::launch_encode_bwd_lv(f->shape, f->d_levels, X, B_local, dY, f->d_g, c->stream));
+            NFG_CUDA(nfg::launch_encode_bwd_lv(f->shape, f->d_levels, X, B_local, dY, f->d_g, c->stream,
+                                               f->d_res->flags));
             c->launches += 3;
         }
     }
@@ -760,7 +769,6 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
     return guard([&] {
         nfg_ctx* c = f->ctx;
         const int d = f->gcfg.dims, no = f->mcfg.output_width;
-        validate_inputs(X, B, d);
         const float* dX = stage(c->s0, X, size_t(B) * d, c->stream);
         const float* dT = stage(c->s1, target, size_t(B) * no, c->stream);
         const uint64_t before = f->step;
@@ -781,11 +789,13 @@ nfg_status nfg_field_gradients(nfg_field* f, const float* X, const float* target
 {
     return guard([&] {
         nfg_ctx* c = f->ctx;
-        validate_inputs(X, B, f->gcfg.dims);
+
         const float* dX = stage(c->s0, X, size_t(B) * f->gcfg.dims, c->stream);
         const float* dT = stage(c->s1, target, size_t(B) * f->mcfg.output_width, c->stream);
         device_backward(f, dX, dT, B, B * c->nranks, loss_kind);
         fetch_result(f);
+        if (f->h_res->flags[3])
+            raise_if_aborted(f);
         const double count = double(B) * c->nranks * f->mcfg.output_width;
         if (loss)
             *loss = count > 0 ? float(f->h_res->loss_sum / count) : 0.0f;

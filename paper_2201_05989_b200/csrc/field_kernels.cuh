@@ -159,6 +159,8 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     float* red = reinterpret_cast<float*>(sm + SM::RED_OFF);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    if (a.scratch.flags[3] != 0u)
+        return;   // invalid input (k_validate): the reference throws before any update
     const MlpShape msh{ s.in_real, s.n_out, s.sigmoid };
     load_weights<IN_STEPS, NH>(ws, bs, a.W, a.b, msh);
     if (SRC == SRC_ENCODE)

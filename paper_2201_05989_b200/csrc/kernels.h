@@ -73,7 +73,7 @@ cudaError_t launch_infer(const FieldShape& s, const LevelDev* lv, int src, const
 cudaError_t launch_encode_fwd_lv(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
                                  const void* table, float* Y, uint32_t* rows, float* weights, cudaStream_t st);
 cudaError_t launch_encode_bwd_lv(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
-                                 const float* dY, float* grads, cudaStream_t st);
+                                 const float* dY, float* grads, cudaStream_t st, const unsigned int* flags = nullptr);
 
 struct AdamArgs {
     float* p;
@@ -86,6 +86,7 @@ struct AdamArgs {
     unsigned int* flags;
 };
 cudaError_t launch_adam(const AdamArgs& a, bool force_check, int num_sms, cudaStream_t st);
+cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cudaStream_t st);
 cudaError_t launch_shadow(const float* p, __half* shadow, uint64_t n, cudaStream_t st);
 cudaError_t launch_loss(int kind, const float* pred, const float* target, int64_t n, float count, float* dpred,
                         double* loss_sum, cudaStream_t st);
