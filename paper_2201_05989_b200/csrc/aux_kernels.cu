@@ -220,6 +220,22 @@ __device__ __forceinline__ void adam_one(const AdamArgs& a, uint64_t i, float& p
     wrote = true;
 }
 
+__device__ __forceinline__ float4 ld4_hint(const float* p, uint64_t pol)
+{
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ void st4_hint(float* p, float4 v, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
+}
+
 __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
 {
     if (a.flags[1] != 0u)
@@ -227,31 +243,45 @@ __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
     const uint64_t n = a.n_tab + a.n_w + a.n_b;
     const uint64_t n4 = n / 4;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    // L2 policy: p, m, v stream through once per step (evict-first); the zeroed
+    // gradients and the fp16 table shadow are what the next step's fused kernel
+    // hits with atomics and gathers (73 MB at config 2), so they are written
+    // evict-last to stay L2-resident across the step boundary.
+    uint64_t pol_stream, pol_keep;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
     for (uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride) {
-        float4 P = reinterpret_cast<const float4*>(a.p)[q];
-        const float4 G = reinterpret_cast<const float4*>(a.g)[q];
+        const float4 G = ld4_hint(a.g + 4 * q, pol_stream);
         const bool any = G.x != 0.0f || G.y != 0.0f || G.z != 0.0f || G.w != 0.0f;
         const uint64_t i0 = 4 * q;
         if (!any && i0 + 3 < a.n_tab)
             continue;   // whole quad skipped: nothing to read or write
-        float4 M = reinterpret_cast<const float4*>(a.m)[q];
-        float4 V = reinterpret_cast<const float4*>(a.v)[q];
+        const float4 P = ld4_hint(a.p + 4 * q, pol_stream);
+        const float4 M = ld4_hint(a.m + 4 * q, pol_stream);
+        const float4 V = ld4_hint(a.v + 4 * q, pol_stream);
         float pg[4] = { P.x, P.y, P.z, P.w }, gq[4] = { G.x, G.y, G.z, G.w };
         float mq[4] = { M.x, M.y, M.z, M.w }, vq[4] = { V.x, V.y, V.z, V.w };
         bool w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e)
             adam_one(a, i0 + e, pg[e], gq[e], mq[e], vq[e], w[e]);
-        reinterpret_cast<float4*>(a.p)[q] = make_float4(pg[0], pg[1], pg[2], pg[3]);
-        reinterpret_cast<float4*>(a.m)[q] = make_float4(mq[0], mq[1], mq[2], mq[3]);
-        reinterpret_cast<float4*>(a.v)[q] = make_float4(vq[0], vq[1], vq[2], vq[3]);
+        st4_hint(a.p + 4 * q, make_float4(pg[0], pg[1], pg[2], pg[3]), pol_stream);
+        st4_hint(a.m + 4 * q, make_float4(mq[0], mq[1], mq[2], mq[3]), pol_stream);
+        st4_hint(a.v + 4 * q, make_float4(vq[0], vq[1], vq[2], vq[3]), pol_stream);
         if (any)
-            reinterpret_cast<float4*>(a.g)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            st4_hint(a.g + 4 * q, make_float4(0.f, 0.f, 0.f, 0.f), pol_keep);
         if (a.shadow && i0 < a.n_tab) {
+            if (i0 + 3 < a.n_tab && w[0] && w[1] && w[2] && w[3]) {
+                const uint2 h = make_uint2(pack_half2(pg[0], pg[1]), pack_half2(pg[2], pg[3]));
+                asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(a.shadow + i0), "r"(h.x),
+                             "r"(h.y), "l"(pol_keep)
+                             : "memory");
+            } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (w[e] && i0 + e < a.n_tab)
-                    a.shadow[i0 + e] = __float2half_rn(pg[e]);
+                for (int e = 0; e < 4; ++e)
+                    if (w[e] && i0 + e < a.n_tab)
+                        a.shadow[i0 + e] = __float2half_rn(pg[e]);
+            }
         }
     }
     // tail
