@@ -1,7 +1,12 @@
+# ncu evidence for the bench workload (one GPU). Usage: bash tools/gpu_ncu.sh <tag>
 cd $GRAFT_REPO_ROOT
+TAG=${1:-r1}
 mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 2 --no-cpu-baseline --infer-b 4194304 > gpurun_out/launches_bench.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_train -s 2 -c 1 -o gpurun_out/prof_train python bench.py --steps 2 --warmup 2 --no-cpu-baseline --infer-b 1048576 > gpurun_out/prof_train.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_adam -s 4 -c 1 -o gpurun_out/prof_adam python bench.py --steps 2 --warmup 2 --no-cpu-baseline --infer-b 1048576 > gpurun_out/prof_adam.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_infer -s 2 -c 1 -o gpurun_out/prof_infer python bench.py --steps 2 --warmup 2 --no-cpu-baseline --infer-b 4194304 > gpurun_out/prof_infer.log 2>&1
+# launch list of this library's kernels (mangled names start with _ZN3nfg)
+ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base mangled -k regex:_ZN3nfg -c 60 --csv \
+    --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline --infer-b 4194304 > gpurun_out/launches_$TAG.log 2>&1
+for K in k_train k_adam k_infer; do
+  ncu --set full --clock-control none --import-source on -k $K -s 3 -c 1 -o gpurun_out/prof_${K}_$TAG \
+      python bench.py --steps 3 --warmup 3 --no-cpu-baseline --infer-b 4194304 > gpurun_out/prof_${K}_$TAG.log 2>&1
+done
 ls -la gpurun_out
