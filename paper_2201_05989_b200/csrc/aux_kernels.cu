@@ -186,6 +186,15 @@ cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cuda
 // forced): exact isfinite scan; records the first bad group and aborts.
 __global__ void __launch_bounds__(256) k_adam_check(const AdamArgs a, int force)
 {
+    const uint64_t nn = a.n_tab + a.n_w + a.n_b;
+    if (a.restore_on_invalid && a.flags[3] != 0u) {
+        // invalid batch detected inside the speculative fused kernel: the slab
+        // was all-zero before the step, so zeroing restores it exactly
+        for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nn;
+             i += uint64_t(gridDim.x) * blockDim.x)
+            a.g[i] = 0.0f;
+        return;
+    }
     if (!force && a.flags[0] == 0u)
         return;
     const uint64_t n = a.n_tab + a.n_w + a.n_b;

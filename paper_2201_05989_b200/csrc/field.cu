@@ -1,6 +1,7 @@
 // field.cu — the C ABI (include/nfg.h): contexts, the device-resident
 // FieldModel and the component entry points. Host orchestration only; the
 // math lives in the kernels.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -132,6 +133,11 @@ struct nfg_ctx {
     int rank = 0, nranks = 1;
     DevBuf s0, s1, s2, s3;   // staging for host-pointer calls
     double* d_red = nullptr;
+    // streamed inputs: H2D chunks on a copy stream, each followed by a
+    // stream memory write of its ready flag (copy engine + front end only)
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_order = nullptr;
+    CUresult (*write_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
     // phase timing (nfg_ctx_set_profiling)
     bool profile = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -211,7 +217,15 @@ struct nfg_field {
     StepResult* h_res = nullptr;   // pinned
     uint64_t step = 0;
     uint64_t pending_steps = 0;    // device steps not yet checked (async API)
+    // The gradient slab is all-zero (after init / a completed Adam step). Then a
+    // step may validate its inputs speculatively inside the fused kernel and
+    // undo by re-zeroing; otherwise k_validate runs first.
+    bool grads_clean = true;
+    unsigned int* d_ready = nullptr;   // NFG_MAX_CHUNKS chunk-ready flags
+    unsigned int epoch = 0;
 };
+
+#define NFG_MAX_CHUNKS 64
 
 namespace {
 
@@ -298,6 +312,7 @@ void run_adam(nfg_field* f, float lr_now, bool force_check)
     a.l2 = s.l2;
     a.lr = s.lr;
     a.flags = f->d_res->flags;
+    a.restore_on_invalid = f->grads_clean ? 1 : 0;
     NFG_CUDA(nfg::launch_adam(a, force_check, f->ctx->num_sms, f->ctx->stream));
     f->ctx->launches += 2;
     f->step = next;
@@ -305,17 +320,29 @@ void run_adam(nfg_field* f, float lr_now, bool force_check)
 
 // Forward + loss + backward: gradients ACCUMULATE into the grad slab (the
 // reference's mlp_backward / encode_backward semantics); no optimizer step.
+struct Streamed {
+    const unsigned int* ready = nullptr;
+    unsigned int epoch = 0;
+    int64_t chunk = 0;
+};
+
 void device_backward(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
-                     int loss_kind)
+                     int loss_kind, const Streamed& sm = Streamed(), bool allow_speculative = true)
 {
     require(loss_kind >= 0 && loss_kind <= 2, "train_step: unknown loss");
     require(B_local >= 0 && B_global >= B_local, "train_step: invalid batch size");
     nfg_ctx* c = f->ctx;
     reset_scratch(f);
-    // encode_forward's input checks (grid.hpp:226-229), on the device: an
-    // invalid batch aborts every later kernel of the step before any update
-    NFG_CUDA(nfg::launch_validate(X, B_local * f->gcfg.dims, f->d_res->flags, c->stream));
-    c->launches++;
+    // encode_forward's input checks (grid.hpp:226-229). With a clean gradient
+    // slab the fused kernel checks its own inputs and Adam's check kernel
+    // undoes the step on failure (re-zeroing); otherwise a separate k_validate
+    // aborts every later kernel before any update.
+    const bool speculative = allow_speculative && f->grads_clean && f->opts.fused_train;
+    require(speculative || sm.ready == nullptr, "streamed inputs need the speculative fused path");
+    if (!speculative) {
+        NFG_CUDA(nfg::launch_validate(X, B_local * f->gcfg.dims, f->d_res->flags, c->stream));
+        c->launches++;
+    }
     const double count = double(B_global) * double(f->mcfg.output_width);
     nfg::TrainArgs a{};
     a.X = X;
@@ -330,6 +357,10 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
     a.gW = f->d_g + f->n_tab_dev;
     a.gb = f->d_g + f->n_tab_dev + f->n_w;
     a.scratch = scratch_of(f);
+    a.validate = speculative ? 1 : 0;
+    a.ready = sm.ready;
+    a.epoch = sm.epoch;
+    a.chunk = sm.chunk;
     if (c->profile)
         c->prof_steps++;
     if (B_local > 0) {
@@ -365,9 +396,9 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
 }
 
 void device_train_step(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
-                       int loss_kind, int64_t step)
+                       int loss_kind, int64_t step, const Streamed& sm = Streamed())
 {
-    device_backward(f, X, target, B_local, B_global, loss_kind);
+    device_backward(f, X, target, B_local, B_global, loss_kind, sm);
     const float lr_now = float(nfg::host::lr_at(f->milestones, f->factor, f->hyper.lr, step));
     Span span(f->ctx, 1);
     run_adam(f, lr_now, false);
@@ -468,6 +499,20 @@ nfg_status nfg_ctx_create(int device, nfg_ctx** out)
             c->device = device;
             NFG_CUDA(cudaSetDevice(device));
             NFG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            NFG_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+            NFG_CUDA(cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming));
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess && fn) {
+                c->write_value32 = reinterpret_cast<decltype(c->write_value32)>(fn);
+                unsigned int* probe = nullptr;   // stream memory ops usable on this device?
+                NFG_CUDA(cudaMalloc(&probe, 4));
+                if (c->write_value32(c->copy_stream, CUdeviceptr(probe), 1u, 0) != CUDA_SUCCESS ||
+                    cudaStreamSynchronize(c->copy_stream) != cudaSuccess)
+                    c->write_value32 = nullptr;
+                cudaFree(probe);
+            }
             NFG_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
         } catch (...) {
             delete c;
@@ -492,6 +537,10 @@ nfg_status nfg_ctx_destroy(nfg_ctx* c)
             cudaEventDestroy(e);
         if (c->stream)
             cudaStreamDestroy(c->stream);
+        if (c->copy_stream)
+            cudaStreamDestroy(c->copy_stream);
+        if (c->ev_order)
+            cudaEventDestroy(c->ev_order);
         delete c;
     });
 }
@@ -642,6 +691,8 @@ nfg_status nfg_field_create(nfg_ctx* ctx, const nfg_grid_config* grid, const nfg
             NFG_CUDA(cudaMalloc(&f->d_shadow, std::max<uint64_t>(f->n_tab_dev, 1) * sizeof(__half)));
             NFG_CUDA(cudaMalloc(&f->d_levels, sizeof(nfg::LevelDev) * NFG_MAX_LEVELS));
             NFG_CUDA(cudaMalloc(&f->d_res, sizeof(StepResult)));
+            NFG_CUDA(cudaMalloc(&f->d_ready, NFG_MAX_CHUNKS * sizeof(unsigned int)));
+            NFG_CUDA(cudaMemset(f->d_ready, 0, NFG_MAX_CHUNKS * sizeof(unsigned int)));
             NFG_CUDA(cudaMallocHost(&f->h_res, sizeof(StepResult)));
             NFG_CUDA(cudaMemcpy(f->d_levels, f->shape.grid.lv, sizeof(nfg::LevelDev) * NFG_MAX_LEVELS,
                                 cudaMemcpyHostToDevice));
@@ -663,7 +714,7 @@ nfg_status nfg_field_destroy(nfg_field* f)
         if (!f)
             return;
         for (void* p : { (void*)f->d_p, (void*)f->d_g, (void*)f->d_m, (void*)f->d_v, (void*)f->d_shadow,
-                         (void*)f->d_levels, (void*)f->d_res })
+                         (void*)f->d_levels, (void*)f->d_res, (void*)f->d_ready })
             if (p)
                 cudaFree(p);
         if (f->h_res)
@@ -685,6 +736,7 @@ nfg_status nfg_field_init(nfg_field* f, uint64_t seed)
         refresh_shadow(f);
         NFG_CUDA(cudaStreamSynchronize(st));
         f->step = 0;
+        f->grads_clean = true;
     });
 }
 
@@ -739,6 +791,8 @@ nfg_status nfg_field_write(nfg_field* f, int32_t which, uint64_t off, uint64_t n
     return guard([&] {
         require(off + n <= f->n_total, "nfg_field_write: range out of bounds");
         copy_ref(f, buffer_of(f, which), off, n, const_cast<float*>(host), cudaMemcpyHostToDevice);
+        if (which == NFG_BUF_GRADS)
+            f->grads_clean = false;
         if (which == NFG_BUF_PARAMS && off < f->n_tab)
             refresh_shadow(f);
         NFG_CUDA(cudaStreamSynchronize(f->ctx->stream));
@@ -769,15 +823,50 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
     return guard([&] {
         nfg_ctx* c = f->ctx;
         const int d = f->gcfg.dims, no = f->mcfg.output_width;
-        const float* dX = stage(c->s0, X, size_t(B) * d, c->stream);
-        const float* dT = stage(c->s1, target, size_t(B) * no, c->stream);
         const uint64_t before = f->step;
-        device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step);
+        const bool was_clean = f->grads_clean;
+        if (f->grads_clean && f->opts.fused_train && c->write_value32 && B >= (int64_t(1) << 15)) {
+            // Overlap the H2D of the batch with the step: the fused kernel is
+            // launched first and waits per tile for its chunk's ready flag,
+            // which the copy stream writes after each chunk lands.
+            float* dX = static_cast<float*>(c->s0.get(size_t(B) * d * 4));
+            float* dT = static_cast<float*>(c->s1.get(size_t(B) * no * 4));
+            const int64_t chunk = std::max<int64_t>((B / 16 + 255) / 256 * 256, (B + NFG_MAX_CHUNKS - 1) / NFG_MAX_CHUNKS);
+            const int64_t nchunks = (B + chunk - 1) / chunk;
+            const unsigned int epoch = ++f->epoch;
+            NFG_CUDA(cudaEventRecord(c->ev_order, c->stream));        // staging buffers free
+            NFG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_order, 0));
+            device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step, Streamed{ f->d_ready, epoch, chunk });
+            int64_t k = 0;
+            try {
+                for (; k < nchunks; ++k) {
+                    const int64_t s0 = k * chunk, n = std::min(chunk, B - s0);
+                    NFG_CUDA(cudaMemcpyAsync(dX + s0 * d, X + s0 * d, size_t(n) * d * 4, cudaMemcpyHostToDevice,
+                                             c->copy_stream));
+                    NFG_CUDA(cudaMemcpyAsync(dT + s0 * no, target + s0 * no, size_t(n) * no * 4,
+                                             cudaMemcpyHostToDevice, c->copy_stream));
+                    if (c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0) != CUDA_SUCCESS)
+                        throw Fail{ NFG_ECUDA, "cuStreamWriteValue32 failed" };
+                }
+            } catch (...) {
+                for (; k < nchunks; ++k)   // never leave the kernel waiting
+                    c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0);
+                throw;
+            }
+        } else {
+            const float* dX = stage(c->s0, X, size_t(B) * d, c->stream);
+            const float* dT = stage(c->s1, target, size_t(B) * no, c->stream);
+            device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step);
+        }
         fetch_result(f);
         if (f->h_res->flags[1]) {
             f->step = before;   // the reference throws before incrementing (adam.hpp:86-92)
+            // invalid input on a clean slab was undone by re-zeroing; a
+            // non-finite gradient leaves the accumulated gradients in place
+            f->grads_clean = was_clean && (f->h_res->flags[3] != 0);
             raise_if_aborted(f);
         }
+        f->grads_clean = true;   // Adam zeroed every gradient (adam.hpp:118-120)
         const double count = double(B) * c->nranks * no;
         if (loss)
             *loss = count > 0 ? float(f->h_res->loss_sum / count) : 0.0f;
@@ -792,7 +881,8 @@ nfg_status nfg_field_gradients(nfg_field* f, const float* X, const float* target
 
         const float* dX = stage(c->s0, X, size_t(B) * f->gcfg.dims, c->stream);
         const float* dT = stage(c->s1, target, size_t(B) * f->mcfg.output_width, c->stream);
-        device_backward(f, dX, dT, B, B * c->nranks, loss_kind);
+        device_backward(f, dX, dT, B, B * c->nranks, loss_kind, Streamed(), false);
+        f->grads_clean = false;
         fetch_result(f);
         if (f->h_res->flags[3])
             raise_if_aborted(f);
@@ -809,6 +899,7 @@ nfg_status nfg_field_train_step_device(nfg_field* f, const float* X, const float
         (void)loss_dev;
         device_train_step(f, X, target, B_local, B_global, loss_kind, step);
         f->pending_steps++;
+        f->grads_clean = true;   // optimistic; nfg_field_check corrects it
     });
 }
 
@@ -819,6 +910,7 @@ nfg_status nfg_field_check(nfg_field* f)
         f->pending_steps = 0;
         if (f->h_res->flags[1]) {
             f->step -= 1;
+            f->grads_clean = f->h_res->flags[3] != 0;
             raise_if_aborted(f);
         }
     });
@@ -892,6 +984,7 @@ nfg_status nfg_encode_backward(nfg_field* f, const float* X, int64_t B, const fl
         const float* ddY = stage(c->s1, dY, size_t(B) * f->shape.in_real, c->stream);
         NFG_CUDA(nfg::launch_encode_bwd_lv(f->shape, f->d_levels, dX, B, ddY, f->d_g, c->stream));
         c->launches++;
+        f->grads_clean = false;
         NFG_CUDA(cudaStreamSynchronize(c->stream));
     });
 }
@@ -938,6 +1031,7 @@ nfg_status nfg_mlp_backward(nfg_field* f, const float* Y, int64_t B, const float
         NFG_CUDA(nfg::launch_train(f->shape, nullptr, nfg::SRC_LOAD_Y, nfg::GRAD_DOUT, nfg::SINK_STORE, a, c->num_sms,
                                    c->stream, nullptr));
         c->launches++;
+        f->grads_clean = false;
         if (B > 0)
             NFG_CUDA(cudaMemcpyAsync(dY, ddY, size_t(B) * f->shape.in_real * 4, cudaMemcpyDeviceToHost, c->stream));
         NFG_CUDA(cudaStreamSynchronize(c->stream));
@@ -977,6 +1071,7 @@ nfg_status nfg_adam_step(nfg_field* f, float lr_now)
             f->step = before;
             raise_if_aborted(f);
         }
+        f->grads_clean = true;
     });
 }
 

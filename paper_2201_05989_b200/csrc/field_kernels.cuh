@@ -201,6 +201,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         dwo[e >> 2][e & 3] = 0.0f;
 
     bool bad = false;
+    unsigned int invalid = 0u;
     NFG_PT_DECL
     const int64_t ntiles = (a.B + TS - 1) / TS;
     const int r0 = 16 * warp;
@@ -208,10 +209,32 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         NFG_PT_START();
         const int64_t sg = tile * TS + r0 + g, sg8 = sg + 8;
         const bool vg = sg < a.B, vg8 = sg8 < a.B;
+        if (a.ready) {   // streamed inputs: wait for this tile's chunk to land
+            if (tid == 0) {
+                const int64_t last = min(a.B, (tile + 1) * TS) - 1;
+                const unsigned int* f = a.ready + last / a.chunk;
+                unsigned int v;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                    if (int(v - a.epoch) >= 0)
+                        break;
+                    __nanosleep(100);
+                }
+            }
+            __syncthreads();
+        }
         float xg[D], xg8[D];
         if (SRC == SRC_ENCODE) {
             load_x<D>(xg, a.X, sg, vg);
             load_x<D>(xg8, a.X, sg8, vg8);
+            if (a.validate) {   // encode_forward's checks (grid.hpp:226-229)
+                const float lo = -1e-6f, hi = 1.0f + 1e-6f;
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    invalid |= (finite_f(xg[i]) ? 0u : 1u) | ((xg[i] < lo || xg[i] > hi) ? 2u : 0u);
+                    invalid |= (finite_f(xg8[i]) ? 0u : 1u) | ((xg8[i] < lo || xg8[i] > hi) ? 2u : 0u);
+                }
+            }
         }
         // ---- encode / load inputs -------------------------------------
         uint32_t afr[IN_STEPS][4];
@@ -496,6 +519,11 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0)
         atomicOr(a.scratch.flags, 1u);
+    invalid = __reduce_or_sync(0xffffffffu, invalid);
+    if (invalid && lane == 0) {
+        atomicOr(&a.scratch.flags[3], invalid);
+        atomicOr(&a.scratch.flags[1], 1u);
+    }
 }
 
 template <int SRC, int D, int F, typename TT, int IN_STEPS, int NH>

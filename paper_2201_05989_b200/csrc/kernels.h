@@ -51,6 +51,16 @@ struct TrainArgs {
     float* pred;             // optional n_out x B
     StepScratch scratch;
     unsigned long long* phase_clk;   // NFG_PHASE_TIMING builds only
+    // Streamed inputs (host-pointer train_step): tile t may start once
+    // ready[(last sample of t) / chunk] >= epoch (written by the copy stream
+    // after the chunk's H2D). ready == nullptr: inputs already resident.
+    const unsigned int* ready;
+    unsigned int epoch;
+    int64_t chunk;
+    // 1: check the inputs inside the kernel (grid.hpp:226-229) and flag an
+    // invalid batch (flags[3], abort flags[1]); Adam's check kernel then
+    // restores the (clean) gradient slab, so no state changes.
+    int validate;
 };
 
 struct InferArgs {
@@ -84,6 +94,7 @@ struct AdamArgs {
     uint64_t n_tab, n_w, n_b;
     float b1, b2, omb1, omb2, bc1, bc2, eps, l2, lr;
     unsigned int* flags;
+    int restore_on_invalid;   // zero the gradient slab if flags[3] (speculative step)
 };
 cudaError_t launch_adam(const AdamArgs& a, bool force_check, int num_sms, cudaStream_t st);
 cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cudaStream_t st);

@@ -230,6 +230,33 @@ def test_invalid_batch_leaves_state_untouched():   # grid.hpp:226-229 through tr
     assert m.step == 1
 
 
+def test_streamed_batch_invalid_tail_and_parity():
+    """Host-pointer train_step with B >= 2^15 streams the batch in chunks while
+    the fused kernel runs, validating inputs speculatively: a bad value in the
+    LAST chunk must still leave parameters, gradients, moments and the step
+    untouched (grid.hpp:226-229), and a good batch must match the oracle."""
+    nf = _nf()
+    from paper_2201_05989_b200._lib import NfgInvalidArgument
+    g = _grid(nf, dims=3, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=512)
+    m = _model(nf, g, hidden_layers=2, table_fp32=True, lr=1e-3)
+    f = _oracle_field(m, lr=1e-3)
+    B = 1 << 16
+    X = _points(B, 3, seed=3)
+    T = O.csg_sdf(X).reshape(B, 1)
+    before = m.params
+    Xb = X.copy()
+    Xb[B - 5, 2] = np.inf
+    with pytest.raises(NfgInvalidArgument, match="non-finite"):
+        m.train_step(Xb, T, nf.LossKind.Mape, 1)
+    assert np.array_equal(m.params, before) and (m.grads == 0).all() and m.step == 0
+    _, mm, vv = m.adam_state()
+    assert (mm == 0).all() and (vv == 0).all()
+    for step in (1, 2):
+        lg = m.train_step(X, T, nf.LossKind.Mape, step)
+        lo = f.train_step(X, T, O.LOSS_MAPE, step)
+        assert abs(lg - lo) <= 1e-3 * abs(lo), (step, lg, lo)
+
+
 def test_invalid_and_unsupported():   # grid.hpp:224-229, NFG_EUNSUPPORTED
     nf = _nf()
     from paper_2201_05989_b200._lib import NfgInvalidArgument, NfgUnsupported
