@@ -172,8 +172,16 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     if (SRC == SRC_ENCODE)
         for (int i = tid; i < s.grid.L; i += blockDim.x)
             lvs[i] = levels[i];
-    for (int i = tid; i < (NH + 1) * H; i += blockDim.x)
-        db[i] = 0.0f;
+    // padding columns of the activation buffers: a 1 then zeros (db_tile)
+    for (int r = tid; r < TS; r += blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            act0[r * SM::INS + 16 * IN_STEPS + c] = __float2half_rn(c == 0 ? 1.0f : 0.0f);
+#pragma unroll
+            for (int k = 0; k < NH; ++k)
+                acth[k * TS * HS + r * HS + H + c] = __float2half_rn(c == 0 ? 1.0f : 0.0f);
+        }
+    }
     __syncthreads();
 
     const __half* W0s = ws;
@@ -184,6 +192,10 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     constexpr int P0 = 4 * IN_STEPS, PH = 16, PO = 4;
     constexpr int C0 = (P0 + TW - 1) / TW, CH = PH / TW, NHM = NH > 1 ? NH - 1 : 1;
     float dw0[C0][2][4], dwh[NHM][CH][2][4], dwo[2][4];
+    float dbh[NH][2], dbo[2] = { 0.0f, 0.0f };
+#pragma unroll
+    for (int k = 0; k < NH; ++k)
+        dbh[k][0] = dbh[k][1] = 0.0f;
 #pragma unroll
     for (int c = 0; c < C0; ++c)
 #pragma unroll
@@ -362,45 +374,17 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         uint32_t azo[1][4];
         c_to_a<1, true>(ao, azo);
         store_a<1>(azo, dzo, SM::OS, r0, lane);
-        {
-            float cs[2][2];
-            col_sums<2>(ao, cs);
-            if (g == 0)
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-#pragma unroll
-                    for (int q = 0; q < 2; ++q)
-                        atomicAdd(&db[NH * H + 8 * j + 2 * t + q], cs[j][q] * isc);
-        }
         layer_bwd<1, HT>(azo, Wos, HS, acc, lane);
         apply_mask<HT>(acc, mask[NH - 1]);
 #pragma unroll
         for (int k = NH - 1; k >= 1; --k) {
             c_to_a<4, true>(acc, ah);
             store_a<4>(ah, dzh + k * TS * HS, HS, r0, lane);
-            float cs[HT][2];
-            col_sums<HT>(acc, cs);
-            if (g == 0)
-#pragma unroll
-                for (int j = 0; j < HT; ++j)
-#pragma unroll
-                    for (int q = 0; q < 2; ++q)
-                        atomicAdd(&db[k * H + 8 * j + 2 * t + q], cs[j][q] * isc);
             layer_bwd<4, HT>(ah, Whs + (k - 1) * Lay::WH_HALVES, HS, acc, lane);
             apply_mask<HT>(acc, mask[k - 1]);
         }
         c_to_a<4, true>(acc, ah);
         store_a<4>(ah, dzh, HS, r0, lane);
-        {
-            float cs[HT][2];
-            col_sums<HT>(acc, cs);
-            if (g == 0)
-#pragma unroll
-                for (int j = 0; j < HT; ++j)
-#pragma unroll
-                    for (int q = 0; q < 2; ++q)
-                        atomicAdd(&db[8 * j + 2 * t + q], cs[j][q] * isc);
-        }
         float ay[2 * IN_STEPS][4];
         layer_bwd<4, 2 * IN_STEPS>(ah, W0s, SM::INS, ay, lane);
 
@@ -472,6 +456,25 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 dwo[1][e] = fmaf(c1[e], isc, dwo[1][e]);
             }
         }
+        // db = dz^T * 1 through the ones column of each activation buffer
+        if (warp < 4) {
+#pragma unroll
+            for (int k = 0; k < NH; ++k) {
+                float c[4];
+                if (k == 0)
+                    db_tile<TS>(c, dzh, HS, act0, SM::INS, warp, 16 * IN_STEPS, lane);
+                else
+                    db_tile<TS>(c, dzh + k * TS * HS, HS, acth + (k - 1) * TS * HS, HS, warp, H, lane);
+                dbh[k][0] = fmaf(c[0], isc, dbh[k][0]);
+                dbh[k][1] = fmaf(c[2], isc, dbh[k][1]);
+            }
+        }
+        if (warp == TW - 1) {
+            float c[4];
+            db_tile<TS>(c, dzo, SM::OS, acth + (NH - 1) * TS * HS, HS, 0, H, lane);
+            dbo[0] = fmaf(c[0], isc, dbo[0]);
+            dbo[1] = fmaf(c[2], isc, dbo[1]);
+        }
         NFG_PT(6);
         __syncthreads();
         NFG_PT(7);
@@ -511,11 +514,24 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         if (warp < PO)
             flush(dwo, 0, warp, s.n_out, H, size_t(H) * s.in_real + size_t(NH - 1) * H * H);
     }
-    __syncthreads();
-    for (int i = tid; i < H * NH + s.n_out; i += blockDim.x) {
-        const float v = db[i] * ic;
-        bad |= !sane(v);
-        atomicAdd(a.gb + i, v);
+    if (t == 0) {
+        if (warp < 4)
+#pragma unroll
+            for (int k = 0; k < NH; ++k)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float v = dbh[k][h] * ic;
+                    bad |= !sane(v);
+                    atomicAdd(a.gb + k * H + 16 * warp + g + 8 * h, v);
+                }
+        if (warp == TW - 1)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (g + 8 * h < s.n_out) {
+                    const float v = dbo[h] * ic;
+                    bad |= !sane(v);
+                    atomicAdd(a.gb + NH * H + g + 8 * h, v);
+                }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0)
         atomicOr(a.scratch.flags, 1u);

@@ -274,6 +274,33 @@ __device__ __forceinline__ float loss_grad(int kind, float p, float t, float& te
     }
 }
 
+__device__ __forceinline__ void ldsm_x2_t(uint32_t& r0, uint32_t& r1, const void* p)
+{
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];\n" : "=r"(r0), "=r"(r1) : "r"(a));
+}
+
+// db via the tensor cores: the activation buffers carry a column of ones at
+// `ones_col` (in their padding), so one extra n8 tile of dz^T * [act | 1]
+// yields sum_samples dz for 16 outputs (C regs 0 and 2 of the t == 0 lanes).
+template <int S>
+__device__ __forceinline__ void db_tile(float (&c)[4], const __half* dz, int dzs, const __half* act, int as, int mt,
+                                        int ones_col, int lane)
+{
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        c[e] = 0.0f;
+    const int ar = (lane & 7) + ((lane >> 4) << 3), ac = ((lane >> 3) & 1) << 3;
+    const int br = (lane & 7) + (((lane >> 3) & 1) << 3);
+#pragma unroll 4
+    for (int ks = 0; ks < S / 16; ++ks) {
+        uint32_t a[4], b0, b1;
+        ldsm_x4_t(a[0], a[1], a[2], a[3], dz + (16 * ks + ar) * dzs + 16 * mt + ac);
+        ldsm_x2_t(b0, b1, act + (16 * ks + br) * as + ones_col);
+        mma16816(c, a, b0, b1);
+    }
+}
+
 // ---- dW: per-CTA K = S samples from smem (dz^T * act) -----------------------
 // One (mt, np) pair = 16 out rows x 16 in cols = two n8 C tiles.
 template <int S>

@@ -59,8 +59,8 @@ def backward(W, b, shapes, Y, dOut, sigmoid):
     sc = tile_scale(dz)
     gW, gb = [None] * len(mats), [None] * len(mats)
     for k in range(len(mats) - 1, -1, -1):
-        gb[k] = dz.sum(0)
         dzh = h(dz * sc) / sc
+        gb[k] = dzh.sum(0)   # the kernel forms db on the tensor cores from the fp16 dz
         gW[k] = dzh.T @ acts[k]
         da = dzh @ h(mats[k])
         if k > 0:
