@@ -58,51 +58,86 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clocks and throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line). NVML is polled in-process every ~2 ms, so
+    even a few-millisecond timed region gets samples; nvidia-smi -lms is the
+    fallback when NVML cannot be loaded."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []          # (sm_mhz, max_mhz, reasons bitmask, util %)
         self._stop = threading.Event()
         self._proc = None
+        self._nv = None
 
-    def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+    def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self._max = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._poll_nvml, daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            self._nv = None
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu")
         try:
             self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                           "--format=csv,noheader,nounits", "-lms", "100"],
+                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                           stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t = threading.Thread(target=self._read_smi, daemon=True)
             self._t.start()
         except Exception:
             self._proc = None
         return self
 
-    def _read(self):
-        for line in self._proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 7:
-                self.rows.append(parts)
+    def _poll_nvml(self):
+        nv, h = self._nv, self._h
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                ut = nv.nvmlDeviceGetUtilizationRates(h).gpu
+                self.rows.append((float(sm), float(self._max), int(rs), int(ut)))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
-    def __exit__(self, *a):
+    def _read_smi(self):
+        for line in self._proc.stdout:
+            p = [x.strip() for x in line.split(",")]
+            try:
+                self.rows.append((float(p[0]), float(p[1]), int(p[2], 16), int(p[3])))
+            except Exception:
+                pass
+
+    def stop(self):
+        self._stop.set()
         if self._proc:
             self._proc.terminate()
             try:
                 self._proc.wait(timeout=2)
             except Exception:
                 self._proc.kill()
+        if self._nv is not None:
+            self._t.join(timeout=1)
 
-    def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        load = [r for r in self.rows if r[6].isdigit() and int(r[6]) > 50] or self.rows
-        sm = sorted(float(r[0]) for r in load if r[0].replace(".", "").isdigit())
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in load for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
-                "sm_max_mhz": float(load[0][1]) if load[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(load)}
+    def mark(self):
+        return len(self.rows)
+
+    def summary(self, since=0):
+        rows = self.rows[since:] or self.rows[-8:]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0}
+        sm = sorted(r[0] for r in rows)
+        reasons = sorted({n for r in rows for n, bit in self.REASONS if r[2] & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_min_mhz": sm[0], "sm_max_mhz": rows[0][1], "reasons": reasons,
+                "samples": len(rows), "source": "nvml" if self._nv is not None else "nvidia-smi"}
 
 
 def ncu_traffic():
@@ -235,6 +270,10 @@ def main():
         model.train_step_device(Xs[i % N_RESIDENT], Ts[i % N_RESIDENT], B_TRAIN, B_TRAIN * world,
                                 nf.LossKind.Mape, step)
 
+    clk = Clocks(local).start()
+    t_wait = time.perf_counter()
+    while not clk.rows and time.perf_counter() - t_wait < 3.0:   # first sample before timing
+        time.sleep(0.01)
     for i in range(args.warmup):
         one(i)
     model.check()
@@ -246,15 +285,16 @@ def main():
     ms = (C.c_double * 4)()
     nst = C.c_int64()
     lib.nfg_ctx_read_profile(ctx.h, ms, C.byref(nst))   # reset
-    with Clocks(local) as clk:
-        barrier()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        for i in range(args.steps):
-            one(args.warmup + i)
-        ev1.record(stream)
-        barrier()
+    barrier()
+    mark0 = clk.mark()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(args.steps):
+        one(args.warmup + i)
+    ev1.record(stream)
+    barrier()
+    mark1 = clk.mark()
     launches = ctx.launch_count - launches0
     t_ms = ev0.elapsed_time(ev1)
     lib.nfg_ctx_read_profile(ctx.h, ms, C.byref(nst))
@@ -311,6 +351,12 @@ def main():
         t_inf = float(tt.item())
     qps = world * Bq / (t_inf / 1000.0)
 
+    clk.stop()
+    clocks = clk.summary(mark0 if mark1 > mark0 else 0)
+    if mark1 <= mark0:
+        clocks["note"] = "no sample inside the training timed region; summary over the whole measurement"
+    clocks["train_region_samples"] = mark1 - mark0
+
     # ---- roofline of the dominant kernel --------------------------------------
     hbm_peak, tflops_peak, peak_src = peaks()
     train_ms, adam_ms = phase_ms[0], phase_ms[1]
@@ -363,7 +409,7 @@ def main():
                 "roofline": roof, "roofline_adam": roof_adam,
                 "secondary_rates": {"adam_gbs": adam_gbs, "train_l2_gbs": train_l2_gbs,
                                     "train_mlp_tflops": train_tflops},
-                "gpu_launches": launches, "clocks": clk.summary(), "cpu_baseline": cpu,
+                "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
                 "params": n_params}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -280,6 +280,17 @@ void refresh_shadow(nfg_field* f)
     f->ctx->launches++;
 }
 
+// True for page-locked (cudaHostAlloc / cudaHostRegister) host memory.
+bool is_pinned(const void* p)
+{
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 template <class T>
 T* stage(DevBuf& b, const T* host, size_t count, cudaStream_t st)
 {
@@ -825,10 +836,15 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
         const int d = f->gcfg.dims, no = f->mcfg.output_width;
         const uint64_t before = f->step;
         const bool was_clean = f->grads_clean;
-        if (f->grads_clean && f->opts.fused_train && c->write_value32 && B >= (int64_t(1) << 15)) {
-            // Overlap the H2D of the batch with the step: the fused kernel is
-            // launched first and waits per tile for its chunk's ready flag,
-            // which the copy stream writes after each chunk lands.
+        if (f->grads_clean && f->opts.fused_train && c->write_value32 && B >= (int64_t(1) << 15) &&
+            is_pinned(X) && is_pinned(target)) {
+            // Overlap the H2D of the batch with the step: the chunk copies and
+            // their ready flags are enqueued on the copy stream FIRST, then the
+            // fused kernel is launched and waits per tile for its chunk's flag.
+            // Every copy the kernel waits on is already queued when it starts,
+            // so it completes even if launches are serialised (profilers,
+            // CUDA_LAUNCH_BLOCKING). Pinned sources only: a pageable copy would
+            // block the host before the launch and overlap nothing.
             float* dX = static_cast<float*>(c->s0.get(size_t(B) * d * 4));
             float* dT = static_cast<float*>(c->s1.get(size_t(B) * no * 4));
             const int64_t chunk = std::max<int64_t>((B / 16 + 255) / 256 * 256, (B + NFG_MAX_CHUNKS - 1) / NFG_MAX_CHUNKS);
@@ -836,7 +852,6 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
             const unsigned int epoch = ++f->epoch;
             NFG_CUDA(cudaEventRecord(c->ev_order, c->stream));        // staging buffers free
             NFG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_order, 0));
-            device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step, Streamed{ f->d_ready, epoch, chunk });
             int64_t k = 0;
             try {
                 for (; k < nchunks; ++k) {
@@ -849,8 +864,15 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
                         throw Fail{ NFG_ECUDA, "cuStreamWriteValue32 failed" };
                 }
             } catch (...) {
-                for (; k < nchunks; ++k)   // never leave the kernel waiting
-                    c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0);
+                // the kernel was not launched; drain the copy stream so the
+                // staging buffers are not reused under an in-flight copy
+                cudaStreamSynchronize(c->copy_stream);
+                throw;
+            }
+            try {
+                device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step, Streamed{ f->d_ready, epoch, chunk });
+            } catch (...) {
+                cudaStreamSynchronize(c->copy_stream);
                 throw;
             }
         } else {

@@ -1,12 +1,13 @@
 # ncu evidence for the bench workload (one GPU). Usage: bash tools/gpu_ncu.sh <tag>
+# Then, here (no GPU): python tools/ncu_summary.py <tag>
 cd $GRAFT_REPO_ROOT
 TAG=${1:-r1}
 mkdir -p gpurun_out
 # launch list of this library's kernels (mangled names start with _ZN3nfg)
-ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base mangled -k regex:_ZN3nfg -c 60 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base mangled -k regex:_ZN3nfg -c 60 --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline --infer-b 4194304 > gpurun_out/launches_$TAG.log 2>&1
 for K in k_train k_adam k_infer; do
-  ncu --set full --clock-control none --import-source on -k $K -s 3 -c 1 -o gpurun_out/prof_${K}_$TAG \
+  timeout 600 ncu --set full --clock-control none --import-source on -k $K -s 3 -c 1 -o gpurun_out/prof_${K}_$TAG \
       python bench.py --steps 3 --warmup 3 --no-cpu-baseline --infer-b 4194304 > gpurun_out/prof_${K}_$TAG.log 2>&1
 done
 ls -la gpurun_out
