@@ -43,7 +43,8 @@ typedef enum {
     NFG_EUNSUPPORTED = 3,  /* valid for the reference, not built for sm_100a (e.g. hidden_width != 64) */
     NFG_ECUDA = 4,
     NFG_ENCCL = 5,
-    NFG_ELOGIC = 6
+    NFG_ELOGIC = 6,
+    NFG_EIO = 7            /* std::runtime_error from checkpoint / report IO (io.cpp) */
 } nfg_status;
 
 typedef enum { NFG_INTERP_LINEAR = 0, NFG_INTERP_SMOOTHSTEP = 1 } nfg_interpolation; /* grid.hpp:20 */
@@ -94,6 +95,9 @@ typedef struct {
 typedef struct {
     int32_t table_fp32;    /* 1: gather fp32 master tables (exact-parity mode); 0: fp16 shadow (default) */
     int32_t fused_train;   /* 1: one fused encode+MLP+loss+backward kernel per step (default); 0: staged kernels */
+    int32_t deterministic; /* 1: run-to-run bit-reproducible backward: table gradients accumulate per
+                              row in the reference's order (grid.hpp:286-294; bit-identical to it for equal dY),
+                              MLP gradients and the loss sum reduce per-CTA partials in a fixed order. Slower. */
 } nfg_options;
 
 typedef struct nfg_ctx nfg_ctx;
@@ -146,6 +150,7 @@ nfg_status nfg_field_read(nfg_field* f, int32_t which, uint64_t offset, uint64_t
 nfg_status nfg_field_write(nfg_field* f, int32_t which, uint64_t offset, uint64_t count, const float* host);
 nfg_status nfg_field_device_buffer(nfg_field* f, int32_t which, float** dev, uint64_t* count);
 /* AdamState::step (adam.hpp:56-73). */
+nfg_status nfg_field_get_config(const nfg_field* f, nfg_grid_config* grid, nfg_mlp_config* mlp);
 nfg_status nfg_field_get_step(const nfg_field* f, uint64_t* step);
 nfg_status nfg_field_set_step(nfg_field* f, uint64_t step);
 
@@ -196,6 +201,19 @@ nfg_status nfg_adam_step(nfg_field* f, float lr_now);
 double nfg_lr_at(const int64_t* milestones, int32_t n, double factor, double base_lr, int64_t step);
 
 /* ---- pinned host memory for zero-copy-staged inputs -------------------- */
+/* ---- checkpoint (io.cpp:222-351, NFC1/HGE1/MLP1/ADM1) --------------------
+ * Byte-compatible with the reference's save_checkpoint / load_checkpoint for
+ * hash-encoder models. load creates a new field from the file's configs (the
+ * reference's load_checkpoint also replaces hash_cfg / mlp_cfg), with hyper
+ * and options supplied by the caller as a resume does (test_tasks.cpp:313-315).
+ * Errors: NFG_EIO with the reference's messages ("checkpoint: missing ...
+ * section", "checkpoint: truncated ...", "checkpoint: level length mismatch",
+ * "cannot read/write checkpoint: <path>"); NFG_EUNSUPPORTED for OCT1 /
+ * frequency-encoder files. */
+nfg_status nfg_field_save(nfg_field* f, const char* path);
+nfg_status nfg_field_load(nfg_ctx* ctx, const char* path, const nfg_adam_hyper* hyper, const nfg_options* opts,
+                          nfg_field** out);
+
 nfg_status nfg_host_alloc(size_t bytes, void** out);
 nfg_status nfg_host_free(void* p);
 

@@ -511,6 +511,93 @@ class Field:
 
 
 # --------------------------------------------------------------------------
+# Checkpoint (io.cpp:222-351): NFC1 | HGE1 | MLP1 | ADM1, little-endian
+# --------------------------------------------------------------------------
+def save_checkpoint(field: "Field", path: str, n_frequencies: int = 10) -> None:   # io.cpp:222-285
+    import struct
+    g, m = field.grid, field.mlp
+    P, M, V = field.params, field.m, field.v
+    out = bytearray(b"NFC1" + struct.pack("<II", 0, n_frequencies) + b"HGE1")
+    out += struct.pack("<7I", g.dims, g.levels, g.table_size, g.features, g.n_min, g.n_max, int(g.smoothstep))
+    for lv in level_resolutions(g):                      # io.cpp:241-244
+        off = lv.row_offset * g.features
+        out += struct.pack("<Q", lv.table_len) + P[off:off + lv.table_len * g.features].astype("<f4").tobytes()
+    out += b"MLP1" + struct.pack("<5I", m.input_width, m.hidden_layers, m.hidden_width, m.output_width,
+                                 int(m.sigmoid))
+    wo, bo = field.n_tab, field.n_tab + field.n_w
+    for (i, o) in m.layer_shapes():                      # io.cpp:264-267: W_k then b_k
+        out += P[wo:wo + o * i].astype("<f4").tobytes() + P[bo:bo + o].astype("<f4").tobytes()
+        wo += o * i
+        bo += o
+    out += b"ADM1" + struct.pack("<QI", field.step, 3)
+    off = 0
+    for n in (field.n_tab, field.n_w, field.n_b):        # io.cpp:273-277
+        out += struct.pack("<Q", n) + M[off:off + n].astype("<f4").tobytes() + V[off:off + n].astype("<f4").tobytes()
+        off += n
+    with open(path, "wb") as f:
+        f.write(bytes(out))
+
+
+def load_checkpoint(path: str, hyper: "Hyper" = None) -> "Field":   # io.cpp:287-351
+    import struct
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise OracleRuntimeError("cannot read checkpoint: " + path) from None
+    pos = 0
+
+    def take(n, what="truncated file"):
+        nonlocal pos
+        if pos + n > len(data):
+            raise OracleRuntimeError("checkpoint: " + what)
+        b = data[pos:pos + n]
+        pos += n
+        return b
+
+    def tag(t, what):
+        if pos + 4 > len(data) or data[pos:pos + 4] != t:
+            raise OracleRuntimeError(f"checkpoint: missing {what} section")
+        take(4)
+
+    def floats(n):
+        return np.frombuffer(take(4 * n, "truncated float block"), "<f4").astype(np.float32)
+
+    tag(b"NFC1", "file header")
+    encoder, _ = struct.unpack("<II", take(8))
+    if encoder != 0:
+        raise OracleRuntimeError("checkpoint: only the hash encoder is restated")
+    tag(b"HGE1", "feature table")
+    d, L, T, F, nmin, nmax, interp = struct.unpack("<7I", take(28))
+    g = GridCfg(levels=L, table_size=T, features=F, n_min=nmin, n_max=nmax, dims=d, smoothstep=bool(interp))
+    tab = []
+    for lv in level_resolutions(g):
+        (n,) = struct.unpack("<Q", take(8))
+        if n != lv.table_len:
+            raise OracleRuntimeError("checkpoint: level length mismatch")
+        tab.append(floats(n * F))
+    tag(b"MLP1", "MLP parameters")
+    iw, hl, hw, ow, act = struct.unpack("<5I", take(20))
+    f = Field(g, MlpCfg(hidden_layers=hl, hidden_width=hw, output_width=ow, sigmoid=bool(act)), hyper or Hyper())
+    Ws, bs = [], []
+    for (i, o) in f.mlp.layer_shapes():
+        Ws.append(floats(o * i))
+        bs.append(floats(o))
+    tag(b"ADM1", "optimizer state")
+    step, ng = struct.unpack("<QI", take(12))
+    ms, vs = [], []
+    for _ in range(ng):
+        (n,) = struct.unpack("<Q", take(8))
+        ms.append(floats(n))
+        vs.append(floats(n))
+    f.params[:] = np.concatenate(tab + Ws + bs)
+    f.m[:] = np.concatenate(ms)
+    f.v[:] = np.concatenate(vs)
+    f.step = step
+    return f
+
+
+# --------------------------------------------------------------------------
 # RNG and fixtures
 # --------------------------------------------------------------------------
 class Pcg32:

@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("NFG_LIB", os.path.join(_HERE, "libnfg.so"))   # NFG_LIB: A/B builds
 
-NFG_OK, NFG_EINVAL, NFG_ENONFINITE, NFG_EUNSUPPORTED, NFG_ECUDA, NFG_ENCCL, NFG_ELOGIC = range(7)
+NFG_OK, NFG_EINVAL, NFG_ENONFINITE, NFG_EUNSUPPORTED, NFG_ECUDA, NFG_ENCCL, NFG_ELOGIC, NFG_EIO = range(8)
 
 
 class nfg_grid_config(C.Structure):
@@ -36,7 +36,7 @@ class nfg_adam_hyper(C.Structure):
 
 
 class nfg_options(C.Structure):
-    _fields_ = [("table_fp32", C.c_int32), ("fused_train", C.c_int32)]
+    _fields_ = [("table_fp32", C.c_int32), ("fused_train", C.c_int32), ("deterministic", C.c_int32)]
 
 
 _vp = C.c_void_p
@@ -72,6 +72,7 @@ SIGNATURES = {
     "nfg_field_read": (C.c_int, [_vp, C.c_int32, C.c_uint64, C.c_uint64, _vp]),
     "nfg_field_write": (C.c_int, [_vp, C.c_int32, C.c_uint64, C.c_uint64, _vp]),
     "nfg_field_device_buffer": (C.c_int, [_vp, C.c_int32, C.POINTER(_fp), _u64p]),
+    "nfg_field_get_config": (C.c_int, [_vp, C.POINTER(nfg_grid_config), C.POINTER(nfg_mlp_config)]),
     "nfg_field_get_step": (C.c_int, [_vp, _u64p]),
     "nfg_field_set_step": (C.c_int, [_vp, C.c_uint64]),
     "nfg_field_train_step": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int64, _fp]),
@@ -87,6 +88,8 @@ SIGNATURES = {
     "nfg_loss": (C.c_int, [_vp, C.c_int32, _vp, _vp, C.c_int64, C.c_int64, _vp, _fp]),
     "nfg_adam_step": (C.c_int, [_vp, C.c_float]),
     "nfg_lr_at": (C.c_double, [_i64p, C.c_int32, C.c_double, C.c_double, C.c_int64]),
+    "nfg_field_save": (C.c_int, [_vp, C.c_char_p]),
+    "nfg_field_load": (C.c_int, [_vp, C.c_char_p, C.POINTER(nfg_adam_hyper), C.POINTER(nfg_options), C.POINTER(_vp)]),
     "nfg_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
     "nfg_host_free": (C.c_int, [_vp]),
 }
@@ -112,6 +115,10 @@ class NfgNonFinite(NfgError):
 
 class NfgUnsupported(NfgError, NotImplementedError):
     """valid for the reference, not built for sm_100a"""
+
+
+class NfgIOError(NfgError):
+    """std::runtime_error from checkpoint / report IO (io.cpp)"""
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:
@@ -140,4 +147,6 @@ def check(status: int) -> None:
         raise NfgNonFinite(status, msg)
     if status == NFG_EUNSUPPORTED:
         raise NfgUnsupported(status, msg)
+    if status == NFG_EIO:
+        raise NfgIOError(status, msg)
     raise NfgError(status, msg)

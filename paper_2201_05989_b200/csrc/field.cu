@@ -124,6 +124,10 @@ struct DevBuf {
 
 }   // namespace
 
+namespace nfg {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}   // namespace nfg
+
 struct nfg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -199,7 +203,7 @@ struct nfg_field {
     nfg_grid_config gcfg{};
     nfg_mlp_config mcfg{};
     nfg_adam_hyper hyper{ 1e-2, 0.9, 0.99, 1e-15, 1e-6 };
-    nfg_options opts{ 0, 1 };
+    nfg_options opts{ 0, 1, 0 };
     std::vector<int64_t> milestones;
     double factor = 0.33;
     std::vector<nfg_level_spec> levels;
@@ -223,6 +227,7 @@ struct nfg_field {
     bool grads_clean = true;
     unsigned int* d_ready = nullptr;   // NFG_MAX_CHUNKS chunk-ready flags
     unsigned int epoch = 0;
+    DevBuf det_part, det_loss, det_sort;   // deterministic mode scratch
 };
 
 #define NFG_MAX_CHUNKS 64
@@ -329,6 +334,44 @@ void run_adam(nfg_field* f, float lr_now, bool force_check)
     f->step = next;
 }
 
+// Deterministic-mode helpers (nfg_options.deterministic; det_kernels.cu).
+// The staged MLP kernel writes per-CTA partials of dW/db (and the loss sum),
+// reduced in CTA order; the table gradients go through the sorted per-row
+// reduction that reproduces the reference's accumulation order.
+void det_prepare(nfg_field* f, nfg::TrainArgs& a, int64_t B, bool with_loss)
+{
+    nfg_ctx* c = f->ctx;
+    const int64_t ntiles = (B + 15) / 16;   // >= tiles of any train instantiation
+    const int64_t max_grid = std::min<int64_t>(ntiles, int64_t(c->num_sms) * 16);
+    a.n_w = int64_t(f->n_w);
+    a.n_wb = int64_t(f->n_w + f->n_b);
+    a.part_wb = static_cast<float*>(f->det_part.get(size_t(std::max<int64_t>(max_grid, 1)) * size_t(a.n_wb) * 4));
+    a.part_loss = with_loss ? static_cast<double*>(f->det_loss.get(
+                                  size_t(std::max<int64_t>(max_grid, 1)) * nfg::train_warps_per_cta() * 8))
+                            : nullptr;
+}
+
+void det_finish(nfg_field* f, const nfg::TrainArgs& a, int grid)
+{
+    nfg_ctx* c = f->ctx;
+    if (grid <= 0)
+        return;
+    NFG_CUDA(nfg::launch_reduce_partials(a.part_wb, grid, a.n_wb, f->d_g + f->n_tab_dev, a.part_loss,
+                                         grid * nfg::train_warps_per_cta(), &f->d_res->loss_sum, f->d_res->flags,
+                                         c->stream));
+    c->launches++;
+}
+
+void det_encode_bwd(nfg_field* f, const float* X, int64_t B, const float* dY)
+{
+    nfg_ctx* c = f->ctx;
+    const size_t bytes = nfg::encode_bwd_det_scratch(B, f->gcfg.dims);
+    void* scratch = f->det_sort.get(std::max<size_t>(bytes, 16));
+    NFG_CUDA(nfg::launch_encode_bwd_det(f->shape, f->d_levels, X, B, dY, f->d_g, f->d_res->flags, scratch, bytes,
+                                        c->stream));
+    c->launches += 3 * size_t(f->gcfg.levels);
+}
+
 // Forward + loss + backward: gradients ACCUMULATE into the grad slab (the
 // reference's mlp_backward / encode_backward semantics); no optimizer step.
 struct Streamed {
@@ -348,7 +391,8 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
     // slab the fused kernel checks its own inputs and Adam's check kernel
     // undoes the step on failure (re-zeroing); otherwise a separate k_validate
     // aborts every later kernel before any update.
-    const bool speculative = allow_speculative && f->grads_clean && f->opts.fused_train;
+    const bool fused = f->opts.fused_train && !f->opts.deterministic;
+    const bool speculative = allow_speculative && f->grads_clean && fused;
     require(speculative || sm.ready == nullptr, "streamed inputs need the speculative fused path");
     if (!speculative) {
         NFG_CUDA(nfg::launch_validate(X, B_local * f->gcfg.dims, f->d_res->flags, c->stream));
@@ -376,10 +420,25 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
         c->prof_steps++;
     if (B_local > 0) {
         Span span(c, 0);
-        if (f->opts.fused_train) {
+        if (fused) {
             NFG_CUDA(nfg::launch_train(f->shape, f->d_levels, nfg::SRC_ENCODE, nfg::GRAD_LOSS, nfg::SINK_SCATTER, a,
                                        c->num_sms, c->stream, nullptr));
             c->launches++;
+        } else if (f->opts.deterministic) {
+            const size_t LF = size_t(f->shape.in_real);
+            float* Y = static_cast<float*>(c->s2.get(size_t(B_local) * LF * 4));
+            float* dY = static_cast<float*>(c->s3.get(size_t(B_local) * LF * 4));
+            NFG_CUDA(nfg::launch_encode_fwd_lv(f->shape, f->d_levels, X, B_local, table_ptr(f), Y, nullptr, nullptr,
+                                               c->stream));
+            a.Y = Y;
+            a.dY = dY;
+            det_prepare(f, a, B_local, true);
+            int grid = 0;
+            NFG_CUDA(nfg::launch_train(f->shape, nullptr, nfg::SRC_LOAD_Y, nfg::GRAD_LOSS, nfg::SINK_STORE, a,
+                                       c->num_sms, c->stream, &grid));
+            c->launches += 2;
+            det_finish(f, a, grid);
+            det_encode_bwd(f, X, B_local, dY);
         } else {
             const size_t LF = size_t(f->shape.in_real);
             float* Y = static_cast<float*>(c->s2.get(size_t(B_local) * LF * 4));
@@ -818,6 +877,16 @@ nfg_status nfg_field_device_buffer(nfg_field* f, int32_t which, float** dev, uin
     });
 }
 
+nfg_status nfg_field_get_config(const nfg_field* f, nfg_grid_config* grid, nfg_mlp_config* mlp)
+{
+    return guard([&] {
+        if (grid)
+            *grid = f->gcfg;
+        if (mlp)
+            *mlp = f->mcfg;
+    });
+}
+
 nfg_status nfg_field_get_step(const nfg_field* f, uint64_t* step)
 {
     return guard([&] { *step = f->step; });
@@ -836,7 +905,7 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
         const int d = f->gcfg.dims, no = f->mcfg.output_width;
         const uint64_t before = f->step;
         const bool was_clean = f->grads_clean;
-        if (f->grads_clean && f->opts.fused_train && c->write_value32 && B >= (int64_t(1) << 15) &&
+        if (f->grads_clean && f->opts.fused_train && !f->opts.deterministic && c->write_value32 && B >= (int64_t(1) << 15) &&
             is_pinned(X) && is_pinned(target)) {
             // Overlap the H2D of the batch with the step: the chunk copies and
             // their ready flags are enqueued on the copy stream FIRST, then the
@@ -1004,8 +1073,13 @@ nfg_status nfg_encode_backward(nfg_field* f, const float* X, int64_t B, const fl
         validate_inputs(X, B, f->gcfg.dims);
         const float* dX = stage(c->s0, X, size_t(B) * f->gcfg.dims, c->stream);
         const float* ddY = stage(c->s1, dY, size_t(B) * f->shape.in_real, c->stream);
-        NFG_CUDA(nfg::launch_encode_bwd_lv(f->shape, f->d_levels, dX, B, ddY, f->d_g, c->stream));
-        c->launches++;
+        if (f->opts.deterministic) {
+            reset_scratch(f);
+            det_encode_bwd(f, dX, B, ddY);
+        } else {
+            NFG_CUDA(nfg::launch_encode_bwd_lv(f->shape, f->d_levels, dX, B, ddY, f->d_g, c->stream));
+            c->launches++;
+        }
         f->grads_clean = false;
         NFG_CUDA(cudaStreamSynchronize(c->stream));
     });
@@ -1050,9 +1124,14 @@ nfg_status nfg_mlp_backward(nfg_field* f, const float* Y, int64_t B, const float
         a.gW = f->d_g + f->n_tab_dev;
         a.gb = f->d_g + f->n_tab_dev + f->n_w;
         a.scratch = scratch_of(f);
+        if (f->opts.deterministic)
+            det_prepare(f, a, B, false);
+        int grid = 0;
         NFG_CUDA(nfg::launch_train(f->shape, nullptr, nfg::SRC_LOAD_Y, nfg::GRAD_DOUT, nfg::SINK_STORE, a, c->num_sms,
-                                   c->stream, nullptr));
+                                   c->stream, &grid));
         c->launches++;
+        if (f->opts.deterministic)
+            det_finish(f, a, grid);
         f->grads_clean = false;
         if (B > 0)
             NFG_CUDA(cudaMemcpyAsync(dY, ddY, size_t(B) * f->shape.in_real * 4, cudaMemcpyDeviceToHost, c->stream));

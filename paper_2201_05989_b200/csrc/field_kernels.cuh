@@ -214,6 +214,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
 
     bool bad = false;
     unsigned int invalid = 0u;
+    double loss_acc = 0.0;   // deterministic mode (lane 0 of each warp)
     NFG_PT_DECL
     const int64_t ntiles = (a.B + TS - 1) / TS;
     const int r0 = 16 * warp;
@@ -347,8 +348,12 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         }
         if (lane == 0) {
             red[warp] = mx;
-            if (GRAD == GRAD_LOSS)
-                atomicAdd(a.scratch.loss_sum, double(term));
+            if (GRAD == GRAD_LOSS) {
+                if (a.part_loss)
+                    loss_acc += double(term);
+                else
+                    atomicAdd(a.scratch.loss_sum, double(term));
+            }
         }
         __syncthreads();
         NFG_PT(2);
@@ -493,7 +498,10 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 if (m < out_k && n < in_k) {
                     const float v = cq[q][e] * ic;
                     bad |= !sane(v);
-                    atomicAdd(a.gW + woff + m + size_t(n) * out_k, v);
+                    if (a.part_wb)
+                        a.part_wb[blockIdx.x * a.n_wb + woff + m + size_t(n) * out_k] = v;
+                    else
+                        atomicAdd(a.gW + woff + m + size_t(n) * out_k, v);
                 }
             }
     };
@@ -522,7 +530,10 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 for (int h = 0; h < 2; ++h) {
                     const float v = dbh[k][h] * ic;
                     bad |= !sane(v);
-                    atomicAdd(a.gb + k * H + 16 * warp + g + 8 * h, v);
+                    if (a.part_wb)
+                        a.part_wb[blockIdx.x * a.n_wb + a.n_w + k * H + 16 * warp + g + 8 * h] = v;
+                    else
+                        atomicAdd(a.gb + k * H + 16 * warp + g + 8 * h, v);
                 }
         if (warp == TW - 1)
 #pragma unroll
@@ -530,9 +541,14 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 if (g + 8 * h < s.n_out) {
                     const float v = dbo[h] * ic;
                     bad |= !sane(v);
-                    atomicAdd(a.gb + NH * H + g + 8 * h, v);
+                    if (a.part_wb)
+                        a.part_wb[blockIdx.x * a.n_wb + a.n_w + NH * H + g + 8 * h] = v;
+                    else
+                        atomicAdd(a.gb + NH * H + g + 8 * h, v);
                 }
     }
+    if (GRAD == GRAD_LOSS && a.part_loss && lane == 0)
+        a.part_loss[blockIdx.x * TW + warp] = loss_acc;
     if (__any_sync(0xffffffffu, bad) && lane == 0)
         atomicOr(a.scratch.flags, 1u);
     invalid = __reduce_or_sync(0xffffffffu, invalid);

@@ -61,6 +61,12 @@ struct TrainArgs {
     // invalid batch (flags[3], abort flags[1]); Adam's check kernel then
     // restores the (clean) gradient slab, so no state changes.
     int validate;
+    // Deterministic mode (nfg_options.deterministic): per-CTA partials instead
+    // of float atomics. part_wb[cta * n_wb + i] (i over [W | b], pre-zeroed),
+    // part_loss[cta * TW + warp]; reduced in CTA order by launch_reduce_partials.
+    float* part_wb;
+    double* part_loss;
+    int64_t n_w, n_wb;
 };
 
 struct InferArgs {
@@ -99,6 +105,13 @@ struct AdamArgs {
 cudaError_t launch_adam(const AdamArgs& a, bool force_check, int num_sms, cudaStream_t st);
 cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cudaStream_t st);
 cudaError_t launch_shadow(const float* p, __half* shadow, uint64_t n, cudaStream_t st);
+size_t encode_bwd_det_scratch(int64_t B, int d);
+cudaError_t launch_encode_bwd_det(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
+                                  const float* dY, float* grads, const unsigned int* flags, void* scratch,
+                                  size_t bytes, cudaStream_t st);
+cudaError_t launch_reduce_partials(const float* part, int nparts, int64_t n, float* out, const double* part_loss,
+                                   int nloss, double* loss_sum, const unsigned int* flags, cudaStream_t st);
+int train_warps_per_cta();
 cudaError_t launch_loss(int kind, const float* pred, const float* target, int64_t n, float count, float* dpred,
                         double* loss_sum, cudaStream_t st);
 

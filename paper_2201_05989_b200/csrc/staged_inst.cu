@@ -51,6 +51,8 @@ cudaError_t launch_train(const FieldShape& s, const LevelDev* lv, int src, int g
     return launch_staged_train(s, grad, a, num_sms, st, grid_used);
 }
 
+int train_warps_per_cta() { return TW; }
+
 cudaError_t launch_infer(const FieldShape& s, const LevelDev* lv, int src, const InferArgs& a, int num_sms,
                          cudaStream_t st)
 {

@@ -20,6 +20,7 @@ reference but not built for sm_100a, e.g. hidden_width != 64).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -164,9 +165,10 @@ class Options:
     """sm_100a build options (no reference equivalent)."""
     table_fp32: bool = False    # gather fp32 master tables instead of the fp16 shadow
     fused_train: bool = True    # one fused kernel per step vs staged encode / MLP / encode-bwd kernels
+    deterministic: bool = False  # bit-reproducible backward in the reference's accumulation order (SPEC.md:139)
 
     def c(self) -> L.nfg_options:
-        return L.nfg_options(int(self.table_fp32), int(self.fused_train))
+        return L.nfg_options(int(self.table_fp32), int(self.fused_train), int(self.deterministic))
 
 
 class Context:
@@ -477,6 +479,77 @@ def loss_with_grad(kind: LossKind, pred, target, ctx: Optional[Context] = None):
     out = C.c_float()
     L.check(ctx.lib.nfg_loss(ctx.h, int(kind), _ptr(p), _ptr(t), p.size, p.size, _ptr(d), C.byref(out)))
     return float(out.value), d
+
+
+# ---- checkpoint + train report (io.cpp:189-351) --------------------------------
+def save_checkpoint(model: "FieldModel", path: str) -> None:   # io.cpp:222-285
+    """NFC1/HGE1/MLP1/ADM1 bytes, loadable by the reference's load_checkpoint."""
+    L.check(model.lib.nfg_field_save(model.h, os.fsencode(path)))
+
+
+def load_checkpoint(model: "FieldModel", path: str) -> None:   # io.cpp:287-351
+    """Replaces the model's configs, parameters and Adam state with the file's;
+    ``model.hyper`` / ``schedule`` / ``options`` are kept (re-supplied by the
+    caller on resume, test_tasks.cpp:313-315)."""
+    h = C.c_void_p()
+    L.check(model.lib.nfg_field_load(model.ctx.h, os.fsencode(path), C.byref(model.hyper.c()),
+                                     C.byref(model.options.c()), C.byref(h)))
+    model.close()
+    model.h = h
+    g, m = L.nfg_grid_config(), L.nfg_mlp_config()
+    L.check(model.lib.nfg_field_get_config(h, C.byref(g), C.byref(m)))
+    model.hash_cfg = HashEncodingConfig(g.levels, g.table_size, g.features, g.n_min, g.n_max, g.dims,
+                                        Interpolation(g.interpolation))
+    model.mlp_cfg = MlpConfig(m.input_width, m.hidden_layers, m.hidden_width, m.output_width,
+                              OutputActivation(m.output_activation))
+    sz = (C.c_uint64 * 3)()
+    L.check(model.lib.nfg_field_sizes(h, sz))
+    model._sizes = tuple(int(x) for x in sz)
+    model._push_schedule()
+
+
+@dataclass
+class TrainReportRow:   # io.hpp:25-31
+    step: int = 0
+    time_s: float = 0.0
+    loss: float = 0.0
+    metric: float = 0.0
+    lr: float = 0.0
+
+
+@dataclass
+class TrainReport:   # io.hpp:33-35
+    rows: List[TrainReportRow] = field(default_factory=list)
+
+
+def _g10(v) -> str:
+    """C++ ostream with precision(10) (default float format) == printf %.10g."""
+    return "%.10g" % v
+
+
+def write_report_csv(report: TrainReport, path: str) -> None:   # io.cpp:189-199
+    try:
+        with open(path, "w") as out:
+            out.write("step,time_s,loss,metric,lr\n")
+            for r in report.rows:
+                out.write(f"{int(r.step)},{_g10(r.time_s)},{_g10(r.loss)},{_g10(r.metric)},{_g10(r.lr)}\n")
+    except OSError:
+        raise L.NfgIOError(L.NFG_EIO, "cannot write report: " + path) from None
+
+
+def read_report_csv(path: str) -> TrainReport:   # io.cpp:201-220
+    try:
+        with open(path) as f:
+            lines = f.read().splitlines()
+    except OSError:
+        raise L.NfgIOError(L.NFG_EIO, "cannot read report: " + path) from None
+    rep = TrainReport()
+    for line in lines[1:]:
+        if not line:
+            continue
+        a = line.split(",")
+        rep.rows.append(TrainReportRow(int(a[0]), float(a[1]), float(a[2]), float(a[3]), float(a[4])))
+    return rep
 
 
 class PinnedBuffer:
