@@ -165,6 +165,20 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
 nfg_status nfg_field_train_step_device(nfg_field* f, const float* X, const float* target,
                                        int64_t B_local, int64_t B_global, int32_t loss_kind,
                                        int64_t step, float* loss_dev);
+/* Per-step status of asynchronous device steps, for loops that check lazily
+ * (nfg_fit_image): nfg_field_step_record copies the step's 32-byte device
+ * scratch (loss sum + abort flags) into rec_dev, stream-ordered after the last
+ * enqueued step; nfg_step_record_check turns a host copy of it into exactly
+ * what the synchronous train_step would have done: the same error (EINVAL for
+ * invalid input, ENONFINITE naming the group) or the step's loss. */
+typedef struct {
+    double loss_sum;
+    uint32_t flags[4];
+    float dy_max;
+    float pad;
+} nfg_step_record;
+nfg_status nfg_field_step_record(nfg_field* f, nfg_step_record* rec_dev);
+nfg_status nfg_step_record_check(nfg_field* f, const nfg_step_record* rec, int64_t B_global, float* loss);
 /* Forward + loss + backward of train_step WITHOUT the Adam update: gradients
  * accumulate into the field's grad slab (mlp_backward / encode_backward
  * semantics, mlp.hpp:147-148, grid.hpp:292); pair with nfg_adam_step. */
@@ -213,6 +227,59 @@ double nfg_lr_at(const int64_t* milestones, int32_t n, double factor, double bas
 nfg_status nfg_field_save(nfg_field* f, const char* path);
 nfg_status nfg_field_load(nfg_ctx* ctx, const char* path, const nfg_adam_hyper* hyper, const nfg_options* opts,
                           nfg_field** out);
+
+/* ---- training-loop data path on the device (tasks.cpp) ---
+ * nfg_rng: the reference's Pcg32 (pcg32.hpp) as a device stream. Draws are
+ * generated in parallel by jump-ahead, bit-identical to the sequential host
+ * generator INCLUDING next_below's rejection sampling: n draws advance the
+ * stream exactly as n host calls would. Asynchronous on the context stream;
+ * nfg_rng_get_state synchronises. */
+typedef struct nfg_rng nfg_rng;
+nfg_status nfg_rng_create(nfg_ctx* ctx, uint64_t seed, uint64_t seq, nfg_rng** out);   /* Pcg32(seed, seq) */
+nfg_status nfg_rng_destroy(nfg_rng* r);
+nfg_status nfg_rng_below_device(nfg_rng* r, uint32_t bound, int64_t n, uint32_t* out_dev);   /* next_below x n */
+nfg_status nfg_rng_floats_device(nfg_rng* r, int64_t n, float* out_dev);                     /* next_float x n */
+nfg_status nfg_rng_get_state(nfg_rng* r, uint64_t* state, uint64_t* inc);
+
+/* fit_image's batch assembly (tasks.cpp:114-120): pixel p -> X = (((p % w) +
+ * 0.5) / w, ((p / w) + 0.5) / h) in fp32, T = rgb column p (rgb: 3 x w*h,
+ * the reference's Image::rgb). idx_dev == NULL means p = i. */
+nfg_status nfg_image_batch_device(nfg_ctx* ctx, const uint32_t* idx_dev, int64_t n, const float* rgb_dev,
+                                  int32_t width, int32_t height, float* X_dev, float* T_dev);
+
+/* ImageTask (tasks.hpp:16-31) for the hash encoder; cfg.dims is forced to 2,
+ * cfg.n_max <= 0 means width / 2, cfg.interpolation is task.interpolation. */
+typedef struct {
+    int32_t width, height;
+    nfg_grid_config cfg;
+    int32_t hidden_layers;
+    int32_t hidden_width;
+    int32_t batch_size;
+    int64_t total_steps;
+    int64_t log_interval;
+    double lr;
+    double lr_decay;
+} nfg_image_task;
+
+/* TrainReportRow (io.hpp:25-31). */
+typedef struct {
+    int64_t step;
+    double time_s;
+    double loss;
+    double metric;
+    double lr;
+} nfg_report_row;
+
+/* fit_image (tasks.cpp:49-131) with every step on the device: batches drawn
+ * from Pcg32(seed, 1) on the GPU (identical pixel sequence), PSNR rows on the
+ * full image (<= 2^20 pixels) or 2^16 pixels from Pcg32(seed, 7). The model is
+ * returned in *model_out (destroy with nfg_field_destroy); up to rows_cap
+ * report rows are written, *n_rows = rows produced. Errors as the reference:
+ * EINVAL ("fit_image: image must be at least 2x2"), ENONFINITE ("fit_image:
+ * non-finite loss at step N" / adam_step's non-finite gradient). */
+nfg_status nfg_fit_image(nfg_ctx* ctx, const nfg_image_task* task, const float* rgb, uint64_t seed,
+                         const nfg_options* opts, nfg_field** model_out, nfg_report_row* rows, int64_t rows_cap,
+                         int64_t* n_rows);
 
 nfg_status nfg_host_alloc(size_t bytes, void** out);
 nfg_status nfg_host_free(void* p);

@@ -39,6 +39,21 @@ class nfg_options(C.Structure):
     _fields_ = [("table_fp32", C.c_int32), ("fused_train", C.c_int32), ("deterministic", C.c_int32)]
 
 
+class nfg_image_task(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("cfg", nfg_grid_config),
+                ("hidden_layers", C.c_int32), ("hidden_width", C.c_int32), ("batch_size", C.c_int32),
+                ("total_steps", C.c_int64), ("log_interval", C.c_int64), ("lr", C.c_double), ("lr_decay", C.c_double)]
+
+
+class nfg_report_row(C.Structure):
+    _fields_ = [("step", C.c_int64), ("time_s", C.c_double), ("loss", C.c_double), ("metric", C.c_double),
+                ("lr", C.c_double)]
+
+
+class nfg_step_record(C.Structure):
+    _fields_ = [("loss_sum", C.c_double), ("flags", C.c_uint32 * 4), ("dy_max", C.c_float), ("pad", C.c_float)]
+
+
 _vp = C.c_void_p
 _fp = C.POINTER(C.c_float)
 _u32p = C.POINTER(C.c_uint32)
@@ -90,6 +105,16 @@ SIGNATURES = {
     "nfg_lr_at": (C.c_double, [_i64p, C.c_int32, C.c_double, C.c_double, C.c_int64]),
     "nfg_field_save": (C.c_int, [_vp, C.c_char_p]),
     "nfg_field_load": (C.c_int, [_vp, C.c_char_p, C.POINTER(nfg_adam_hyper), C.POINTER(nfg_options), C.POINTER(_vp)]),
+    "nfg_field_step_record": (C.c_int, [_vp, _vp]),
+    "nfg_step_record_check": (C.c_int, [_vp, C.POINTER(nfg_step_record), C.c_int64, _fp]),
+    "nfg_rng_create": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.POINTER(_vp)]),
+    "nfg_rng_destroy": (C.c_int, [_vp]),
+    "nfg_rng_below_device": (C.c_int, [_vp, C.c_uint32, C.c_int64, _vp]),
+    "nfg_rng_floats_device": (C.c_int, [_vp, C.c_int64, _vp]),
+    "nfg_rng_get_state": (C.c_int, [_vp, _u64p, _u64p]),
+    "nfg_image_batch_device": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp, _vp]),
+    "nfg_fit_image": (C.c_int, [_vp, C.POINTER(nfg_image_task), _vp, C.c_uint64, C.POINTER(nfg_options),
+                                C.POINTER(_vp), C.POINTER(nfg_report_row), C.c_int64, _i64p]),
     "nfg_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
     "nfg_host_free": (C.c_int, [_vp]),
 }

@@ -377,4 +377,19 @@ cudaError_t launch_loss(int kind, const float* pred, const float* target, int64_
     return cudaGetLastError();
 }
 
+// ---- loss of an asynchronous device step (nfg_field_train_step_device) --------
+// train_step's return value: float(loss_sum / count) (model.cpp:111-138), NaN
+// when the step aborted (the host call would have thrown instead).
+__global__ void k_loss_out(const double* loss_sum, const unsigned int* flags, double count, float* out)
+{
+    *out = flags[1] ? __int_as_float(0x7fffffff) : (count > 0 ? float(*loss_sum / count) : 0.0f);
+}
+
+cudaError_t launch_loss_out(const double* loss_sum, const unsigned int* flags, double count, float* out,
+                            cudaStream_t st)
+{
+    k_loss_out<<<1, 1, 0, st>>>(loss_sum, flags, count, out);
+    return cudaGetLastError();
+}
+
 }   // namespace nfg

@@ -987,10 +987,42 @@ nfg_status nfg_field_train_step_device(nfg_field* f, const float* X, const float
                                        int64_t B_global, int32_t loss_kind, int64_t step, float* loss_dev)
 {
     return guard([&] {
-        (void)loss_dev;
         device_train_step(f, X, target, B_local, B_global, loss_kind, step);
         f->pending_steps++;
         f->grads_clean = true;   // optimistic; nfg_field_check corrects it
+        if (loss_dev) {
+            NFG_CUDA(nfg::launch_loss_out(&f->d_res->loss_sum, f->d_res->flags,
+                                          double(B_global) * f->mcfg.output_width, loss_dev, f->ctx->stream));
+            f->ctx->launches++;
+        }
+    });
+}
+
+static_assert(sizeof(StepResult) == sizeof(nfg_step_record), "nfg_step_record mirrors the device scratch");
+
+nfg_status nfg_field_step_record(nfg_field* f, nfg_step_record* rec_dev)
+{
+    return guard([&] {
+        NFG_CUDA(cudaMemcpyAsync(rec_dev, f->d_res, sizeof(StepResult), cudaMemcpyDeviceToDevice, f->ctx->stream));
+    });
+}
+
+nfg_status nfg_step_record_check(nfg_field* f, const nfg_step_record* rec, int64_t B_global, float* loss)
+{
+    return guard([&] {
+        StepResult saved = *f->h_res;
+        std::memcpy(f->h_res, rec, sizeof(StepResult));
+        try {
+            if (f->h_res->flags[1])
+                raise_if_aborted(f);
+        } catch (...) {
+            *f->h_res = saved;
+            throw;
+        }
+        *f->h_res = saved;
+        const double count = double(B_global) * f->mcfg.output_width;
+        if (loss)
+            *loss = count > 0 ? float(rec->loss_sum / count) : 0.0f;
     });
 }
 

@@ -552,6 +552,99 @@ def read_report_csv(path: str) -> TrainReport:   # io.cpp:201-220
     return rep
 
 
+# ---- training-loop data path on the device (tasks.cpp) -------
+class DeviceRng:
+    """Pcg32(seed, seq) (pcg32.hpp) as a device stream: ``below`` / ``floats``
+    fill device buffers (torch CUDA tensors or pointers) with exactly the draws
+    of n sequential host calls (rejection sampling included)."""
+
+    def __init__(self, seed: int, seq: int = 1, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        h = C.c_void_p()
+        L.check(self.lib.nfg_rng_create(self.ctx.h, seed, seq, C.byref(h)))
+        self.h = h
+
+    def below(self, bound: int, n: int, out) -> None:   # next_below x n (pcg32.hpp:30-38)
+        L.check(self.lib.nfg_rng_below_device(self.h, bound, n, _dptr(out)))
+
+    def floats(self, n: int, out) -> None:   # next_float x n (pcg32.hpp:41-44)
+        L.check(self.lib.nfg_rng_floats_device(self.h, n, _dptr(out)))
+
+    def state(self):
+        s, i = C.c_uint64(), C.c_uint64()
+        L.check(self.lib.nfg_rng_get_state(self.h, C.byref(s), C.byref(i)))
+        return int(s.value), int(i.value)
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.nfg_rng_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class ImageTask:   # tasks.hpp:16-31 (hash encoder)
+    image: np.ndarray = None          # (w*h, 3) float32, pixel i = y*w + x (Image::rgb, io.hpp:12-19)
+    width: int = 0
+    height: int = 0
+    cfg: HashEncodingConfig = field(default_factory=lambda: HashEncodingConfig(n_max=0))   # n_max <= 0: width/2
+    interpolation: Interpolation = Interpolation.Linear
+    hidden_layers: int = 2
+    hidden_width: int = 64
+    batch_size: int = 1 << 14
+    total_steps: int = 10000
+    log_interval: int = 1000
+    lr: float = 1e-2
+    lr_decay: float = 0.33
+
+
+@dataclass
+class FitResult:   # tasks.hpp:58-61
+    model: "FieldModel"
+    report: TrainReport
+
+
+def fit_image(task: ImageTask, seed: int, options: Optional[Options] = None,
+              ctx: Optional[Context] = None) -> FitResult:   # tasks.cpp:49-131, all steps on the device
+    ctx = ctx or default_context()
+    rgb = _f32(task.image)
+    if rgb.shape != (task.width * task.height, 3):
+        raise L.NfgInvalidArgument(L.NFG_EINVAL, "fit_image: image shape does not match width x height")
+    cfg = HashEncodingConfig(task.cfg.levels, task.cfg.table_size, task.cfg.features, task.cfg.n_min,
+                             task.cfg.n_max, 2, task.interpolation)
+    t = L.nfg_image_task(task.width, task.height, cfg.c(), task.hidden_layers, task.hidden_width, task.batch_size,
+                         task.total_steps, task.log_interval, task.lr, task.lr_decay)
+    cap = task.total_steps // max(task.log_interval, 1) + 2
+    rows = (L.nfg_report_row * cap)()
+    n = C.c_int64()
+    h = C.c_void_p()
+    opts = options or Options()
+    L.check(ctx.lib.nfg_fit_image(ctx.h, C.byref(t), _ptr(rgb), seed, C.byref(opts.c()), C.byref(h), rows, cap,
+                                  C.byref(n)))
+    model = FieldModel(ctx, opts)
+    model.h = h
+    g, m = L.nfg_grid_config(), L.nfg_mlp_config()
+    L.check(ctx.lib.nfg_field_get_config(h, C.byref(g), C.byref(m)))
+    model.hash_cfg = HashEncodingConfig(g.levels, g.table_size, g.features, g.n_min, g.n_max, g.dims,
+                                        Interpolation(g.interpolation))
+    model.mlp_cfg = MlpConfig(m.input_width, m.hidden_layers, m.hidden_width, m.output_width,
+                              OutputActivation(m.output_activation))
+    model.hyper = AdamHyper(lr=task.lr)
+    model.schedule = default_schedule(task.total_steps, task.lr_decay)
+    sz = (C.c_uint64 * 3)()
+    L.check(ctx.lib.nfg_field_sizes(h, sz))
+    model._sizes = tuple(int(x) for x in sz)
+    rep = TrainReport([TrainReportRow(int(r.step), r.time_s, r.loss, r.metric, r.lr)
+                       for r in rows[:min(n.value, cap)]])
+    return FitResult(model, rep)
+
+
 class PinnedBuffer:
     """Page-locked host memory (cudaMallocHost) viewed as a numpy array."""
 

@@ -1,0 +1,141 @@
+"""Training-loop data path on the device (tasks.cpp:49-131).
+
+* the device Pcg32 stream is bit-identical to the host generator (pcg32.hpp),
+  including next_below's rejection sampling and stream continuity;
+* fit_image's batch assembly (pixel -> x, target) is bit-identical to the
+  reference's float arithmetic;
+* nf.fit_image (every step on the device) takes exactly the steps of a
+  host-driven fit_image loop on the same model (deterministic mode: parameters
+  bit-identical), and its report rows follow the reference's schedule.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from test_gpu_parity import _nf
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@pytest.mark.parametrize("bound", [1 << 20, 7700, (1 << 31) + 1, 3000000019, 3, 1])
+def test_rng_below_matches_host_stream(bound):   # pcg32.hpp:30-38
+    nf = _nf()
+    torch = _torch()
+    r = nf.DeviceRng(1337, 1)
+    host = O.Pcg32(1337, 1)
+    for n in (5000, 1, 0, 4099):
+        out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        r.below(bound, n, out)
+        got = out[:n].cpu().numpy().view(np.uint32)
+        want = np.array([host.next_below(bound) for _ in range(n)], np.uint32)
+        assert np.array_equal(got, want), (bound, n)
+
+
+def test_rng_floats_matches_host_stream():   # pcg32.hpp:41-44
+    nf = _nf()
+    torch = _torch()
+    r = nf.DeviceRng(7, 3)
+    host = O.Pcg32(7, 3)
+    for n in (100003, 17):
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+        r.floats(n, out)
+        assert np.array_equal(out.cpu().numpy(), host.floats(n))
+
+
+def test_image_batch_bit_exact():   # tasks.cpp:114-120
+    nf = _nf()
+    torch = _torch()
+    w, h, B = 100, 77, 3000
+    rgb = O.make_test_image(w, h)
+    ctx = nf.default_context()
+    r = nf.DeviceRng(42, 1)
+    idx = torch.empty(B, dtype=torch.int32, device="cuda")
+    r.below(w * h, B, idx)
+    rgb_d = torch.from_numpy(rgb).cuda()
+    X = torch.empty(B, 2, device="cuda")
+    T = torch.empty(B, 3, device="cuda")
+    from paper_2201_05989_b200 import _lib as L
+    L.check(ctx.lib.nfg_image_batch_device(ctx.h, idx.data_ptr(), B, rgb_d.data_ptr(), w, h, X.data_ptr(),
+                                           T.data_ptr()))
+    Xo, To = O.Pcg32(42, 1).image_batch(rgb, w, h, B)
+    assert np.array_equal(X.cpu().numpy().view(np.uint32), Xo.view(np.uint32))
+    assert np.array_equal(T.cpu().numpy(), To)
+
+
+def _task(nf, w, h, steps=60, log=20, batch=1 << 11):
+    return nf.ImageTask(image=O.make_test_image(w, h), width=w, height=h,
+                        cfg=nf.HashEncodingConfig(levels=8, table_size=1 << 12, features=2, n_min=8, n_max=0),
+                        batch_size=batch, total_steps=steps, log_interval=log, lr=1e-2)
+
+
+def test_fit_image_device_loop_equals_host_loop():   # tasks.cpp:49-131
+    nf = _nf()
+    from _tasks import fit_image as host_fit_image
+    w, h, seed = 64, 48, 9
+    task = _task(nf, w, h)
+    res = nf.fit_image(task, seed, nf.Options(deterministic=True))
+    # the same model trained by the host-side restatement of the loop
+    m = nf.FieldModel(options=nf.Options(deterministic=True))
+    m.hash_cfg = nf.HashEncodingConfig(levels=8, table_size=1 << 12, features=2, n_min=8, n_max=w // 2, dims=2)
+    m.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=3,
+                             output_activation=nf.OutputActivation.Sigmoid)
+    m.hyper = nf.AdamHyper(lr=1e-2)
+    m.schedule = nf.default_schedule(task.total_steps)
+    m.init(seed)
+    rows = host_fit_image(m, task.image, w, h, seed, task.batch_size, task.total_steps, task.log_interval)
+    assert [r.step for r in res.report.rows] == [r[0] for r in rows] == [0, 20, 40, 60]
+    assert np.array_equal(res.model.params.view(np.uint32), m.params.view(np.uint32))
+    for r, (s, loss, psnr) in zip(res.report.rows, rows):
+        if s > 0:
+            assert r.loss == pytest.approx(loss, rel=1e-6)
+        assert r.metric == pytest.approx(psnr, abs=1e-4)
+        assert r.lr == nf.lr_at(m.schedule, 1e-2, s)
+        assert r.time_s >= 0
+    assert res.model.hash_cfg.n_max == w // 2 and res.model.mlp_cfg.output_width == 3
+
+
+def test_fit_image_against_oracle_curve():   # fit_image on the oracle, identical batch stream
+    nf = _nf()
+    from _tasks import fit_image as host_fit_image
+    w, h, seed = 64, 64, 3
+    task = _task(nf, w, h, steps=100, log=25)
+    res = nf.fit_image(task, seed)
+    f = O.Field(O.GridCfg(levels=8, table_size=1 << 12, features=2, n_min=8, n_max=w // 2, dims=2),
+                O.MlpCfg(hidden_layers=2, hidden_width=64, output_width=3, sigmoid=True), O.Hyper(lr=1e-2))
+    f.init(seed)
+    f.set_schedule(O.default_milestones(task.total_steps))
+    rows = host_fit_image(f, task.image, w, h, seed, task.batch_size, task.total_steps, task.log_interval)
+    mse = lambda p: 10 ** (-p / 10)   # noqa: E731
+    assert res.report.rows[0].metric == pytest.approx(rows[0][2], abs=1e-3)   # identical init
+    assert abs(mse(res.report.rows[1].metric) - mse(rows[1][2])) <= 0.05 * mse(rows[1][2])
+    assert res.report.rows[-1].metric > 30 and rows[-1][2] > 30
+
+
+def test_fit_image_large_image_eval_subset():   # tasks.cpp:78-87 (2^16 pixels from Pcg32(seed, 7))
+    nf = _nf()
+    from _tasks import eval_grid
+    w, h, seed = 1100, 1000, 5
+    task = _task(nf, w, h, steps=2, log=1, batch=256)
+    res = nf.fit_image(task, seed)
+    m = nf.FieldModel()
+    m.hash_cfg = nf.HashEncodingConfig(levels=8, table_size=1 << 12, features=2, n_min=8, n_max=w // 2, dims=2)
+    m.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=3,
+                             output_activation=nf.OutputActivation.Sigmoid)
+    m.init(seed)
+    ex, pix = eval_grid(w, h, seed)
+    assert ex.shape[0] == 1 << 16
+    pred = m.evaluate(ex)
+    assert res.report.rows[0].metric == pytest.approx(O.psnr(pred, task.image[pix]), abs=1e-6)
+    assert [r.step for r in res.report.rows] == [0, 1, 2]
+
+
+def test_fit_image_rejects_tiny_image():   # tasks.cpp:52-53
+    nf = _nf()
+    t = _task(nf, 1, 5)
+    with pytest.raises(ValueError, match="at least 2x2"):
+        nf.fit_image(t, 1)
