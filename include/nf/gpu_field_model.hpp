@@ -13,7 +13,10 @@
 // std::runtime_error (non-finite gradient in adam_step), std::logic_error.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <fstream>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -201,6 +204,42 @@ public:
 
     nfg_field* handle() const { return f_; }
 
+    // save_checkpoint / load_checkpoint (io.cpp:222-351), NFC1 bytes. load
+    // replaces hash_cfg / mlp_cfg with the file's and keeps hyper / schedule /
+    // options (re-supplied by the caller on resume, test_tasks.cpp:313-315).
+    void save_checkpoint(const std::string& path) const { check(nfg_field_save(f_, path.c_str())); }
+    void load_checkpoint(const std::string& path)
+    {
+        const nfg_adam_hyper h = to_c_hyper(hyper);
+        nfg_field* nf_ = nullptr;
+        check(nfg_field_load(ctx_.get(), path.c_str(), &h, &options, &nf_));
+        adopt(nf_);
+    }
+
+    // Takes ownership of a field created by the C ABI (nfg_fit_image, load).
+    void adopt(nfg_field* f)
+    {
+        if (f_)
+            nfg_field_destroy(f_);
+        f_ = f;
+        nfg_grid_config g{};
+        nfg_mlp_config m{};
+        check(nfg_field_get_config(f_, &g, &m));
+        hash_cfg.levels = g.levels;
+        hash_cfg.table_size = g.table_size;
+        hash_cfg.features = g.features;
+        hash_cfg.n_min = g.n_min;
+        hash_cfg.n_max = g.n_max;
+        hash_cfg.dims = g.dims;
+        hash_cfg.interpolation = decltype(hash_cfg.interpolation)(g.interpolation);
+        mlp_cfg.input_width = m.input_width;
+        mlp_cfg.hidden_layers = m.hidden_layers;
+        mlp_cfg.hidden_width = m.hidden_width;
+        mlp_cfg.output_width = m.output_width;
+        mlp_cfg.output_activation = decltype(mlp_cfg.output_activation)(m.output_activation);
+        push_run_config();
+    }
+
 private:
     void push_run_config()
     {
@@ -225,6 +264,88 @@ float loss_with_grad(Context& ctx, int kind, const M& pred, const M& target, M& 
     float loss = 0.0f;
     check(nfg_loss(ctx.get(), kind, pred.data(), target.data(), n, n, dPred.data(), &loss));
     return loss;
+}
+
+// TrainReport CSV (io.cpp:189-220), the reference's exact schema.
+struct ReportRow {
+    std::int64_t step = 0;
+    double time_s = 0, loss = 0, metric = 0, lr = 0;
+};
+
+inline void write_report_csv(const std::vector<ReportRow>& rows, const std::string& path)
+{
+    std::ofstream out(path);
+    if (!out)
+        throw std::runtime_error("cannot write report: " + path);
+    out << "step,time_s,loss,metric,lr\n";
+    out.precision(10);
+    for (const auto& r : rows)
+        out << r.step << ',' << r.time_s << ',' << r.loss << ',' << r.metric << ',' << r.lr << '\n';
+}
+
+inline std::vector<ReportRow> read_report_csv(const std::string& path)
+{
+    std::ifstream in(path);
+    if (!in)
+        throw std::runtime_error("cannot read report: " + path);
+    std::vector<ReportRow> rows;
+    std::string line;
+    std::getline(in, line);
+    while (std::getline(in, line)) {
+        if (line.empty())
+            continue;
+        ReportRow r;
+        char comma;
+        std::istringstream ss(line);
+        ss >> r.step >> comma >> r.time_s >> comma >> r.loss >> comma >> r.metric >> comma >> r.lr;
+        rows.push_back(r);
+    }
+    return rows;
+}
+
+// fit_image (tasks.cpp:49-131) with every step on the device. `rgb` is the
+// reference's Image::rgb (3 x w*h column-major); Task reads ImageTask by member
+// name (cfg, interpolation, hidden_layers, hidden_width, batch_size,
+// total_steps, log_interval, lr, lr_decay). The trained field is adopted by
+// `model`; returns the report rows.
+template <class Task, class Model>
+std::vector<ReportRow> fit_image(Context& ctx, const Task& task, const float* rgb, int width, int height,
+                                 std::uint64_t seed, Model& model)
+{
+    nfg_image_task t{};
+    t.width = width;
+    t.height = height;
+    t.cfg = to_c_grid(task.cfg);
+    t.cfg.interpolation = int32_t(task.interpolation);
+    t.hidden_layers = task.hidden_layers;
+    t.hidden_width = task.hidden_width;
+    t.batch_size = task.batch_size;
+    t.total_steps = task.total_steps;
+    t.log_interval = task.log_interval;
+    t.lr = task.lr;
+    t.lr_decay = task.lr_decay;
+    const std::int64_t cap = task.total_steps / std::max<std::int64_t>(task.log_interval, 1) + 2;
+    std::vector<nfg_report_row> rows(static_cast<size_t>(cap));
+    std::int64_t n = 0;
+    nfg_field* f = nullptr;
+    check(nfg_fit_image(ctx.get(), &t, rgb, seed, &model.options, &f, rows.data(), cap, &n));
+    model.hyper.lr = task.lr;
+    model.schedule.milestones.clear();
+    {   // default_schedule (adam.hpp:150-161)
+        std::int64_t next = std::int64_t(0.65 * double(task.total_steps));
+        const std::int64_t stride = std::int64_t(0.30 * double(task.total_steps));
+        while (next < task.total_steps && stride > 0) {
+            model.schedule.milestones.push_back(next);
+            next += stride;
+        }
+        model.schedule.factor = task.lr_decay;
+    }
+    model.adopt(f);
+    std::vector<ReportRow> out;
+    for (std::int64_t i = 0; i < std::min(n, cap); ++i)
+        out.push_back(ReportRow{ rows[size_t(i)].step, rows[size_t(i)].time_s, rows[size_t(i)].loss,
+                                 rows[size_t(i)].metric, rows[size_t(i)].lr });
+    return out;
 }
 
 }   // namespace gpu

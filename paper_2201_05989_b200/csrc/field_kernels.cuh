@@ -404,6 +404,10 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             bad |= !(sane(d0.x) && sane(d0.y) && sane(d8.x) && sane(d8.y));
             if (col >= s.in_real)
                 continue;
+#ifdef NFG_EXP_SKIP_LEVELS   // experiment builds only (tools/kbench.cu): drop coarse-level reductions
+            if (col / F < NFG_EXP_SKIP_LEVELS)
+                continue;
+#endif
             if (SINK == SINK_SCATTER) {
                 if (vg)
                     scatter_pair<D, F>(s.grid, lvs, xg, col, d0, a.table_grad);

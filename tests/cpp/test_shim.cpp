@@ -32,6 +32,13 @@ struct LrSchedule {
     std::vector<std::int64_t> milestones;
     double factor = 0.33;
 };
+struct ImageTask {   // tasks.hpp:16-31 member names
+    HashEncodingConfig cfg;
+    int interpolation = 0;
+    int hidden_layers = 2, hidden_width = 64, batch_size = 64;
+    std::int64_t total_steps = 20, log_interval = 10;
+    double lr = 1e-2, lr_decay = 0.33;
+};
 using FieldModel = nf::gpu::FieldModelT<HashEncodingConfig, MlpConfig, AdamHyper, LrSchedule>;
 using nf::gpu::Mat;
 
@@ -128,6 +135,57 @@ int main()
         const float l = nf::gpu::loss_with_grad(ctx, NFG_LOSS_L2, p, t, d);
         CHECK(std::fabs(l - 2.5f) < 1e-6f);
         CHECK(d(0, 0) == 1.0f && d(0, 1) == 2.0f);
+    }
+
+    // fit_image -> save_checkpoint -> load_checkpoint -> identical resume
+    // (test_tasks.cpp:284-324), deterministic mode for the bit-exact step
+    {
+        const int w = 16, h = 16;
+        Mat rgb(3, w * h);
+        for (int i = 0; i < w * h; ++i)
+            for (int c = 0; c < 3; ++c)
+                rgb(c, i) = 0.2f + 0.6f * float((i * (c + 3)) % 17) / 16.0f;
+        ImageTask task;
+        task.cfg.levels = 3;
+        task.cfg.table_size = 1u << 8;
+        task.cfg.n_min = 4;
+        task.cfg.n_max = 16;
+        FieldModel a(ctx);
+        a.options.deterministic = 1;
+        const auto rows = nf::gpu::fit_image(ctx, task, rgb.data(), w, h, 9, a);
+        CHECK(rows.size() == 3 && rows[0].step == 0 && rows[2].step == 20);
+        CHECK(a.hash_cfg.dims == 2 && a.mlp_cfg.output_width == 3);
+        a.save_checkpoint("test_checkpoint_roundtrip.bin");
+        FieldModel b(ctx);
+        b.options.deterministic = 1;
+        b.load_checkpoint("test_checkpoint_roundtrip.bin");
+        std::remove("test_checkpoint_roundtrip.bin");
+        Mat X(2, 32), T(3, 32, 0.5f);
+        std::uint32_t s = 7u;
+        for (long i = 0; i < 64; ++i) {
+            s = s * 1664525u + 1013904223u;
+            X.v[size_t(i)] = float(s >> 8) * 0x1p-24f;
+        }
+        const Mat ea = a.evaluate(X), eb = b.evaluate(X);
+        CHECK(ea.v == eb.v);
+        CHECK(a.adam_step_count() == b.adam_step_count());
+        b.hyper = a.hyper;
+        b.schedule = a.schedule;
+        const float l1 = a.train_step(X, T, NFG_LOSS_L2, 21), l2 = b.train_step(X, T, NFG_LOSS_L2, 21);
+        CHECK(l1 == l2);
+        CHECK(a.read(NFG_BUF_PARAMS) == b.read(NFG_BUF_PARAMS));
+        nf::gpu::write_report_csv(rows, "test_report.csv");
+        const auto back = nf::gpu::read_report_csv("test_report.csv");
+        std::remove("test_report.csv");
+        CHECK(back.size() == rows.size() && back[2].step == 20);
+        bool threw = false;
+        try {
+            FieldModel c(ctx);
+            c.load_checkpoint("nonexistent_checkpoint.bin");
+        } catch (const std::runtime_error&) {
+            threw = true;
+        }
+        CHECK(threw);
     }
 
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);

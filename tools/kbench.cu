@@ -3,6 +3,7 @@
 // optional per-phase clock64 breakdown (-DNFG_PHASE_TIMING). Development tool:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DNFG_PHASE_TIMING \
 //        -I paper_2201_05989_b200/csrc tools/kbench.cu paper_2201_05989_b200/csrc/host_init.cpp -o kbench
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
@@ -65,6 +66,23 @@ int main(int argc, char** argv)
         v = U(rng);
     for (auto& v : T)
         v = U(rng) - 0.5f;
+    if (const char* sb = getenv("KB_SORT")) {   // Morton order of the batch at 2^bits cells per axis
+        const int bits = std::atoi(sb);
+        std::vector<std::pair<uint64_t, int64_t>> key(B);
+        for (int64_t i = 0; i < B; ++i) {
+            uint64_t k = 0;
+            for (int bt = bits - 1; bt >= 0; --bt)
+                for (int d = 2; d >= 0; --d)
+                    k = (k << 1) | ((uint64_t(X[i * 3 + d] * float(1 << bits)) >> bt) & 1u);
+            key[i] = { k, i };
+        }
+        std::sort(key.begin(), key.end());
+        std::vector<float> X2(B * 3);
+        for (int64_t i = 0; i < B; ++i)
+            for (int d = 0; d < 3; ++d)
+                X2[i * 3 + d] = X[key[i].second * 3 + d];
+        X.swap(X2);
+    }
 
     __half* d_tab;
     float *d_W, *d_b, *d_X, *d_T, *d_g;
