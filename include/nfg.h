@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define NFG_ABI_VERSION 1
+#define NFG_ABI_VERSION 2
 
 typedef enum {
     NFG_OK = 0,
@@ -151,6 +151,7 @@ nfg_status nfg_field_write(nfg_field* f, int32_t which, uint64_t offset, uint64_
 nfg_status nfg_field_device_buffer(nfg_field* f, int32_t which, float** dev, uint64_t* count);
 /* AdamState::step (adam.hpp:56-73). */
 nfg_status nfg_field_get_config(const nfg_field* f, nfg_grid_config* grid, nfg_mlp_config* mlp);
+nfg_status nfg_field_context(const nfg_field* f, nfg_ctx** ctx);
 nfg_status nfg_field_get_step(const nfg_field* f, uint64_t* step);
 nfg_status nfg_field_set_step(nfg_field* f, uint64_t step);
 
@@ -239,6 +240,7 @@ nfg_status nfg_rng_create(nfg_ctx* ctx, uint64_t seed, uint64_t seq, nfg_rng** o
 nfg_status nfg_rng_destroy(nfg_rng* r);
 nfg_status nfg_rng_below_device(nfg_rng* r, uint32_t bound, int64_t n, uint32_t* out_dev);   /* next_below x n */
 nfg_status nfg_rng_floats_device(nfg_rng* r, int64_t n, float* out_dev);                     /* next_float x n */
+nfg_status nfg_rng_u32_device(nfg_rng* r, int64_t n, uint32_t* out_dev);                      /* next_u32 x n */
 nfg_status nfg_rng_get_state(nfg_rng* r, uint64_t* state, uint64_t* inc);
 
 /* fit_image's batch assembly (tasks.cpp:114-120): pixel p -> X = (((p % w) +
@@ -280,6 +282,37 @@ typedef struct {
 nfg_status nfg_fit_image(nfg_ctx* ctx, const nfg_image_task* task, const float* rgb, uint64_t seed,
                          const nfg_options* opts, nfg_field** model_out, nfg_report_row* rows, int64_t rows_cap,
                          int64_t* n_rows);
+
+/* ---- inference consumers (tasks.cpp:195-356) -------------
+ * A field is an nfg_field model, evaluated by the fused sm_100a inference, or, when field == NULL, a
+ * host FieldFn callback (tasks.hpp:70): X is d x n column-major on the host,
+ * out receives 1 x n (any function, e.g. an analytic SDF). */
+typedef void (*nfg_field_fn)(const float* X, int64_t n, float* out, void* user);
+/* oracle sign for iou (tasks.hpp:90-92): the point is 3 doubles. */
+typedef int (*nfg_sign_fn)(const double* p, void* user);
+/* Camera (tasks.hpp:72-77). */
+typedef struct {
+    double position[3];
+    double target[3];
+    double up[3];
+    double fov_deg;
+} nfg_camera;
+
+/* render_image (tasks.cpp:195-209): the 2D model at every pixel centre;
+ * rgb_host receives output_width x (width*height), pixel i = y*width + x. */
+nfg_status nfg_render_image(nfg_field* f, int32_t width, int32_t height, float* rgb_host);
+/* render_sdf_shaded (tasks.cpp:233-329): sphere tracing (step = field value,
+ * hit at < 1e-4, <= 256 steps) with active-ray compaction on the device,
+ * central-difference normals (h = 1e-3), Lambert headlight; background 1.
+ * rgb_host: 3 x (width*height). */
+nfg_status nfg_render_sdf_shaded(nfg_ctx* ctx, nfg_field* field, nfg_field_fn fn, void* user, const nfg_camera* cam,
+                                 int32_t width, int32_t height, float* rgb_host);
+/* iou (tasks.cpp:331-356): interior IoU of the field (< 0) and oracle_sign
+ * (< 0) at n_points uniform points in [lo, hi] drawn from rng exactly as
+ * Pcg32::uniform<double> (x, y, z per point); 1 when neither interior shows. */
+nfg_status nfg_iou(nfg_ctx* ctx, nfg_field* field, nfg_field_fn fn, void* user, nfg_sign_fn oracle_sign,
+                   void* sign_user, int64_t n_points, nfg_rng* rng, const double lo[3], const double hi[3],
+                   double* out);
 
 nfg_status nfg_host_alloc(size_t bytes, void** out);
 nfg_status nfg_host_free(void* p);

@@ -598,6 +598,95 @@ def load_checkpoint(path: str, hyper: "Hyper" = None) -> "Field":   # io.cpp:287
 
 
 # --------------------------------------------------------------------------
+# Inference consumers (tasks.cpp:195-356), vectorised over rays / points; the
+# field is any function (n, d) float32 -> n values (FieldFn, tasks.hpp:70).
+# --------------------------------------------------------------------------
+def _cross(a, b):   # Eigen cross
+    return np.array([a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]])
+
+
+def _normalized(v):   # v / sqrt(squaredNorm)
+    return v / np.sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2])
+
+
+def render_sdf_shaded(field, position, target, up, fov_deg, W, H):   # tasks.cpp:233-329
+    import math
+    pos = np.asarray(position, np.float64)
+    fwd = _normalized(np.asarray(target, np.float64) - pos)
+    right = _normalized(_cross(fwd, np.asarray(up, np.float64)))
+    up2 = _cross(right, fwd)
+    half_tan = math.tan(0.5 * fov_deg * math.pi / 180.0)
+    aspect = float(W) / float(H)
+    i = np.arange(W * H)
+    x, y = (i % W).astype(np.float64), (i // W).astype(np.float64)
+    u = ((2.0 * (x + 0.5)) / W - 1.0) * half_tan * aspect
+    v = (1.0 - (2.0 * (y + 0.5)) / H) * half_tan
+    d = [(fwd[k] + u * right[k]) + v * up2[k] for k in range(3)]
+    nn = np.sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2])
+    d = np.stack([dk / nn for dk in d], axis=1)
+    t0 = np.zeros(W * H)
+    t1 = np.full(W * H, np.inf)
+    fail = np.zeros(W * H, bool)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        for k in range(3):   # ray_unit_cube (tasks.cpp:213-229)
+            inv = 1.0 / d[:, k]
+            near, far = (0.0 - pos[k]) * inv, (1.0 - pos[k]) * inv
+            sw = near > far
+            near, far = np.where(sw, far, near), np.where(sw, near, far)
+            t0 = np.where(t0 < near, near, t0)
+            t1 = np.where(far < t1, far, t1)
+            fail |= t0 > t1
+    act = np.nonzero(~fail)[0]
+    t, texit = t0[act] + 1e-6, t1[act]
+    rgb = np.ones((W * H, 3), np.float32)
+    hit_pix, hit_t = [], []
+    for _ in range(256):
+        if act.size == 0:
+            break
+        pts = np.clip(pos[None, :] + t[:, None] * d[act], 0.0, 1.0).astype(np.float32)
+        val = np.asarray(field(pts), np.float32).reshape(-1).astype(np.float64)
+        hit = val < 1e-4
+        hit_pix.append(act[hit])
+        hit_t.append(t[hit])
+        t2 = t + val
+        keep = ~hit & (t2 <= texit)
+        act, t, texit = act[keep], t2[keep], texit[keep]
+    if hit_pix:
+        hp, ht = np.concatenate(hit_pix), np.concatenate(hit_t)
+        if hp.size:
+            p = pos[None, :] + ht[:, None] * d[hp]
+            probes = np.repeat(p[:, None, :], 6, axis=1)
+            for a in range(3):
+                probes[:, 2 * a, a] += 1e-3
+                probes[:, 2 * a + 1, a] -= 1e-3
+            vals = np.asarray(field(np.clip(probes.reshape(-1, 3), 0.0, 1.0).astype(np.float32)),
+                              np.float32).reshape(-1, 6)
+            n = np.stack([(vals[:, 2 * a] - vals[:, 2 * a + 1]).astype(np.float64) for a in range(3)], axis=1)
+            ln = np.sqrt((n[:, 0] * n[:, 0] + n[:, 1] * n[:, 1]) + n[:, 2] * n[:, 2])
+            with np.errstate(divide="ignore", invalid="ignore"):
+                n = np.where(ln[:, None] > 0, n / ln[:, None], n)
+            dd = d[hp]
+            dot = (n[:, 0] * -dd[:, 0] + n[:, 1] * -dd[:, 1]) + n[:, 2] * -dd[:, 2]
+            shade = (0.15 + 0.85 * np.where(dot > 0, dot, 0.0)).astype(np.float32)
+            rgb[hp] = (np.float32(0.9) * shade)[:, None]
+    return rgb
+
+
+def iou(field, oracle_sign, n_points, rng: "Pcg32", lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0)):   # tasks.cpp:331-356
+    lo, hi = np.asarray(lo, np.float64), np.asarray(hi, np.float64)
+    both = either = 0
+    for done in range(0, n_points, 1 << 16):
+        n = min(1 << 16, n_points - done)
+        P = lo[None, :] + (hi - lo)[None, :] * rng.doubles(3 * n).reshape(n, 3)
+        pred = np.asarray(field(P.astype(np.float32)), np.float32).reshape(-1)
+        m_in = pred < 0
+        o_in = np.array([oracle_sign(P[i]) < 0 for i in range(n)])
+        both += int(np.sum(m_in & o_in))
+        either += int(np.sum(m_in | o_in))
+    return 1.0 if either == 0 else both / either
+
+
+# --------------------------------------------------------------------------
 # RNG and fixtures
 # --------------------------------------------------------------------------
 class Pcg32:

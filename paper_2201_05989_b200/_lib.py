@@ -54,6 +54,14 @@ class nfg_step_record(C.Structure):
     _fields_ = [("loss_sum", C.c_double), ("flags", C.c_uint32 * 4), ("dy_max", C.c_float), ("pad", C.c_float)]
 
 
+class nfg_camera(C.Structure):
+    _fields_ = [("position", C.c_double * 3), ("target", C.c_double * 3), ("up", C.c_double * 3),
+                ("fov_deg", C.c_double)]
+
+
+FIELD_FN = C.CFUNCTYPE(None, C.POINTER(C.c_float), C.c_int64, C.POINTER(C.c_float), C.c_void_p)
+SIGN_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_void_p)
+
 _vp = C.c_void_p
 _fp = C.POINTER(C.c_float)
 _u32p = C.POINTER(C.c_uint32)
@@ -115,6 +123,12 @@ SIGNATURES = {
     "nfg_image_batch_device": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp, _vp]),
     "nfg_fit_image": (C.c_int, [_vp, C.POINTER(nfg_image_task), _vp, C.c_uint64, C.POINTER(nfg_options),
                                 C.POINTER(_vp), C.POINTER(nfg_report_row), C.c_int64, _i64p]),
+    "nfg_rng_u32_device": (C.c_int, [_vp, C.c_int64, _vp]),
+    "nfg_field_context": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "nfg_render_image": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp]),
+    "nfg_render_sdf_shaded": (C.c_int, [_vp, _vp, FIELD_FN, _vp, C.POINTER(nfg_camera), C.c_int32, C.c_int32, _vp]),
+    "nfg_iou": (C.c_int, [_vp, _vp, FIELD_FN, _vp, SIGN_FN, _vp, C.c_int64, _vp, C.POINTER(C.c_double),
+                          C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "nfg_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
     "nfg_host_free": (C.c_int, [_vp]),
 }

@@ -877,6 +877,11 @@ nfg_status nfg_field_device_buffer(nfg_field* f, int32_t which, float** dev, uin
     });
 }
 
+nfg_status nfg_field_context(const nfg_field* f, nfg_ctx** ctx)
+{
+    return guard([&] { *ctx = f->ctx; });
+}
+
 nfg_status nfg_field_get_config(const nfg_field* f, nfg_grid_config* grid, nfg_mlp_config* mlp)
 {
     return guard([&] {

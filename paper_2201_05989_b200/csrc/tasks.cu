@@ -83,7 +83,7 @@ __global__ void k_rng_direct(const RngState* __restrict__ src, RngState* __restr
         for (int64_t j = j0; j < n; j += stride) {
             const uint32_t v = pcg_output(s);
             if (out_u)
-                out_u[j] = v % bound;   // threshold == 0: next_below never rejects
+                out_u[j] = bound ? v % bound : v;   // threshold == 0: next_below never rejects; 0: raw next_u32
             else
                 out_f[j] = float(v >> 8) * 0x1p-24f;   // next_float (pcg32.hpp:41-44)
             s = sm * s + sp;
@@ -273,6 +273,15 @@ struct nfg_rng {
         cur ^= 1;
     }
 
+    void u32(int64_t n, uint32_t* out)
+    {
+        if (n < 0)
+            throw std::invalid_argument("nfg_rng: negative count");
+        k_rng_direct<<<grid_for(n), 256, 0, stream>>>(d + cur, d + (cur ^ 1), 0u, n, out, nullptr);
+        TK_CUDA(cudaGetLastError());
+        cur ^= 1;
+    }
+
     void floats(int64_t n, float* out)
     {
         if (n < 0)
@@ -334,6 +343,11 @@ nfg_status nfg_rng_destroy(nfg_rng* r)
 nfg_status nfg_rng_below_device(nfg_rng* r, uint32_t bound, int64_t n, uint32_t* out_dev)
 {
     return run([&] { r->below(bound, n, out_dev); });
+}
+
+nfg_status nfg_rng_u32_device(nfg_rng* r, int64_t n, uint32_t* out_dev)
+{
+    return run([&] { r->u32(n, out_dev); });
 }
 
 nfg_status nfg_rng_floats_device(nfg_rng* r, int64_t n, float* out_dev)

@@ -645,6 +645,65 @@ def fit_image(task: ImageTask, seed: int, options: Optional[Options] = None,
     return FitResult(model, rep)
 
 
+# ---- inference consumers (tasks.cpp:195-356) -----------------
+@dataclass
+class Camera:   # tasks.hpp:72-77
+    position: tuple = (0.5, 0.5, -1.2)
+    target: tuple = (0.5, 0.5, 0.5)
+    up: tuple = (0.0, 1.0, 0.0)
+    fov_deg: float = 40.0
+
+    def c(self) -> L.nfg_camera:
+        return L.nfg_camera((C.c_double * 3)(*self.position), (C.c_double * 3)(*self.target),
+                            (C.c_double * 3)(*self.up), self.fov_deg)
+
+
+def _field_args(field, dims: int):
+    """(nfg_field handle, FieldFn callback) for a FieldModel or a Python callable
+    mapping an (n, dims) float32 array to n values."""
+    if isinstance(field, FieldModel):
+        return field.h, L.FIELD_FN(), field.ctx
+
+    def cb(xp, n, outp, _user):
+        X = np.ctypeslib.as_array(xp, shape=(int(n), dims))
+        out = np.ctypeslib.as_array(outp, shape=(int(n),))
+        out[:] = np.asarray(field(X), np.float32).reshape(-1)[: int(n)]
+
+    return None, L.FIELD_FN(cb), None
+
+
+def render_image(model: "FieldModel", width: int, height: int) -> np.ndarray:   # tasks.cpp:195-209
+    """(width*height, output_width) float32, pixel i = y*width + x."""
+    out = np.empty((width * height, model.mlp_cfg.output_width), np.float32)
+    L.check(model.lib.nfg_render_image(model.h, width, height, _ptr(out)))
+    return out
+
+
+def render_sdf_shaded(field, camera: Camera, width: int, height: int,
+                      ctx: Optional[Context] = None) -> np.ndarray:   # tasks.cpp:233-329
+    """Sphere-traced, Lambert-shaded image of the zero level set: (width*height, 3)."""
+    h, fn, fctx = _field_args(field, 3)
+    ctx = fctx or ctx or default_context()
+    out = np.empty((width * height, 3), np.float32)
+    L.check(ctx.lib.nfg_render_sdf_shaded(ctx.h, h, fn, None, C.byref(camera.c()), width, height, _ptr(out)))
+    return out
+
+
+def iou(field, oracle_sign, n_points: int, rng: DeviceRng, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0)) -> float:
+    """tasks.cpp:331-356: ``oracle_sign(p)`` gets a (3,) float64 point; points come
+    from ``rng`` exactly as Pcg32::uniform<double>."""
+    h, fn, _ = _field_args(field, 3)
+
+    def sign(pp, _user):
+        return int(oracle_sign(np.ctypeslib.as_array(pp, shape=(3,)).copy()))
+
+    scb = L.SIGN_FN(sign)
+    out = C.c_double()
+    L.check(rng.lib.nfg_iou(rng.ctx.h, h, fn, None, scb, None, n_points, rng.h, (C.c_double * 3)(*lo),
+                            (C.c_double * 3)(*hi), C.byref(out)))
+    return float(out.value)
+
+
 class PinnedBuffer:
     """Page-locked host memory (cudaMallocHost) viewed as a numpy array."""
 
