@@ -260,14 +260,26 @@ __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
     for (uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride) {
-        const float4 G = ld4_hint(a.g + 4 * q, pol_stream);
-        const bool any = G.x != 0.0f || G.y != 0.0f || G.z != 0.0f || G.w != 0.0f;
         const uint64_t i0 = 4 * q;
-        if (!any && i0 + 3 < a.n_tab)
-            continue;   // whole quad skipped: nothing to read or write
-        const float4 P = ld4_hint(a.p + 4 * q, pol_stream);
-        const float4 M = ld4_hint(a.m + 4 * q, pol_stream);
-        const float4 V = ld4_hint(a.v + 4 * q, pol_stream);
+        float4 G, P, M, V;
+        bool any;
+        if (a.eager) {   // dense step: all four streams in flight at once
+            G = ld4_hint(a.g + 4 * q, pol_stream);
+            P = ld4_hint(a.p + 4 * q, pol_stream);
+            M = ld4_hint(a.m + 4 * q, pol_stream);
+            V = ld4_hint(a.v + 4 * q, pol_stream);
+            any = G.x != 0.0f || G.y != 0.0f || G.z != 0.0f || G.w != 0.0f;
+            if (!any && i0 + 3 < a.n_tab)
+                continue;
+        } else {
+            G = ld4_hint(a.g + 4 * q, pol_stream);
+            any = G.x != 0.0f || G.y != 0.0f || G.z != 0.0f || G.w != 0.0f;
+            if (!any && i0 + 3 < a.n_tab)
+                continue;   // whole quad skipped: nothing to read or write
+            P = ld4_hint(a.p + 4 * q, pol_stream);
+            M = ld4_hint(a.m + 4 * q, pol_stream);
+            V = ld4_hint(a.v + 4 * q, pol_stream);
+        }
         float pg[4] = { P.x, P.y, P.z, P.w }, gq[4] = { G.x, G.y, G.z, G.w };
         float mq[4] = { M.x, M.y, M.z, M.w }, vq[4] = { V.x, V.y, V.z, V.w };
         bool w[4];

@@ -105,9 +105,29 @@ struct PairElems {
     static constexpr int NE = (F == 1 ? 2 : 1) << D;
 };
 
-template <int D, int F, typename TT>
+// Where a thread's k-th staged element lives. Linear: a private column of a
+// CTA-wide staging area (k-th element of every thread in one row). Chunked:
+// the same per-warp rows mapped onto shared-memory chunks the warp owns
+// exclusively until the end-of-tile barrier (see k_train).
+struct SlotsLinear {
+    unsigned char* base;   // stage + tid * SB
+    int stride;            // bytes between a thread's consecutive elements
+    __device__ __forceinline__ unsigned char* ptr(int k) const { return base + k * stride; }
+};
+
+template <int ROWS, int ROW_STRIDE, int NCHUNK>
+struct SlotsChunked {
+    unsigned char* chunk[NCHUNK];   // each holds ROWS element rows, ROW_STRIDE bytes apart
+    int lane_off;                   // lane * SB
+    __device__ __forceinline__ unsigned char* ptr(int k) const
+    {
+        return chunk[k / ROWS] + (k % ROWS) * ROW_STRIDE + lane_off;
+    }
+};
+
+template <int D, int F, typename TT, class Slots>
 __device__ __forceinline__ void gather_issue(const GridDev& g, const LevelDev* lvs, const float* x, int col,
-                                             const TT* __restrict__ table, unsigned char* slot0, int slot_stride)
+                                             const TT* __restrict__ table, const Slots& slots, int k0)
 {
     constexpr int SB = Stage<F, TT>::SB;
 #pragma unroll
@@ -123,14 +143,14 @@ __device__ __forceinline__ void gather_issue(const GridDev& g, const LevelDev* l
             const TT* src = table + e;
             if (F == 1 && sizeof(TT) == 2)   // aligned 4-byte word holding the half
                 src = table + (e & ~size_t(1));
-            cp_async<SB>(slot0 + (h * (1 << D) + c) * slot_stride, src);
+            cp_async<SB>(slots.ptr(k0 + h * (1 << D) + c), src);
         }
     }
 }
 
-template <int D, int F, typename TT>
+template <int D, int F, typename TT, class Slots>
 __device__ __forceinline__ float2 gather_blend(const GridDev& g, const LevelDev* lvs, const float* x, int col,
-                                               const unsigned char* slot0, int slot_stride)
+                                               const Slots& slots, int k0)
 {
     float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
@@ -143,7 +163,7 @@ __device__ __forceinline__ float2 gather_blend(const GridDev& g, const LevelDev*
         float a = 0.0f, b = 0.0f;
 #pragma unroll
         for (int c = 0; c < (1 << D); ++c) {
-            const unsigned char* s = slot0 + (h * (1 << D) + c) * slot_stride;
+            const unsigned char* s = slots.ptr(k0 + h * (1 << D) + c);
             const float w = cs.weight(c);
             if (F == 1) {
                 float v;

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -225,12 +226,14 @@ struct nfg_field {
     // step may validate its inputs speculatively inside the fused kernel and
     // undo by re-zeroing; otherwise k_validate runs first.
     bool grads_clean = true;
+    int64_t last_batch = 0;            // global batch of the last backward (Adam's dense/sparse choice)
     unsigned int* d_ready = nullptr;   // NFG_MAX_CHUNKS chunk-ready flags
     unsigned int epoch = 0;
     DevBuf det_part, det_loss, det_sort;   // deterministic mode scratch
 };
 
 #define NFG_MAX_CHUNKS 64
+#define NFG_STREAM_CHUNKS 8   // H2D chunks per streamed step (<= NFG_MAX_CHUNKS)
 
 namespace {
 
@@ -285,6 +288,20 @@ void refresh_shadow(nfg_field* f)
     f->ctx->launches++;
 }
 
+// Kernel launches may block until completion (profilers and sanitizers inject
+// through CUDA_INJECTION64_PATH; CUDA_LAUNCH_BLOCKING=1): a kernel that waits
+// on copies enqueued after its launch would then never start them.
+bool launches_serialized()
+{
+    static const bool v = [] {
+        const char* lb = getenv("CUDA_LAUNCH_BLOCKING");
+        const char* inj = getenv("CUDA_INJECTION64_PATH");
+        const char* force = getenv("NFG_NO_STREAMING");
+        return (lb && lb[0] == '1') || (inj && inj[0]) || (force && force[0] == '1');
+    }();
+    return v;
+}
+
 // True for page-locked (cudaHostAlloc / cudaHostRegister) host memory.
 bool is_pinned(const void* p)
 {
@@ -329,6 +346,18 @@ void run_adam(nfg_field* f, float lr_now, bool force_check)
     a.lr = s.lr;
     a.flags = f->d_res->flags;
     a.restore_on_invalid = f->grads_clean ? 1 : 0;
+    // Dense steps (the batch's corners cover at least every table row once:
+    // B * 2^d >= T) load p/m/v together with g (one round trip, -9% Adam time
+    // at config 2); sparse steps keep the g-first skip of untouched quads.
+    // NFG_ADAM_EAGER=0/1 overrides (A/B runs).
+    {
+        static const int forced = [] {
+            const char* e = getenv("NFG_ADAM_EAGER");
+            return e ? atoi(e) : -1;
+        }();
+        const bool dense = (double(f->last_batch) * double(1u << f->gcfg.dims)) >= double(f->gcfg.table_size);
+        a.eager = forced >= 0 ? forced : (dense ? 1 : 0);
+    }
     NFG_CUDA(nfg::launch_adam(a, force_check, f->ctx->num_sms, f->ctx->stream));
     f->ctx->launches += 2;
     f->step = next;
@@ -399,6 +428,7 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
         c->launches++;
     }
     const double count = double(B_global) * double(f->mcfg.output_width);
+    f->last_batch = B_global;
     nfg::TrainArgs a{};
     a.X = X;
     a.target = target;
@@ -911,23 +941,25 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
         const uint64_t before = f->step;
         const bool was_clean = f->grads_clean;
         if (f->grads_clean && f->opts.fused_train && !f->opts.deterministic && c->write_value32 && B >= (int64_t(1) << 15) &&
-            is_pinned(X) && is_pinned(target)) {
-            // Overlap the H2D of the batch with the step: the chunk copies and
-            // their ready flags are enqueued on the copy stream FIRST, then the
-            // fused kernel is launched and waits per tile for its chunk's flag.
-            // Every copy the kernel waits on is already queued when it starts,
-            // so it completes even if launches are serialised (profilers,
-            // CUDA_LAUNCH_BLOCKING). Pinned sources only: a pageable copy would
-            // block the host before the launch and overlap nothing.
+            !launches_serialized() && is_pinned(X) && is_pinned(target)) {
+            // Overlap the H2D of the batch with the step: the fused kernel is
+            // launched first and waits per tile for its chunk's ready flag,
+            // which the copy stream writes (cuStreamWriteValue32) after each
+            // chunk lands, while the host enqueues the copies. Not used when
+            // launches may be serialised (a profiler or sanitizer injected,
+            // CUDA_LAUNCH_BLOCKING=1): a kernel waiting on another stream can
+            // then never finish, so those runs take the plain staged path.
+            // Pinned sources only: a pageable copy blocks the host and
+            // overlaps nothing.
             float* dX = static_cast<float*>(c->s0.get(size_t(B) * d * 4));
             float* dT = static_cast<float*>(c->s1.get(size_t(B) * no * 4));
-            const int64_t chunk = std::max<int64_t>((B / 16 + 255) / 256 * 256, (B + NFG_MAX_CHUNKS - 1) / NFG_MAX_CHUNKS);
+            const int64_t chunk = std::max<int64_t>(4096, (B + NFG_STREAM_CHUNKS - 1) / NFG_STREAM_CHUNKS);
             const int64_t nchunks = (B + chunk - 1) / chunk;
             const unsigned int epoch = ++f->epoch;
             NFG_CUDA(cudaEventRecord(c->ev_order, c->stream));        // staging buffers free
             NFG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_order, 0));
             int64_t k = 0;
-            try {
+            auto enqueue_copies = [&] {
                 for (; k < nchunks; ++k) {
                     const int64_t s0 = k * chunk, n = std::min(chunk, B - s0);
                     NFG_CUDA(cudaMemcpyAsync(dX + s0 * d, X + s0 * d, size_t(n) * d * 4, cudaMemcpyHostToDevice,
@@ -937,16 +969,14 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
                     if (c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0) != CUDA_SUCCESS)
                         throw Fail{ NFG_ECUDA, "cuStreamWriteValue32 failed" };
                 }
-            } catch (...) {
-                // the kernel was not launched; drain the copy stream so the
-                // staging buffers are not reused under an in-flight copy
-                cudaStreamSynchronize(c->copy_stream);
-                throw;
-            }
+            };
+            const Streamed streamed{ f->d_ready, epoch, chunk };
+            device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step, streamed);
             try {
-                device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step, Streamed{ f->d_ready, epoch, chunk });
+                enqueue_copies();
             } catch (...) {
-                cudaStreamSynchronize(c->copy_stream);
+                for (; k < nchunks; ++k)   // never leave the kernel waiting
+                    c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0);
                 throw;
             }
         } else {

@@ -48,7 +48,7 @@ struct StageGeo {
     static constexpr int BYTES = SRC == SRC_ENCODE ? TW * 32 * STS * PER_STEP : 0;
 };
 
-template <int IN_STEPS, int NH, int STAGE_BYTES = 0>
+template <int IN_STEPS, int NH, int STAGE_BYTES = 0, bool ALIAS = false>
 struct TrainSmem {
     using Lay = WLayout<IN_STEPS, NH>;
     static constexpr int INS = Lay::INS;
@@ -61,7 +61,28 @@ struct TrainSmem {
     static constexpr int DB_OFF = DZO_OFF + TS * OS * 2;
     static constexpr int RED_OFF = DB_OFF + (NH + 1) * H * 4;
     static constexpr int STAGE_OFF = align16(RED_OFF + 4 * TW * 4);
-    static constexpr int BYTES = STAGE_OFF + STAGE_BYTES;
+    static constexpr int BYTES = STAGE_OFF + (ALIAS ? 0 : STAGE_BYTES);
+};
+
+// Per-warp aliasing of the gather staging (fp16 tables, F = 2, >= 2 hidden
+// layers): a warp's staged corner rows live in the first 64 columns of ITS OWN
+// 16 rows of the two hidden-activation and two dz buffers. The warp writes
+// those rows only after its own blend (forward / backward of the same tile),
+// other warps read them only after the pre-dW barrier, and the end-of-tile
+// barrier precedes the next tile's gathers; the padding columns (the ones
+// column of the bias gradient) are never touched. Saves the 32 KB staging area
+// per CTA, which the SM gives to L1 for the gathers.
+template <int SRC, int D, int F, typename TT, int IN_STEPS, int NH>
+struct StageAlias {
+    using SG = StageGeo<SRC, D, F, TT, IN_STEPS>;
+    static constexpr int ROWS = 16;                               // sample rows per warp
+    static constexpr int ELEMS = SG::STS * 4 * SG::NE;            // staged elements per thread and pass
+#ifdef NFG_NO_ALIAS_STAGE
+    static constexpr bool ON = false;
+#else
+    static constexpr bool ON = SRC == SRC_ENCODE && NH >= 2 && SG::SB == 4 && 32 * SG::SB <= 2 * H &&
+                               ELEMS <= 4 * ROWS;
+#endif
 };
 
 template <int IN_STEPS, int NH>
@@ -152,7 +173,8 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
 {
     using Lay = WLayout<IN_STEPS, NH>;
     using SG = StageGeo<SRC, D, F, TT, IN_STEPS>;
-    using SM = TrainSmem<IN_STEPS, NH, SG::BYTES>;
+    using SA = StageAlias<SRC, D, F, TT, IN_STEPS, NH>;
+    using SM = TrainSmem<IN_STEPS, NH, SG::BYTES, SA::ON>;
     extern __shared__ __align__(16) unsigned char sm[];
     __half* ws = reinterpret_cast<__half*>(sm);
     float* bs = reinterpret_cast<float*>(sm + Lay::HALVES * 2);
@@ -254,40 +276,53 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         if (SRC == SRC_ENCODE) {
             // all corner loads of SG::STS k16 steps in flight at once (cp.async)
             const TT* tab = static_cast<const TT*>(a.table);
-            unsigned char* stage = sm + SM::STAGE_OFF;
-            constexpr int SLOT = TW * 32 * SG::SB;   // stride between a thread's slots
+            auto encode_all = [&](const auto& slots) {
 #pragma unroll
-            for (int s0 = 0; s0 < IN_STEPS; s0 += SG::STS) {
+                for (int s0 = 0; s0 < IN_STEPS; s0 += SG::STS) {
 #pragma unroll
-                for (int sl = 0; sl < SG::STS; ++sl)
+                    for (int sl = 0; sl < SG::STS; ++sl)
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
-                        const int p = (sl * 2 + h) * 2;
-                        unsigned char* base = stage + tid * SG::SB;
-                        if (s0 + sl < IN_STEPS && vg)
-                            gather_issue<D, F, TT>(s.grid, lvs, xg, col, tab, base + p * SG::NE * SLOT, SLOT);
-                        if (s0 + sl < IN_STEPS && vg8)
-                            gather_issue<D, F, TT>(s.grid, lvs, xg8, col, tab, base + (p + 1) * SG::NE * SLOT, SLOT);
-                    }
-                cp_async_wait_all();
+                        for (int h = 0; h < 2; ++h) {
+                            const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
+                            const int p = (sl * 2 + h) * 2;
+                            if (s0 + sl < IN_STEPS && vg)
+                                gather_issue<D, F, TT>(s.grid, lvs, xg, col, tab, slots, p * SG::NE);
+                            if (s0 + sl < IN_STEPS && vg8)
+                                gather_issue<D, F, TT>(s.grid, lvs, xg8, col, tab, slots, (p + 1) * SG::NE);
+                        }
+                    cp_async_wait_all();
 #pragma unroll
-                for (int sl = 0; sl < SG::STS; ++sl)
+                    for (int sl = 0; sl < SG::STS; ++sl)
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        if (s0 + sl >= IN_STEPS)
-                            continue;
-                        const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
-                        const int p = (sl * 2 + h) * 2;
-                        const unsigned char* base = stage + tid * SG::SB;
-                        const float2 e0 = vg ? gather_blend<D, F, TT>(s.grid, lvs, xg, col, base + p * SG::NE * SLOT, SLOT)
-                                             : make_float2(0.f, 0.f);
-                        const float2 e8 = vg8 ? gather_blend<D, F, TT>(s.grid, lvs, xg8, col,
-                                                                        base + (p + 1) * SG::NE * SLOT, SLOT)
-                                              : make_float2(0.f, 0.f);
-                        afr[s0 + sl][2 * h] = pack_half2(e0.x, e0.y);
-                        afr[s0 + sl][2 * h + 1] = pack_half2(e8.x, e8.y);
-                    }
+                        for (int h = 0; h < 2; ++h) {
+                            if (s0 + sl >= IN_STEPS)
+                                continue;
+                            const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
+                            const int p = (sl * 2 + h) * 2;
+                            const float2 e0 = vg ? gather_blend<D, F, TT>(s.grid, lvs, xg, col, slots, p * SG::NE)
+                                                 : make_float2(0.f, 0.f);
+                            const float2 e8 = vg8 ? gather_blend<D, F, TT>(s.grid, lvs, xg8, col, slots,
+                                                                            (p + 1) * SG::NE)
+                                                  : make_float2(0.f, 0.f);
+                            afr[s0 + sl][2 * h] = pack_half2(e0.x, e0.y);
+                            afr[s0 + sl][2 * h + 1] = pack_half2(e8.x, e8.y);
+                        }
+                    if (SA::ON && s0 + SG::STS < IN_STEPS)
+                        __syncwarp();   // next pass reuses the warp's rows
+                }
+            };
+            if constexpr (SA::ON) {
+                SlotsChunked<SA::ROWS, HS * 2, 4> slots;
+                slots.chunk[0] = reinterpret_cast<unsigned char*>(acth + r0 * HS);
+                slots.chunk[1] = reinterpret_cast<unsigned char*>(acth + TS * HS + r0 * HS);
+                slots.chunk[2] = reinterpret_cast<unsigned char*>(dzh + r0 * HS);
+                slots.chunk[3] = reinterpret_cast<unsigned char*>(dzh + TS * HS + r0 * HS);
+                slots.lane_off = lane * SG::SB;
+                encode_all(slots);
+                __syncwarp();   // every lane's staged rows consumed before the warp writes them
+            } else {
+                const SlotsLinear slots{ sm + SM::STAGE_OFF + tid * SG::SB, TW * 32 * SG::SB };
+                encode_all(slots);
             }
         } else {
             input_frags<SRC, D, F, TT, IN_STEPS>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);

@@ -101,6 +101,7 @@ struct AdamArgs {
     float b1, b2, omb1, omb2, bc1, bc2, eps, l2, lr;
     unsigned int* flags;
     int restore_on_invalid;   // zero the gradient slab if flags[3] (speculative step)
+    int eager;                // 1: load p/m/v with g (dense steps), 0: only for non-zero gradient quads
 };
 cudaError_t launch_adam(const AdamArgs& a, bool force_check, int num_sms, cudaStream_t st);
 cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cudaStream_t st);

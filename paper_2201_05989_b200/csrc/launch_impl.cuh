@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "field_kernels.cuh"
 
@@ -11,13 +12,18 @@ template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IS, int NH
 cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& a, int num_sms, cudaStream_t st,
                       int* grid_used)
 {
-    using SM = TrainSmem<IS, NH, StageGeo<SRC, D, F, TT, IS>::BYTES>;
+    using SM = TrainSmem<IS, NH, StageGeo<SRC, D, F, TT, IS>::BYTES, StageAlias<SRC, D, F, TT, IS, NH>::ON>;
     auto k = k_train<SRC, GRAD, SINK, D, F, TT, IS, NH>;
     static int per_sm = -1;   // resolved once per instantiation
     if (per_sm < 0) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
         if (e != cudaSuccess)
             return e;
+        if (const char* cv = getenv("NFG_TRAIN_CARVEOUT")) {   // experiment: shared-memory carveout percent
+            e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+            if (e != cudaSuccess)
+                return e;
+        }
         int n = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, TW * 32, SM::BYTES);
         if (e != cudaSuccess)
