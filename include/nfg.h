@@ -216,6 +216,17 @@ nfg_status nfg_adam_step(nfg_field* f, float lr_now);
 double nfg_lr_at(const int64_t* milestones, int32_t n, double factor, double base_lr, int64_t step);
 
 /* ---- pinned host memory for zero-copy-staged inputs -------------------- */
+/* ---- device-pointer components (asynchronous; errors via nfg_field_check) --
+ * For pipelines that chain fields on the device (the NeRF density -> color
+ * networks). Gradients accumulate into the field's slab (mlp.hpp:147-148,
+ * grid.hpp:292); nfg_adam_step_device applies adam_step (adam.hpp:78-122)
+ * with an exact non-finite scan and zeroes them. dOut is dLoss/d(output after
+ * the output activation), as mlp_backward's dOut. */
+nfg_status nfg_field_backward_device(nfg_field* f, const float* X, int64_t B, const float* dOut);
+nfg_status nfg_mlp_forward_device(nfg_field* f, const float* Y, int64_t B, float* out);
+nfg_status nfg_mlp_backward_device(nfg_field* f, const float* Y, int64_t B, const float* dOut, float* dY);
+nfg_status nfg_adam_step_device(nfg_field* f, float lr_now);
+
 /* ---- checkpoint (io.cpp:222-351, NFC1/HGE1/MLP1/ADM1) --------------------
  * Byte-compatible with the reference's save_checkpoint / load_checkpoint for
  * hash-encoder models. load creates a new field from the file's configs (the
@@ -313,6 +324,49 @@ nfg_status nfg_render_sdf_shaded(nfg_ctx* ctx, nfg_field* field, nfg_field_fn fn
 nfg_status nfg_iou(nfg_ctx* ctx, nfg_field* field, nfg_field_fn fn, void* user, nfg_sign_fn oracle_sign,
                    void* sign_user, int64_t n_points, nfg_rng* rng, const double lo[3], const double hi[3],
                    double* out);
+
+/* ---- NeRF (§5.4 + Appendix E) -------------------
+ * Density network: hash encoding (levels * features == 32) -> 1 x 64 -> 16
+ * outputs, the first is log-density; color network: [16 density outputs |
+ * SH degree-4 of the view direction] -> 2 x 64 -> RGB (sigmoid). Training
+ * steps march rays through a 128^3 occupancy bitfield (Morton order) at
+ * dt = sqrt(3)/1024 in [0,1]^3, compact the samples into dense buffers,
+ * composite (transmittance stop at 1e-4), and update the occupancy grid
+ * every 16 steps. The reference has no NeRF: parity is against
+ * a restatement of the paper's appendix (oracle/oracle.py). */
+typedef struct {
+    nfg_grid_config grid;        /* density encoding; dims forced to 3 */
+    double lr;                   /* Adam learning rate (eps 1e-15, beta 0.9 / 0.99) */
+    int32_t target_samples;      /* samples per training step (2^18) */
+    int32_t max_samples_per_ray; /* 1024 */
+    float background[3];
+} nfg_nerf_config;
+typedef struct nfg_nerf nfg_nerf;
+nfg_status nfg_nerf_create(nfg_ctx* ctx, const nfg_nerf_config* cfg, uint64_t seed, nfg_nerf** out);
+nfg_status nfg_nerf_destroy(nfg_nerf* n);
+nfg_status nfg_nerf_fields(nfg_nerf* n, nfg_field** density, nfg_field** color);
+/* cams: n_views x 12 floats (position, forward, right, up); a pixel (x, y)
+ * looks along normalize(forward + u right + v up), u = (x + 0.5 - w/2) / focal,
+ * v = (h/2 - y - 0.5) / focal. rgb: n_views x height x width x 3. */
+nfg_status nfg_nerf_set_dataset(nfg_nerf* n, int32_t n_views, int32_t width, int32_t height, float focal,
+                                const float* cams, const float* rgb);
+nfg_status nfg_nerf_train_step(nfg_nerf* n, int64_t step, float* loss, int64_t* rays_used, int64_t* samples_used);
+nfg_status nfg_nerf_update_occupancy(nfg_nerf* n, int64_t step);
+nfg_status nfg_nerf_render(nfg_nerf* n, const float* cam12, int32_t width, int32_t height, float focal, float* rgb);
+nfg_status nfg_nerf_occupancy(nfg_nerf* n, uint8_t* bits, float* density);   /* 128^3/8 bytes, 128^3 floats */
+nfg_status nfg_nerf_set_occupancy(nfg_nerf* n, const uint8_t* bits);
+/* components on host buffers (tests): marching + compaction (rays n x 6:
+ * origin, unit direction; samples: total x 3 positions), compositing forward
+ * and backward (raw = log-density per sample), SH4, and the synthetic scene
+ * (three textured soft spheres) rendered by fine marching. */
+nfg_status nfg_nerf_march(nfg_ctx* ctx, const float* rays, int64_t n, const uint8_t* bits, int32_t max_steps,
+                          uint32_t* counts, float* samples, int64_t cap, int64_t* total);
+nfg_status nfg_nerf_composite(nfg_ctx* ctx, int64_t n_rays, const uint32_t* counts, const float* raw,
+                              const float* rgb, const float* target, const float* bg, float dt, float* color,
+                              float* d_rgb, float* d_raw, double* loss_sum);
+nfg_status nfg_nerf_sh4(nfg_ctx* ctx, const float* dirs, int64_t n, float* out);
+nfg_status nfg_nerf_scene_render(nfg_ctx* ctx, const float* cams, int32_t n_views, int32_t width, int32_t height,
+                                 float focal, const float* bg, float* rgb);
 
 nfg_status nfg_host_alloc(size_t bytes, void** out);
 nfg_status nfg_host_free(void* p);

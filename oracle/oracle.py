@@ -687,6 +687,181 @@ def iou(field, oracle_sign, n_points, rng: "Pcg32", lo=(0.0, 0.0, 0.0), hi=(1.0,
 
 
 # --------------------------------------------------------------------------
+# NeRF. PARITY UNPINNED: the reference has no NeRF
+# (SPEC.md:8); these functions restate the paper's Appendix E
+# and §5.4 and are the checker for
+# paper_2201_05989_b200/csrc/nerf.cu. fp32 scalar arithmetic in the device
+# kernel's order (no contraction) for the marching, float64 for compositing.
+# --------------------------------------------------------------------------
+NERF_RES = 128
+NERF_DT = np.float32(1.7320508075688772) / np.float32(1024.0)
+
+
+def _spread3(v):
+    v &= 0x7F
+    v = (v | (v << 8)) & 0x0000F00F
+    v = (v | (v << 4)) & 0x000C30C3
+    v = (v | (v << 2)) & 0x00249249
+    return v
+
+
+def morton3(x, y, z):
+    return _spread3(x) | (_spread3(y) << 1) | (_spread3(z) << 2)
+
+
+def nerf_march(rays, bits, max_steps=1024):   # PAPER.md:904-936 (fixed step, occupancy skip)
+    f = np.float32
+    rays = np.asarray(rays, np.float32)
+    bits = np.asarray(bits, np.uint8)
+    counts, out = [], []
+
+    def cell(p):
+        c = int(p * f(NERF_RES))
+        return min(max(c, 0), NERF_RES - 1)
+
+    with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+        for r in rays:
+            o, d = r[:3], r[3:]
+            t0, t1 = f(-np.inf), f(np.inf)
+            for k in range(3):
+                inv = f(1.0) / d[k]
+                a, b = (f(0.0) - o[k]) * inv, (f(1.0) - o[k]) * inv
+                t0 = np.fmax(t0, np.fmin(a, b))
+                t1 = np.fmin(t1, np.fmax(a, b))
+            t0 = np.fmax(t0, f(0.0))
+            n = 0
+            if t1 > t0:
+                t = t0 + f(0.5) * NERF_DT
+                while t < t1 and n < max_steps:
+                    p = [o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]]
+                    c = [cell(v) for v in p]
+                    m = morton3(c[0], c[1], c[2])
+                    if (bits[m >> 3] >> (m & 7)) & 1:
+                        out.append(p)
+                        n += 1
+                        t = t + NERF_DT
+                        continue
+                    tn = f(np.inf)
+                    for k in range(3):
+                        cb = f(c[k] + (1 if d[k] > 0 else 0))
+                        tk = (cb / f(NERF_RES) - p[k]) / d[k]
+                        tn = np.fmin(tn, tk)
+                    steps = np.ceil(np.fmax(tn / NERF_DT, f(0.5)))
+                    t = t + steps * NERF_DT
+            counts.append(n)
+    return np.array(counts, np.uint32), np.array(out, np.float32).reshape(-1, 3)
+
+
+def nerf_composite(counts, raw, rgb, target, bg=(1.0, 1.0, 1.0), dt=float(NERF_DT)):
+    """Volume rendering C = sum T_i a_i c_i + T_end bg, a = 1 - exp(-exp(raw) dt),
+    transmittance stop at 1e-4; L2 loss averaged over rays x 3 and its gradients
+    w.r.t. the per-sample colours and log-densities (float64)."""
+    raw = np.asarray(raw, np.float64)
+    rgb = np.asarray(rgb, np.float64)
+    target = np.asarray(target, np.float64)
+    bg = np.asarray(bg, np.float64)
+    R = len(counts)
+    color = np.zeros((R, 3))
+    d_rgb = np.zeros_like(rgb)
+    d_raw = np.zeros_like(raw)
+    loss = 0.0
+    off = 0
+    for r, n in enumerate(counts):
+        T, C, used, ws = 1.0, np.zeros(3), 0, []
+        for i in range(off, off + int(n)):
+            if T < 1e-4:
+                break
+            a = 1.0 - np.exp(-np.exp(raw[i]) * dt)
+            ws.append(T * a)
+            C += T * a * rgb[i]
+            T *= 1.0 - a
+            used += 1
+        color[r] = C + T * bg
+        e = color[r] - target[r]
+        loss += float(e @ e)
+        g = 2.0 * e / (3.0 * R)
+        P = np.zeros(3)
+        T2 = 1.0
+        for j in range(used):
+            i = off + j
+            a = 1.0 - np.exp(-np.exp(raw[i]) * dt)
+            P += ws[j] * rgb[i]
+            T2 *= 1.0 - a
+            d_rgb[i] = ws[j] * g
+            d_raw[i] = dt * ((T2 * rgb[i] - (C - P) - T * bg) @ g) * np.exp(min(raw[i], 15.0))
+        off += int(n)
+    return color, d_rgb, d_raw, loss
+
+
+def sh4(d):   # real spherical harmonics up to degree 4 (16 coefficients), PAPER.md:602
+    x, y, z = d[:, 0].astype(np.float64), d[:, 1].astype(np.float64), d[:, 2].astype(np.float64)
+    xy, xz, yz, x2, y2, z2 = x * y, x * z, y * z, x * x, y * y, z * z
+    return np.stack([
+        np.full_like(x, 0.28209479177387814), -0.48860251190291987 * y, 0.48860251190291987 * z,
+        -0.48860251190291987 * x, 1.0925484305920792 * xy, -1.0925484305920792 * yz,
+        0.94617469575755997 * z2 - 0.31539156525251999, -1.0925484305920792 * xz,
+        0.54627421529603959 * x2 - 0.54627421529603959 * y2, 0.59004358992664352 * y * (-3.0 * x2 + y2),
+        2.8906114426405538 * xy * z, 0.45704579946446572 * y * (1.0 - 5.0 * z2),
+        0.3731763325901154 * z * (5.0 * z2 - 3.0), 0.45704579946446572 * x * (1.0 - 5.0 * z2),
+        1.4453057213202769 * z * (x2 - y2), 0.59004358992664352 * x * (-x2 + 3.0 * y2)], axis=1)
+
+
+NERF_SCENE = [((0.40, 0.45, 0.50), 0.18, (0.90, 0.30, 0.20)), ((0.62, 0.55, 0.45), 0.14, (0.20, 0.70, 0.90)),
+              ((0.50, 0.30, 0.62), 0.10, (0.85, 0.85, 0.25))]
+
+
+def nerf_scene(P):   # the synthetic procedural scene: (sigma (n,), rgb (n, 3))
+    P = np.asarray(P, np.float64)
+    sig = np.zeros(len(P))
+    best = np.full(len(P), 1e9)
+    col = np.zeros((len(P), 3))
+    for c, r, rgb in NERF_SCENE:
+        dist = np.linalg.norm(P - np.array(c), axis=1) - r
+        with np.errstate(over="ignore"):
+            sig += 80.0 / (1.0 + np.exp(dist * 150.0))
+        m = dist < best
+        best = np.where(m, dist, best)
+        col[m] = rgb
+    tex = 0.65 + 0.35 * np.sin(18.0 * (P[:, 0] + 0.7 * P[:, 1] - 0.4 * P[:, 2]))
+    return sig, col * tex[:, None]
+
+
+def nerf_pixel_rays(cam, w, h, focal):
+    cam = np.asarray(cam, np.float64)
+    i = np.arange(w * h)
+    x, y = i % w, i // w
+    u = (x + 0.5 - 0.5 * w) / focal
+    v = (0.5 * h - y - 0.5) / focal
+    d = cam[3:6][None, :] + u[:, None] * cam[6:9][None, :] + v[:, None] * cam[9:12][None, :]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return np.repeat(cam[None, :3], w * h, axis=0), d
+
+
+def nerf_scene_render(cam, w, h, focal, bg=(1.0, 1.0, 1.0)):   # fine marching of the analytic scene (float64)
+    o, d = nerf_pixel_rays(cam, w, h, focal)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inv = 1.0 / d
+        a, b = (0.0 - o) * inv, (1.0 - o) * inv
+        t0 = np.fmax(np.nanmax(np.fmin(a, b), axis=1), 0.0)
+        t1 = np.nanmin(np.fmax(a, b), axis=1)
+    dt = float(NERF_DT)
+    T = np.ones(len(o))
+    C = np.zeros((len(o), 3))
+    t = t0 + 0.5 * dt
+    live = t1 > t0
+    while live.any():
+        live &= (t < t1) & (T >= 1e-4)
+        if not live.any():
+            break
+        s, c = nerf_scene(o[live] + t[live, None] * d[live])
+        a = 1.0 - np.exp(-s * dt)
+        C[live] += (T[live] * a)[:, None] * c
+        T[live] *= 1.0 - a
+        t = t + dt
+    return C + T[:, None] * np.asarray(bg)
+
+
+# --------------------------------------------------------------------------
 # RNG and fixtures
 # --------------------------------------------------------------------------
 class Pcg32:

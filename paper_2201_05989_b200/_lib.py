@@ -59,6 +59,11 @@ class nfg_camera(C.Structure):
                 ("fov_deg", C.c_double)]
 
 
+class nfg_nerf_config(C.Structure):
+    _fields_ = [("grid", nfg_grid_config), ("lr", C.c_double), ("target_samples", C.c_int32),
+                ("max_samples_per_ray", C.c_int32), ("background", C.c_float * 3)]
+
+
 FIELD_FN = C.CFUNCTYPE(None, C.POINTER(C.c_float), C.c_int64, C.POINTER(C.c_float), C.c_void_p)
 SIGN_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_void_p)
 
@@ -129,6 +134,24 @@ SIGNATURES = {
     "nfg_render_sdf_shaded": (C.c_int, [_vp, _vp, FIELD_FN, _vp, C.POINTER(nfg_camera), C.c_int32, C.c_int32, _vp]),
     "nfg_iou": (C.c_int, [_vp, _vp, FIELD_FN, _vp, SIGN_FN, _vp, C.c_int64, _vp, C.POINTER(C.c_double),
                           C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "nfg_field_backward_device": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
+    "nfg_mlp_forward_device": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
+    "nfg_mlp_backward_device": (C.c_int, [_vp, _vp, C.c_int64, _vp, _vp]),
+    "nfg_adam_step_device": (C.c_int, [_vp, C.c_float]),
+    "nfg_nerf_create": (C.c_int, [_vp, C.POINTER(nfg_nerf_config), C.c_uint64, C.POINTER(_vp)]),
+    "nfg_nerf_destroy": (C.c_int, [_vp]),
+    "nfg_nerf_fields": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
+    "nfg_nerf_set_dataset": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_float, _vp, _vp]),
+    "nfg_nerf_train_step": (C.c_int, [_vp, C.c_int64, _fp, _i64p, _i64p]),
+    "nfg_nerf_update_occupancy": (C.c_int, [_vp, C.c_int64]),
+    "nfg_nerf_render": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_float, _vp]),
+    "nfg_nerf_occupancy": (C.c_int, [_vp, _vp, _vp]),
+    "nfg_nerf_set_occupancy": (C.c_int, [_vp, _vp]),
+    "nfg_nerf_march": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int32, _vp, _vp, C.c_int64, _i64p]),
+    "nfg_nerf_composite": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, C.c_float, _vp, _vp, _vp,
+                                     C.POINTER(C.c_double)]),
+    "nfg_nerf_sh4": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
+    "nfg_nerf_scene_render": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int32, C.c_float, _vp, _vp]),
     "nfg_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
     "nfg_host_free": (C.c_int, [_vp]),
 }

@@ -230,6 +230,7 @@ struct nfg_field {
     unsigned int* d_ready = nullptr;   // NFG_MAX_CHUNKS chunk-ready flags
     unsigned int epoch = 0;
     DevBuf det_part, det_loss, det_sort;   // deterministic mode scratch
+    DevBuf comp_y, comp_dy;                // nfg_field_backward_device scratch
 };
 
 #define NFG_MAX_CHUNKS 64
@@ -1240,6 +1241,89 @@ nfg_status nfg_adam_step(nfg_field* f, float lr_now)
             raise_if_aborted(f);
         }
         f->grads_clean = true;
+    });
+}
+
+// ---- device-pointer components (asynchronous on the context stream) --------
+// Building blocks for pipelines that chain fields on the device (the NeRF
+// density -> color networks, csrc/nerf.cu). Gradients ACCUMULATE into the
+// field's slab like mlp_backward / encode_backward (mlp.hpp:147-148,
+// grid.hpp:292); nfg_adam_step_device applies and zeroes them; deferred
+// errors surface through nfg_field_check.
+nfg_status nfg_field_backward_device(nfg_field* f, const float* X, int64_t B, const float* dOut)
+{
+    return guard([&] {
+        nfg_ctx* c = f->ctx;
+        if (B <= 0)
+            return;
+        reset_scratch(f);
+        const size_t LF = size_t(f->shape.in_real);
+        float* Y = static_cast<float*>(f->comp_y.get(size_t(B) * LF * 4));
+        float* dY = static_cast<float*>(f->comp_dy.get(size_t(B) * LF * 4));
+        NFG_CUDA(nfg::launch_encode_fwd_lv(f->shape, f->d_levels, X, B, table_ptr(f), Y, nullptr, nullptr, c->stream));
+        nfg::TrainArgs a{};
+        a.Y = Y;
+        a.dout = dOut;
+        a.B = B;
+        a.inv_count = 1.0f;
+        a.W = f->d_p + f->n_tab_dev;
+        a.b = f->d_p + f->n_tab_dev + f->n_w;
+        a.dY = dY;
+        a.gW = f->d_g + f->n_tab_dev;
+        a.gb = f->d_g + f->n_tab_dev + f->n_w;
+        a.scratch = scratch_of(f);
+        NFG_CUDA(nfg::launch_train(f->shape, nullptr, nfg::SRC_LOAD_Y, nfg::GRAD_DOUT, nfg::SINK_STORE, a, c->num_sms,
+                                   c->stream, nullptr));
+        NFG_CUDA(nfg::launch_encode_bwd_lv(f->shape, f->d_levels, X, B, dY, f->d_g, c->stream, f->d_res->flags));
+        c->launches += 3;
+        f->grads_clean = false;
+    });
+}
+
+nfg_status nfg_mlp_forward_device(nfg_field* f, const float* Y, int64_t B, float* out)
+{
+    return guard([&] {
+        nfg::InferArgs a{};
+        a.Y = Y;
+        a.B = B;
+        a.W = f->d_p + f->n_tab_dev;
+        a.b = f->d_p + f->n_tab_dev + f->n_w;
+        a.out = out;
+        NFG_CUDA(nfg::launch_infer(f->shape, nullptr, nfg::SRC_LOAD_Y, a, f->ctx->num_sms, f->ctx->stream));
+        f->ctx->launches++;
+    });
+}
+
+nfg_status nfg_mlp_backward_device(nfg_field* f, const float* Y, int64_t B, const float* dOut, float* dY)
+{
+    return guard([&] {
+        if (B <= 0)
+            return;
+        reset_scratch(f);
+        nfg::TrainArgs a{};
+        a.Y = Y;
+        a.dout = dOut;
+        a.B = B;
+        a.inv_count = 1.0f;
+        a.W = f->d_p + f->n_tab_dev;
+        a.b = f->d_p + f->n_tab_dev + f->n_w;
+        a.dY = dY;
+        a.gW = f->d_g + f->n_tab_dev;
+        a.gb = f->d_g + f->n_tab_dev + f->n_w;
+        a.scratch = scratch_of(f);
+        NFG_CUDA(nfg::launch_train(f->shape, nullptr, nfg::SRC_LOAD_Y, nfg::GRAD_DOUT, nfg::SINK_STORE, a,
+                                   f->ctx->num_sms, f->ctx->stream, nullptr));
+        f->ctx->launches++;
+        f->grads_clean = false;
+    });
+}
+
+nfg_status nfg_adam_step_device(nfg_field* f, float lr_now)
+{
+    return guard([&] {
+        run_adam(f, lr_now, true);   // exact non-finite scan: the producers' flags are not trusted here
+        f->pending_steps++;
+        f->grads_clean = true;   // optimistic; nfg_field_check corrects it
     });
 }
 

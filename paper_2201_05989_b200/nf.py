@@ -704,6 +704,130 @@ def iou(field, oracle_sign, n_points: int, rng: DeviceRng, lo=(0.0, 0.0, 0.0), h
     return float(out.value)
 
 
+# ---- NeRF (§5.4 + Appendix E) -------------------------
+OCC_RES = 128
+
+
+def orbit_cameras(n: int, radius: float = 1.3, height: float = 0.25, fov_deg: float = 40.0, width: int = 64,
+                  phase: float = 0.0):
+    """n views on a circle around (0.5, 0.5, 0.5) looking at the centre: (cams (n, 12), focal)."""
+    cams = np.zeros((n, 12), np.float32)
+    for i in range(n):
+        a = phase + 2 * np.pi * i / n
+        pos = np.array([0.5 + radius * np.cos(a), 0.5 + height * np.sin(3 * a + 0.3), 0.5 + radius * np.sin(a)])
+        fwd = np.array([0.5, 0.5, 0.5]) - pos
+        fwd /= np.linalg.norm(fwd)
+        right = np.cross(fwd, [0.0, 1.0, 0.0])
+        right /= np.linalg.norm(right)
+        up = np.cross(right, fwd)
+        cams[i] = np.concatenate([pos, fwd, right, up]).astype(np.float32)
+    focal = 0.5 * width / np.tan(0.5 * np.radians(fov_deg))
+    return cams, float(focal)
+
+
+class NeRF:
+    """Hash-grid NeRF (density 1x64 -> 16, color 2x64 -> RGB) trained with
+    occupancy-grid ray marching and compacted samples, all on the device."""
+
+    def __init__(self, grid: Optional[HashEncodingConfig] = None, lr: float = 1e-2, target_samples: int = 1 << 18,
+                 max_samples_per_ray: int = 1024, background=(1.0, 1.0, 1.0), seed: int = 1337,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        g = grid or HashEncodingConfig(levels=16, table_size=1 << 19, features=2, n_min=16, n_max=2048, dims=3)
+        cfg = L.nfg_nerf_config(g.c(), lr, target_samples, max_samples_per_ray, (C.c_float * 3)(*background))
+        h = C.c_void_p()
+        L.check(self.lib.nfg_nerf_create(self.ctx.h, C.byref(cfg), seed, C.byref(h)))
+        self.h = h
+        self.background = tuple(background)
+
+    def set_dataset(self, cams, rgb, width: int, height: int, focal: float) -> None:
+        cams = _f32(cams)
+        rgb = _f32(rgb)
+        self._keep = (cams, rgb)
+        L.check(self.lib.nfg_nerf_set_dataset(self.h, cams.shape[0], width, height, focal, _ptr(cams), _ptr(rgb)))
+
+    def train_step(self, step: int):
+        loss, nr, ns = C.c_float(), C.c_int64(), C.c_int64()
+        L.check(self.lib.nfg_nerf_train_step(self.h, step, C.byref(loss), C.byref(nr), C.byref(ns)))
+        return float(loss.value), int(nr.value), int(ns.value)
+
+    def render(self, cam, width: int, height: int, focal: float) -> np.ndarray:
+        cam = _f32(cam).reshape(12)
+        out = np.empty((height * width, 3), np.float32)
+        L.check(self.lib.nfg_nerf_render(self.h, _ptr(cam), width, height, focal, _ptr(out)))
+        return out
+
+    def occupancy(self):
+        bits = np.empty(OCC_RES ** 3 // 8, np.uint8)
+        dens = np.empty(OCC_RES ** 3, np.float32)
+        L.check(self.lib.nfg_nerf_occupancy(self.h, _ptr(bits), _ptr(dens)))
+        return bits, dens
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.nfg_nerf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nerf_march(rays, bits, max_steps: int = 1024, ctx: Optional[Context] = None):
+    """Occupancy-grid marching + compaction: (counts (n,), samples (total, 3))."""
+    ctx = ctx or default_context()
+    rays = _f32(rays)
+    bits = np.ascontiguousarray(bits, np.uint8)
+    n = rays.shape[0]
+    counts = np.zeros(n, np.uint32)
+    cap = n * max_steps
+    samples = np.empty((max(cap, 1), 3), np.float32)
+    tot = C.c_int64()
+    L.check(ctx.lib.nfg_nerf_march(ctx.h, _ptr(rays), n, _ptr(bits), max_steps, _ptr(counts), _ptr(samples), cap,
+                                   C.byref(tot)))
+    return counts, samples[: tot.value].copy()
+
+
+def nerf_composite(counts, raw, rgb, target, bg=(1.0, 1.0, 1.0), dt: float = 3 ** 0.5 / 1024,
+                   ctx: Optional[Context] = None):
+    """Compositing forward + backward: (color (R,3), d_rgb (S,3), d_raw (S,), loss_sum)."""
+    ctx = ctx or default_context()
+    counts = np.ascontiguousarray(counts, np.uint32)
+    raw, rgb, target = _f32(raw), _f32(rgb), _f32(target)
+    R, S = counts.shape[0], raw.shape[0]
+    color = np.empty((R, 3), np.float32)
+    d_rgb = np.empty((S, 3), np.float32)
+    d_raw = np.empty(S, np.float32)
+    bgv = np.asarray(bg, np.float32)
+    loss = C.c_double()
+    L.check(ctx.lib.nfg_nerf_composite(ctx.h, R, _ptr(counts), _ptr(raw), _ptr(rgb), _ptr(target), _ptr(bgv), dt,
+                                       _ptr(color), _ptr(d_rgb), _ptr(d_raw), C.byref(loss)))
+    return color, d_rgb, d_raw, float(loss.value)
+
+
+def nerf_sh4(dirs, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    dirs = _f32(dirs)
+    out = np.empty((dirs.shape[0], 16), np.float32)
+    L.check(ctx.lib.nfg_nerf_sh4(ctx.h, _ptr(dirs), dirs.shape[0], _ptr(out)))
+    return out
+
+
+def nerf_scene_render(cams, width: int, height: int, focal: float, bg=(1.0, 1.0, 1.0),
+                      ctx: Optional[Context] = None) -> np.ndarray:
+    """The synthetic procedural scene (BASELINE config 4) by fine marching: (n, h*w, 3)."""
+    ctx = ctx or default_context()
+    cams = _f32(cams)
+    out = np.empty((cams.shape[0], height * width, 3), np.float32)
+    bgv = np.asarray(bg, np.float32)
+    L.check(ctx.lib.nfg_nerf_scene_render(ctx.h, _ptr(cams), cams.shape[0], width, height, focal, _ptr(bgv),
+                                          _ptr(out)))
+    return out
+
+
 class PinnedBuffer:
     """Page-locked host memory (cudaMallocHost) viewed as a numpy array."""
 
