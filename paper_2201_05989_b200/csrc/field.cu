@@ -1257,6 +1257,31 @@ nfg_status nfg_field_backward_device(nfg_field* f, const float* X, int64_t B, co
         if (B <= 0)
             return;
         reset_scratch(f);
+        if (f->opts.fused_train && !f->opts.deterministic) {
+            // one fused encode -> MLP -> backward -> scatter kernel when built
+            nfg::TrainArgs a{};
+            a.X = X;
+            a.dout = dOut;
+            a.B = B;
+            a.inv_count = 1.0f;
+            a.table = table_ptr(f);
+            a.W = f->d_p + f->n_tab_dev;
+            a.b = f->d_p + f->n_tab_dev + f->n_w;
+            a.table_grad = f->d_g;
+            a.gW = f->d_g + f->n_tab_dev;
+            a.gb = f->d_g + f->n_tab_dev + f->n_w;
+            a.scratch = scratch_of(f);
+            const cudaError_t e = nfg::launch_train(f->shape, f->d_levels, nfg::SRC_ENCODE, nfg::GRAD_DOUT,
+                                                    nfg::SINK_SCATTER, a, c->num_sms, c->stream, nullptr);
+            if (e == cudaSuccess) {
+                c->launches++;
+                f->grads_clean = false;
+                return;
+            }
+            if (e != cudaErrorNotSupported)
+                NFG_CUDA(e);
+            cudaGetLastError();
+        }
         const size_t LF = size_t(f->shape.in_real);
         float* Y = static_cast<float*>(f->comp_y.get(size_t(B) * LF * 4));
         float* dY = static_cast<float*>(f->comp_dy.get(size_t(B) * LF * 4));

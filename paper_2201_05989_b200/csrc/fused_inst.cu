@@ -34,6 +34,25 @@ cudaError_t NFG_CAT(launch_fused_train_d, NFG_D)(const FieldShape& s, const Leve
     return cudaErrorNotSupported;
 }
 
+// Fused backward with an external dLoss/dOutput (nfg_field_backward_device:
+// the NeRF density network, 3D, L*F = 32, 1 or 2 hidden layers).
+cudaError_t NFG_CAT(launch_fused_dout_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
+                                                int num_sms, cudaStream_t st, int* grid_used)
+{
+#if NFG_D == 3
+    const bool f32 = s.table_fp32 != 0;
+#define X(F_, TT_, IS_, NH_)                                                                               \
+    if (s.grid.F == F_ && f32 == (sizeof(TT_) == 4) && s.in_steps == IS_ && s.hidden_layers == NH_)         \
+        return run_train<SRC_ENCODE, GRAD_DOUT, SINK_SCATTER, NFG_D, F_, TT_, IS_, NH_>(s, lv, a, num_sms, st, \
+                                                                                         grid_used);
+    X(2, __half, 2, 1) X(2, __half, 2, 2) X(2, float, 2, 1) X(2, float, 2, 2)
+#undef X
+#else
+    (void)s, (void)lv, (void)a, (void)num_sms, (void)st, (void)grid_used;
+#endif
+    return cudaErrorNotSupported;
+}
+
 cudaError_t NFG_CAT(launch_fused_infer_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const InferArgs& a,
                                                  int num_sms, cudaStream_t st)
 {

@@ -34,6 +34,8 @@ cudaError_t launch_staged_infer(const FieldShape& s, const InferArgs& a, int num
 
 cudaError_t launch_fused_train_d2(const FieldShape&, const LevelDev*, const TrainArgs&, int, cudaStream_t, int*);
 cudaError_t launch_fused_train_d3(const FieldShape&, const LevelDev*, const TrainArgs&, int, cudaStream_t, int*);
+cudaError_t launch_fused_dout_d2(const FieldShape&, const LevelDev*, const TrainArgs&, int, cudaStream_t, int*);
+cudaError_t launch_fused_dout_d3(const FieldShape&, const LevelDev*, const TrainArgs&, int, cudaStream_t, int*);
 cudaError_t launch_fused_infer_d2(const FieldShape&, const LevelDev*, const InferArgs&, int, cudaStream_t);
 cudaError_t launch_fused_infer_d3(const FieldShape&, const LevelDev*, const InferArgs&, int, cudaStream_t);
 
@@ -41,8 +43,11 @@ cudaError_t launch_train(const FieldShape& s, const LevelDev* lv, int src, int g
                          int num_sms, cudaStream_t st, int* grid_used)
 {
     if (src == SRC_ENCODE) {
-        if (grad != GRAD_LOSS || sink != SINK_SCATTER)
+        if (sink != SINK_SCATTER)
             return cudaErrorNotSupported;
+        if (grad == GRAD_DOUT)
+            return s.grid.d == 2 ? launch_fused_dout_d2(s, lv, a, num_sms, st, grid_used)
+                                 : launch_fused_dout_d3(s, lv, a, num_sms, st, grid_used);
         return s.grid.d == 2 ? launch_fused_train_d2(s, lv, a, num_sms, st, grid_used)
                              : launch_fused_train_d3(s, lv, a, num_sms, st, grid_used);
     }

@@ -116,3 +116,25 @@ def test_nerf_training_converges_and_culls():   # BASELINE config 4 shape at des
     # the scene's spheres are occupied
     c = [O.morton3(int(0.40 * 128), int(0.45 * 128), int(0.50 * 128))]
     assert (bits[c[0] >> 3] >> (c[0] & 7)) & 1
+
+
+def test_field_backward_device_fused_matches_staged():   # nfg_field_backward_device (density network)
+    nf = _nf()
+    import torch
+    g = nf.HashEncodingConfig(levels=16, table_size=1 << 14, features=2, n_min=16, n_max=512, dims=3)
+    grads = []
+    for fused in (True, False):
+        m = nf.FieldModel(options=nf.Options(table_fp32=True, fused_train=fused))
+        m.hash_cfg = g
+        m.mlp_cfg = nf.MlpConfig(hidden_layers=1, hidden_width=64, output_width=16)
+        m.init(5)
+        rng = O.Pcg32(5, 5)
+        X = torch.from_numpy(rng.floats(4000 * 3).reshape(4000, 3)).cuda()
+        dO = torch.from_numpy(rng.floats(4000 * 16).reshape(4000, 16) - 0.5).cuda() * 1e-3
+        from paper_2201_05989_b200 import _lib as L
+        L.check(m.lib.nfg_field_backward_device(m.h, X.data_ptr(), 4000, dO.data_ptr()))
+        m.check()
+        grads.append(m.grads)
+    a, b = grads
+    assert np.array_equal(a != 0, b != 0)
+    assert np.linalg.norm(a - b) <= 2e-2 * np.linalg.norm(b)
