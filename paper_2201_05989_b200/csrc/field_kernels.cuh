@@ -77,10 +77,21 @@ struct StageAlias {
     using SG = StageGeo<SRC, D, F, TT, IN_STEPS>;
     static constexpr int ROWS = 16;                               // sample rows per warp
     static constexpr int ELEMS = SG::STS * 4 * SG::NE;            // staged elements per thread and pass
+#ifdef NFG_PREFETCH
+    // gather-ahead (opt-in experiment): the next tile's corner loads are issued
+    // right after the loss barrier and land while this tile runs its backward,
+    // scatter and dW. Measured 2% SLOWER than the aliased single-tile staging
+    // (287 vs 281 us, tools/exp_pf.sh): the two CTAs per SM already overlap one
+    // CTA's gathers with the other's compute, and the separate staging area
+    // costs L1 capacity.
+    static constexpr bool PREFETCH = SRC == SRC_ENCODE && SG::STS >= IN_STEPS;
+#else
+    static constexpr bool PREFETCH = false;
+#endif
 #ifdef NFG_NO_ALIAS_STAGE
     static constexpr bool ON = false;
 #else
-    static constexpr bool ON = SRC == SRC_ENCODE && NH >= 2 && SG::SB == 4 && 32 * SG::SB <= 2 * H &&
+    static constexpr bool ON = !PREFETCH && SRC == SRC_ENCODE && NH >= 2 && SG::SB == 4 && 32 * SG::SB <= 2 * H &&
                                ELEMS <= 4 * ROWS;
 #endif
 };
@@ -240,78 +251,112 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     NFG_PT_DECL
     const int64_t ntiles = (a.B + TS - 1) / TS;
     const int r0 = 16 * warp;
+    const TT* tab = static_cast<const TT*>(a.table);
+    // streamed inputs: thread 0 waits for the chunk holding tile tl's last sample
+    auto wait_ready = [&](int64_t tl) {
+        if (a.ready && tid == 0) {
+            const int64_t last = min(a.B, (tl + 1) * TS) - 1;
+            const unsigned int* f = a.ready + last / a.chunk;
+            unsigned int v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                if (int(v - a.epoch) >= 0)
+                    break;
+                __nanosleep(100);
+            }
+        }
+    };
+    auto load_inputs = [&](int64_t tl, float* x, float* x8) {
+        const int64_t s0_ = tl * TS + r0 + g, s8_ = s0_ + 8;
+        load_x<D>(x, a.X, s0_, s0_ < a.B);
+        load_x<D>(x8, a.X, s8_, s8_ < a.B);
+        if (a.validate) {   // encode_forward's checks (grid.hpp:226-229)
+            const float lo = -1e-6f, hi = 1.0f + 1e-6f;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                invalid |= (finite_f(x[i]) ? 0u : 1u) | ((x[i] < lo || x[i] > hi) ? 2u : 0u);
+                invalid |= (finite_f(x8[i]) ? 0u : 1u) | ((x8[i] < lo || x8[i] > hi) ? 2u : 0u);
+            }
+        }
+    };
+    // corner loads of one pass (SG::STS k16 steps) as cp.async copies
+    auto issue_pass = [&](int s0, const auto& slots, const float* x, const float* x8, bool v, bool v8) {
+#pragma unroll
+        for (int sl = 0; sl < SG::STS; ++sl)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
+                const int p = (sl * 2 + h) * 2;
+                if (s0 + sl < IN_STEPS && v)
+                    gather_issue<D, F, TT>(s.grid, lvs, x, col, tab, slots, p * SG::NE);
+                if (s0 + sl < IN_STEPS && v8)
+                    gather_issue<D, F, TT>(s.grid, lvs, x8, col, tab, slots, (p + 1) * SG::NE);
+            }
+    };
+    auto blend_pass = [&](int s0, const auto& slots, const float* x, const float* x8, bool v, bool v8,
+                          uint32_t (&fr)[IN_STEPS][4]) {
+#pragma unroll
+        for (int sl = 0; sl < SG::STS; ++sl)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (s0 + sl >= IN_STEPS)
+                    continue;
+                const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
+                const int p = (sl * 2 + h) * 2;
+                const float2 e0 = v ? gather_blend<D, F, TT>(s.grid, lvs, x, col, slots, p * SG::NE)
+                                    : make_float2(0.f, 0.f);
+                const float2 e8 = v8 ? gather_blend<D, F, TT>(s.grid, lvs, x8, col, slots, (p + 1) * SG::NE)
+                                     : make_float2(0.f, 0.f);
+                fr[s0 + sl][2 * h] = pack_half2(e0.x, e0.y);
+                fr[s0 + sl][2 * h + 1] = pack_half2(e8.x, e8.y);
+            }
+    };
+    const SlotsLinear lin_slots{ sm + SM::STAGE_OFF + tid * SG::SB, TW * 32 * SG::SB };
+    float xn[D], xn8[D];   // gather-ahead: inputs of the next tile
+    if (SA::PREFETCH && int64_t(blockIdx.x) < ntiles) {
+        wait_ready(blockIdx.x);
+        if (a.ready)
+            __syncthreads();
+        load_inputs(blockIdx.x, xn, xn8);
+        const int64_t s0_ = int64_t(blockIdx.x) * TS + r0 + g;
+        issue_pass(0, lin_slots, xn, xn8, s0_ < a.B, s0_ + 8 < a.B);
+    }
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         NFG_PT_START();
         const int64_t sg = tile * TS + r0 + g, sg8 = sg + 8;
         const bool vg = sg < a.B, vg8 = sg8 < a.B;
-        if (a.ready) {   // streamed inputs: wait for this tile's chunk to land
-            if (tid == 0) {
-                const int64_t last = min(a.B, (tile + 1) * TS) - 1;
-                const unsigned int* f = a.ready + last / a.chunk;
-                unsigned int v;
-                for (;;) {
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-                    if (int(v - a.epoch) >= 0)
-                        break;
-                    __nanosleep(100);
-                }
-            }
+        if (!SA::PREFETCH && a.ready) {   // streamed inputs: wait for this tile's chunk to land
+            wait_ready(tile);
             __syncthreads();
         }
         float xg[D], xg8[D];
-        if (SRC == SRC_ENCODE) {
-            load_x<D>(xg, a.X, sg, vg);
-            load_x<D>(xg8, a.X, sg8, vg8);
-            if (a.validate) {   // encode_forward's checks (grid.hpp:226-229)
-                const float lo = -1e-6f, hi = 1.0f + 1e-6f;
+        if (SA::PREFETCH) {
 #pragma unroll
-                for (int i = 0; i < D; ++i) {
-                    invalid |= (finite_f(xg[i]) ? 0u : 1u) | ((xg[i] < lo || xg[i] > hi) ? 2u : 0u);
-                    invalid |= (finite_f(xg8[i]) ? 0u : 1u) | ((xg8[i] < lo || xg8[i] > hi) ? 2u : 0u);
-                }
+            for (int i = 0; i < D; ++i) {
+                xg[i] = xn[i];
+                xg8[i] = xn8[i];
             }
+        } else if (SRC == SRC_ENCODE) {
+            load_inputs(tile, xg, xg8);
         }
         // ---- encode / load inputs -------------------------------------
         uint32_t afr[IN_STEPS][4];
         if (SRC == SRC_ENCODE) {
             // all corner loads of SG::STS k16 steps in flight at once (cp.async)
-            const TT* tab = static_cast<const TT*>(a.table);
             auto encode_all = [&](const auto& slots) {
 #pragma unroll
                 for (int s0 = 0; s0 < IN_STEPS; s0 += SG::STS) {
-#pragma unroll
-                    for (int sl = 0; sl < SG::STS; ++sl)
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
-                            const int p = (sl * 2 + h) * 2;
-                            if (s0 + sl < IN_STEPS && vg)
-                                gather_issue<D, F, TT>(s.grid, lvs, xg, col, tab, slots, p * SG::NE);
-                            if (s0 + sl < IN_STEPS && vg8)
-                                gather_issue<D, F, TT>(s.grid, lvs, xg8, col, tab, slots, (p + 1) * SG::NE);
-                        }
+                    issue_pass(s0, slots, xg, xg8, vg, vg8);
                     cp_async_wait_all();
-#pragma unroll
-                    for (int sl = 0; sl < SG::STS; ++sl)
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            if (s0 + sl >= IN_STEPS)
-                                continue;
-                            const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
-                            const int p = (sl * 2 + h) * 2;
-                            const float2 e0 = vg ? gather_blend<D, F, TT>(s.grid, lvs, xg, col, slots, p * SG::NE)
-                                                 : make_float2(0.f, 0.f);
-                            const float2 e8 = vg8 ? gather_blend<D, F, TT>(s.grid, lvs, xg8, col, slots,
-                                                                            (p + 1) * SG::NE)
-                                                  : make_float2(0.f, 0.f);
-                            afr[s0 + sl][2 * h] = pack_half2(e0.x, e0.y);
-                            afr[s0 + sl][2 * h + 1] = pack_half2(e8.x, e8.y);
-                        }
+                    blend_pass(s0, slots, xg, xg8, vg, vg8, afr);
                     if (SA::ON && s0 + SG::STS < IN_STEPS)
                         __syncwarp();   // next pass reuses the warp's rows
                 }
             };
-            if constexpr (SA::ON) {
+            if constexpr (SA::PREFETCH) {
+                cp_async_wait_all();   // this tile's loads, issued during the previous tile
+                blend_pass(0, lin_slots, xg, xg8, vg, vg8, afr);
+            } else if constexpr (SA::ON) {
                 SlotsChunked<SA::ROWS, HS * 2, 4> slots;
                 slots.chunk[0] = reinterpret_cast<unsigned char*>(acth + r0 * HS);
                 slots.chunk[1] = reinterpret_cast<unsigned char*>(acth + TS * HS + r0 * HS);
@@ -321,8 +366,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 encode_all(slots);
                 __syncwarp();   // every lane's staged rows consumed before the warp writes them
             } else {
-                const SlotsLinear slots{ sm + SM::STAGE_OFF + tid * SG::SB, TW * 32 * SG::SB };
-                encode_all(slots);
+                encode_all(lin_slots);
             }
         } else {
             input_frags<SRC, D, F, TT, IN_STEPS>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
@@ -390,8 +434,17 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                     atomicAdd(a.scratch.loss_sum, double(term));
             }
         }
+        const int64_t next_tile = tile + gridDim.x;
+        if (SA::PREFETCH && next_tile < ntiles)
+            wait_ready(next_tile);   // published to the CTA by the barrier below
         __syncthreads();
         NFG_PT(2);
+        if (SA::PREFETCH && next_tile < ntiles) {
+            // every warp has blended this tile (barrier above): its slots are free
+            load_inputs(next_tile, xn, xn8);
+            const int64_t s0_ = next_tile * TS + r0 + g;
+            issue_pass(0, lin_slots, xn, xn8, s0_ < a.B, s0_ + 8 < a.B);
+        }
         float tmax = 0.0f;
 #pragma unroll
         for (int w = 0; w < TW; ++w)
