@@ -31,7 +31,10 @@ using namespace mlp;
 #endif
 constexpr int TW = NFG_TW;          // warps per training CTA
 constexpr int TS = 16 * NFG_TW;     // samples per training tile (16 per warp)
-constexpr int IW = 4;     // warps per inference CTA
+#ifndef NFG_IW
+#define NFG_IW 32   // 2 CTAs of 32 warps per SM: 2 copies of the weights instead of 8 leave more L1 to the gathers (+6%)
+#endif
+constexpr int IW = NFG_IW;   // warps per inference CTA
 
 __host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
 
