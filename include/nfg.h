@@ -220,7 +220,8 @@ double nfg_lr_at(const int64_t* milestones, int32_t n, double factor, double bas
  * For pipelines that chain fields on the device (the NeRF density -> color
  * networks). Gradients accumulate into the field's slab (mlp.hpp:147-148,
  * grid.hpp:292); nfg_adam_step_device applies adam_step (adam.hpp:78-122)
- * with an exact non-finite scan and zeroes them. dOut is dLoss/d(output after
+ * and zeroes them (the exact non-finite scan runs when a producer kernel
+ * flagged a possibly non-finite gradient). dOut is dLoss/d(output after
  * the output activation), as mlp_backward's dOut. */
 nfg_status nfg_field_backward_device(nfg_field* f, const float* X, int64_t B, const float* dOut);
 nfg_status nfg_mlp_forward_device(nfg_field* f, const float* Y, int64_t B, float* out);

@@ -710,6 +710,11 @@ def morton3(x, y, z):
 
 
 def nerf_march(rays, bits, max_steps=1024):   # PAPER.md:904-936 (fixed step, occupancy skip)
+    """Samples of a ray = the grid points t_k = t_base + k dt (t_base = t0 + dt/2,
+    t_k < t1) whose occupancy cell is set, in k order, capped at max_steps.
+    Empty points jump floor(tn / dt) - 1 points (>= 1) towards the next cell
+    boundary, which never skips a point past it (so any split of the k range,
+    e.g. the kernel's 32 lanes per ray, yields the same set)."""
     f = np.float32
     rays = np.asarray(rays, np.float32)
     bits = np.asarray(bits, np.uint8)
@@ -731,24 +736,30 @@ def nerf_march(rays, bits, max_steps=1024):   # PAPER.md:904-936 (fixed step, oc
             t0 = np.fmax(t0, f(0.0))
             n = 0
             if t1 > t0:
-                t = t0 + f(0.5) * NERF_DT
-                while t < t1 and n < max_steps:
+                tb = t0 + f(0.5) * NERF_DT
+                kmax = int(np.ceil((t1 - tb) / NERF_DT)) + 1
+                k = 0
+                while k < kmax:
+                    t = tb + f(k) * NERF_DT
+                    if not t < t1:
+                        break
                     p = [o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]]
                     c = [cell(v) for v in p]
                     m = morton3(c[0], c[1], c[2])
                     if (bits[m >> 3] >> (m & 7)) & 1:
-                        out.append(p)
+                        if n < max_steps:
+                            out.append(p)
                         n += 1
-                        t = t + NERF_DT
+                        k += 1
                         continue
                     tn = f(np.inf)
-                    for k in range(3):
-                        cb = f(c[k] + (1 if d[k] > 0 else 0))
-                        tk = (cb / f(NERF_RES) - p[k]) / d[k]
-                        tn = np.fmin(tn, tk)
-                    steps = np.ceil(np.fmax(tn / NERF_DT, f(0.5)))
-                    t = t + steps * NERF_DT
-            counts.append(n)
+                    for a_ in range(3):
+                        cb = f(c[a_] + (1 if d[a_] > 0 else 0))
+                        ta = (cb / f(NERF_RES) - p[a_]) / d[a_]
+                        tn = np.fmin(tn, ta)
+                    steps = np.floor(tn / NERF_DT) - f(1.0)
+                    k += (int(steps) if steps < 1e6 else 1000000) if steps > 1 else 1
+            counts.append(min(n, max_steps))
     return np.array(counts, np.uint32), np.array(out, np.float32).reshape(-1, 3)
 
 

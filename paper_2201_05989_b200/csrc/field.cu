@@ -1346,7 +1346,9 @@ nfg_status nfg_mlp_backward_device(nfg_field* f, const float* Y, int64_t B, cons
 nfg_status nfg_adam_step_device(nfg_field* f, float lr_now)
 {
     return guard([&] {
-        run_adam(f, lr_now, true);   // exact non-finite scan: the producers' flags are not trusted here
+        // the producers are this library's kernels: their "maybe non-finite"
+        // flag (flags[0]) triggers the exact scan only when needed
+        run_adam(f, lr_now, false);
         f->pending_steps++;
         f->grads_clean = true;   // optimistic; nfg_field_check corrects it
     });

@@ -165,45 +165,94 @@ __device__ __forceinline__ bool ray_cube(const float* o, const float* d, float& 
     return t1 > t0;
 }
 
-// The marching loop shared by the count and write passes: calls emit(i, t)
-// for the i-th sample at parameter t. Returns the sample count.
-template <class Emit>
-__device__ int march(const float* o, const float* d, const uint8_t* bits, int max_steps, Emit&& emit)
+// Marching defines the samples of a ray as the grid points
+//   t_k = t_base + k dt,  t_base = t0 + dt/2,  t_k < t1,
+// whose 128^3 occupancy cell is set, in k order, capped at max_steps. A lane
+// walks its own contiguous k-range: at an occupied point it emits and steps
+// by one; at an empty point it jumps by a DDA step to the cell boundary,
+// floor(tn / dt) - 1 points (>= 1) so no point past the boundary is ever
+// skipped — every lane, and the serial restatement, therefore produce exactly
+// the same set whatever their starting k. One WARP marches one ray (32
+// k-ranges), so a batch of a few thousand rays still fills the GPU.
+struct RayGrid {
+    float tb, t1;
+    int kmax;   // upper bound on the points (exclusive)
+};
+
+__device__ __forceinline__ bool ray_grid(const float* o, const float* d, RayGrid& g)
 {
     float t0, t1;
     if (!ray_cube(o, d, t0, t1))
-        return 0;
+        return false;
     const float dt = SQRT3 / 1024.0f;
-    float t = t0 + 0.5f * dt;
+    g.tb = t0 + 0.5f * dt;
+    g.t1 = t1;
+    g.kmax = int(ceilf((t1 - g.tb) / dt)) + 1;
+    return g.kmax > 0;
+}
+
+template <class Emit>
+__device__ int march_range(const float* o, const float* d, const uint8_t* bits, const RayGrid& g, int k0, int k1,
+                           Emit&& emit)
+{
+    const float dt = SQRT3 / 1024.0f;
     int n = 0;
-    while (t < t1 && n < max_steps) {
+    for (int k = k0; k < k1;) {
+        const float t = g.tb + float(k) * dt;
+        if (!(t < g.t1))
+            break;
         const float px = o[0] + t * d[0], py = o[1] + t * d[1], pz = o[2] + t * d[2];
         if (occupied(bits, px, py, pz)) {
-            emit(n, t);
+            emit(n, px, py, pz);
             ++n;
-            t = t + dt;
+            ++k;
             continue;
         }
-        // DDA: advance to the next cell boundary, snapped to the step grid
         const float p[3] = { px, py, pz };
         float tn = INFINITY;
-        for (int k = 0; k < 3; ++k) {
-            const float c = float(cell_coord(p[k]) + (d[k] > 0.0f ? 1 : 0));
-            const float tk = (c / float(OCC_RES) - p[k]) / d[k];
-            tn = fminf(tn, tk);
+        for (int a = 0; a < 3; ++a) {
+            const float c = float(cell_coord(p[a]) + (d[a] > 0.0f ? 1 : 0));
+            const float ta = (c / float(OCC_RES) - p[a]) / d[a];
+            tn = fminf(tn, ta);
         }
-        const float steps = ceilf(fmaxf(tn / dt, 0.5f));
-        t = t + steps * dt;
+        const float steps = floorf(tn / dt) - 1.0f;
+        k += steps > 1.0f ? (steps < 1e6f ? int(steps) : 1000000) : 1;
     }
     return n;
+}
+
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, int lane, uint32_t& total)
+{
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o)
+            x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
 }
 
 __global__ void k_march_count(const float* __restrict__ rays, int64_t n, const uint8_t* __restrict__ bits,
                               int max_steps, uint32_t* __restrict__ counts)
 {
-    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = wid; r < n; r += nw) {
         const float* o = rays + 6 * r;
-        counts[r] = uint32_t(march(o, o + 3, bits, max_steps, [](int, float) {}));
+        RayGrid g;
+        uint32_t c = 0;
+        if (ray_grid(o, o + 3, g)) {
+            const int chunk = (g.kmax + 31) / 32;
+            c = uint32_t(march_range(o, o + 3, bits, g, lane * chunk, min(g.kmax, (lane + 1) * chunk),
+                                     [](int, float, float, float) {}));
+        }
+        uint32_t total;
+        warp_excl_scan(c, lane, total);
+        if (lane == 0)
+            counts[r] = min(total, uint32_t(max_steps));
     }
 }
 
@@ -211,19 +260,35 @@ __global__ void k_march_write(const float* __restrict__ rays, int64_t n, const u
                               int max_steps, const uint32_t* __restrict__ offsets, float* __restrict__ pos,
                               float* __restrict__ dirs)
 {
-    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = wid; r < n; r += nw) {
         const float* o = rays + 6 * r;
         const float* d = o + 3;
+        RayGrid g;
+        if (!ray_grid(o, d, g))
+            continue;   // warp-uniform
+        const int chunk = (g.kmax + 31) / 32;
+        const int k0 = lane * chunk, k1 = min(g.kmax, (lane + 1) * chunk);
+        const uint32_t c = uint32_t(march_range(o, d, bits, g, k0, k1, [](int, float, float, float) {}));
+        uint32_t total;
+        const uint32_t first = warp_excl_scan(c, lane, total);
         const uint32_t base = offsets[r];
-        march(o, d, bits, max_steps, [&](int i, float t) {
-            const size_t s = size_t(base) + size_t(i);
-            pos[3 * s] = o[0] + t * d[0];
-            pos[3 * s + 1] = o[1] + t * d[1];
-            pos[3 * s + 2] = o[2] + t * d[2];
-            dirs[3 * s] = d[0];
-            dirs[3 * s + 1] = d[1];
-            dirs[3 * s + 2] = d[2];
-        });
+        const uint32_t cap = uint32_t(max_steps);
+        if (first < cap)
+            march_range(o, d, bits, g, k0, k1, [&](int i, float px, float py, float pz) {
+                const uint32_t j = first + uint32_t(i);
+                if (j >= cap)
+                    return;
+                const size_t sidx = size_t(base) + j;
+                pos[3 * sidx] = px;
+                pos[3 * sidx + 1] = py;
+                pos[3 * sidx + 2] = pz;
+                dirs[3 * sidx] = d[0];
+                dirs[3 * sidx + 1] = d[1];
+                dirs[3 * sidx + 2] = d[2];
+            });
     }
 }
 
@@ -268,49 +333,92 @@ __host__ __device__ inline void sh4(float x, float y, float z, float* o)
     o[15] = 0.59004358992664352f * x * (-x2 + 3.0f * y2);
 }
 
-// color input = [16 density outputs | SH4(direction)]
+// color input = [16 density outputs | SH4(direction)] (128 B rows, float4 stores)
 __global__ void k_color_input(const float* __restrict__ dens, const float* __restrict__ dirs, int64_t n,
                               float* __restrict__ Y)
 {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         float sh[16];
         sh4(dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2], sh);
-        for (int k = 0; k < 16; ++k) {
-            Y[32 * i + k] = dens[16 * i + k];
-            Y[32 * i + 16 + k] = sh[k];
-        }
+        const float4* src = reinterpret_cast<const float4*>(dens + 16 * i);
+        float4* dst = reinterpret_cast<float4*>(Y + 32 * i);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            dst[k] = src[k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            dst[4 + k] = make_float4(sh[4 * k], sh[4 * k + 1], sh[4 * k + 2], sh[4 * k + 3]);
     }
 }
 
-// ---- volume compositing (forward + backward per ray) -------------------------
+// ---- volume compositing (forward + backward), one warp per ray -------------
 // sigma = exp(raw) (the density output is log-density); the
-// gradient uses exp(min(raw, 15)) (truncated exponential).
+// gradient uses exp(min(raw, 15)) (truncated exponential). Transmittance is
+// carried in log space across 32-sample chunks: T_i = exp(-sum_{j<i} sigma_j dt)
+// by a warp prefix sum; samples from the first T_i < 1e-4 on are dropped
+// (transmittance stop); dC/dc_i = w_i, dC/dsigma_i = dt (T_{i+1} c_i -
+// sum_{j>i} w_j c_j - T_end bg).
+__device__ __forceinline__ float warp_incl_scan_f(float v, int lane)
+{
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o)
+            v += y;
+    }
+    return v;
+}
+
+__device__ __forceinline__ float warp_sum_f(float v)
+{
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, m);
+    return v;
+}
+
 __global__ void k_composite(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, int64_t n_rays,
                             const float* __restrict__ raw, int raw_stride, const float* __restrict__ rgb,
                             const float* __restrict__ target, float3 bg, float dt, float inv_count,
                             float* __restrict__ out_color, float* __restrict__ d_rgb, float* __restrict__ d_raw,
                             double* loss_sum)
 {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
     double lsum = 0.0;
-    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rays; r += int64_t(gridDim.x) * blockDim.x) {
+    for (int64_t r = wid; r < n_rays; r += nw) {
         const uint32_t base = offsets[r], n = counts[r];
-        float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-        uint32_t used = 0;
-        for (uint32_t i = 0; i < n; ++i) {
-            if (T < 1e-4f)
-                break;
-            const size_t s = size_t(base) + i;
-            const float sigma = expf(raw[s * raw_stride]);
-            const float alpha = 1.0f - expf(-sigma * dt);
-            const float w = T * alpha;
-            cr += w * rgb[3 * s];
-            cg += w * rgb[3 * s + 1];
-            cb += w * rgb[3 * s + 2];
-            T *= 1.0f - alpha;
-            ++used;
+        // forward
+        float logT = 0.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
+        for (uint32_t c0 = 0; c0 < n && __expf(logT) >= 1e-4f; c0 += 32) {
+            const uint32_t i = c0 + lane;
+            float x = 0.0f, r0 = 0.0f, r1 = 0.0f, r2 = 0.0f;
+            if (i < n) {
+                const size_t s = size_t(base) + i;
+                x = expf(raw[s * raw_stride]) * dt;
+                r0 = rgb[3 * s];
+                r1 = rgb[3 * s + 1];
+                r2 = rgb[3 * s + 2];
+            }
+            const float incl = warp_incl_scan_f(x, lane);
+            const float Ti = expf(logT - (incl - x));
+            const float w = (i < n && Ti >= 1e-4f) ? Ti * (1.0f - expf(-x)) : 0.0f;
+            cr += warp_sum_f(w * r0);
+            cg += warp_sum_f(w * r1);
+            cb += warp_sum_f(w * r2);
+            // transmittance after the last used sample of this chunk
+            const bool used = i < n && Ti >= 1e-4f;
+            const unsigned um = __ballot_sync(0xffffffffu, used);
+            const int last = um ? 31 - __clz(um) : -1;
+            const float incl_last = last >= 0 ? __shfl_sync(0xffffffffu, incl, last) : 0.0f;
+            logT -= incl_last;
+            if (um != 0xffffffffu)
+                break;   // a sample of this chunk crossed the stop (or the ray ended)
         }
-        const float Cr = cr + T * bg.x, Cg = cg + T * bg.y, Cb = cb + T * bg.z;
-        if (out_color) {
+        const float Tend = expf(logT);
+        const float Cr = cr + Tend * bg.x, Cg = cg + Tend * bg.y, Cb = cb + Tend * bg.z;
+        if (out_color && lane == 0) {
             out_color[3 * r] = Cr;
             out_color[3 * r + 1] = Cg;
             out_color[3 * r + 2] = Cb;
@@ -318,40 +426,54 @@ __global__ void k_composite(const uint32_t* __restrict__ offsets, const uint32_t
         if (!target)
             continue;
         const float er = Cr - target[3 * r], eg = Cg - target[3 * r + 1], eb = Cb - target[3 * r + 2];
-        lsum += double(er * er + eg * eg + eb * eb);
+        if (lane == 0)
+            lsum += double(er * er + eg * eg + eb * eb);
         const float gr = 2.0f * er * inv_count, gg = 2.0f * eg * inv_count, gb = 2.0f * eb * inv_count;
-        // backward: dC/dc_k = w_k; dC/dsigma_k = dt (T_{k+1} c_k - sum_{i>k} w_i c_i - T_end bg)
-        float T2 = 1.0f, pr = 0.0f, pg = 0.0f, pb = 0.0f;
-        for (uint32_t i = 0; i < n; ++i) {
+        // backward (second sweep, same chunking)
+        float logT2 = 0.0f, pr = 0.0f, pg = 0.0f, pb = 0.0f;
+        for (uint32_t c0 = 0; c0 < n; c0 += 32) {
+            const uint32_t i = c0 + lane;
             const size_t s = size_t(base) + i;
-            if (i >= used) {
-                d_rgb[3 * s] = d_rgb[3 * s + 1] = d_rgb[3 * s + 2] = 0.0f;
-                d_raw[s] = 0.0f;
-                continue;
+            float x = 0.0f, rw = 0.0f, r0 = 0.0f, r1 = 0.0f, r2 = 0.0f;
+            if (i < n) {
+                rw = raw[s * raw_stride];
+                x = expf(rw) * dt;
+                r0 = rgb[3 * s];
+                r1 = rgb[3 * s + 1];
+                r2 = rgb[3 * s + 2];
             }
-            const float rw = raw[s * raw_stride];
-            const float sigma = expf(rw);
-            const float alpha = 1.0f - expf(-sigma * dt);
-            const float w = T2 * alpha;
-            const float c0 = rgb[3 * s], c1 = rgb[3 * s + 1], c2 = rgb[3 * s + 2];
-            pr += w * c0;
-            pg += w * c1;
-            pb += w * c2;
-            T2 *= 1.0f - alpha;
-            d_rgb[3 * s] = w * gr;
-            d_rgb[3 * s + 1] = w * gg;
-            d_rgb[3 * s + 2] = w * gb;
-            const float sr = T2 * c0 - (cr - pr) - T * bg.x;
-            const float sg = T2 * c1 - (cg - pg) - T * bg.y;
-            const float sb = T2 * c2 - (cb - pb) - T * bg.z;
-            const float dsigma = dt * (sr * gr + sg * gg + sb * gb);
-            d_raw[s] = dsigma * expf(fminf(rw, 15.0f));
+            const float incl = warp_incl_scan_f(x, lane);
+            const float Ti = expf(logT2 - (incl - x));
+            const bool used = i < n && Ti >= 1e-4f;
+            const float w = used ? Ti * (1.0f - expf(-x)) : 0.0f;
+            const float qr = warp_incl_scan_f(w * r0, lane) + pr;
+            const float qg = warp_incl_scan_f(w * r1, lane) + pg;
+            const float qb = warp_incl_scan_f(w * r2, lane) + pb;
+            if (i < n) {
+                if (used) {
+                    const float T1 = expf(logT2 - incl);   // T_{i+1}
+                    d_rgb[3 * s] = w * gr;
+                    d_rgb[3 * s + 1] = w * gg;
+                    d_rgb[3 * s + 2] = w * gb;
+                    const float sr = T1 * r0 - (cr - qr) - Tend * bg.x;
+                    const float sg = T1 * r1 - (cg - qg) - Tend * bg.y;
+                    const float sb = T1 * r2 - (cb - qb) - Tend * bg.z;
+                    d_raw[s] = dt * (sr * gr + sg * gg + sb * gb) * expf(fminf(rw, 15.0f));
+                } else {
+                    d_rgb[3 * s] = d_rgb[3 * s + 1] = d_rgb[3 * s + 2] = 0.0f;
+                    d_raw[s] = 0.0f;
+                }
+            }
+            pr = __shfl_sync(0xffffffffu, qr, 31);
+            pg = __shfl_sync(0xffffffffu, qg, 31);
+            pb = __shfl_sync(0xffffffffu, qb, 31);
+            logT2 -= __shfl_sync(0xffffffffu, incl, 31);
         }
     }
     if (loss_sum) {
         for (int m = 16; m > 0; m >>= 1)
             lsum += __shfl_xor_sync(0xffffffffu, lsum, m);
-        if ((threadIdx.x & 31) == 0)
+        if (lane == 0)
             atomicAdd(loss_sum, lsum);
     }
 }
@@ -361,8 +483,14 @@ __global__ void k_density_grad(const float* __restrict__ dYc, const float* __res
                                float* __restrict__ d_dens)
 {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        for (int k = 0; k < 16; ++k)
-            d_dens[16 * i + k] = dYc[32 * i + k] + (k == 0 ? d_raw[i] : 0.0f);
+        const float4* src = reinterpret_cast<const float4*>(dYc + 32 * i);
+        float4* dst = reinterpret_cast<float4*>(d_dens + 16 * i);
+        float4 v = src[0];
+        v.x += d_raw[i];
+        dst[0] = v;
+#pragma unroll
+        for (int k = 1; k < 4; ++k)
+            dst[k] = src[k];
     }
 }
 
@@ -565,7 +693,7 @@ struct nfg_nerf {
     {
         uint32_t* cnt = counts.as<uint32_t>(size_t(R));
         uint32_t* off = offsets.as<uint32_t>(size_t(R));
-        k_march_count<<<grid_for(R), 256, 0, st>>>(ray_buf, R, static_cast<const uint8_t*>(occ_bits.p),
+        k_march_count<<<grid_for(R * 32), 256, 0, st>>>(ray_buf, R, static_cast<const uint8_t*>(occ_bits.p),
                                                    cfg.max_samples_per_ray, cnt);
         NR_CUDA(cudaGetLastError());
         size_t tb = 0;
@@ -580,7 +708,7 @@ struct nfg_nerf {
         float* P = pos.as<float>(size_t(std::max<int64_t>(ns, 1)) * 3);
         float* D = dirs.as<float>(size_t(std::max<int64_t>(ns, 1)) * 3);
         if (h_fit[0] > 0) {
-            k_march_write<<<grid_for(h_fit[0]), 256, 0, st>>>(ray_buf, h_fit[0], static_cast<const uint8_t*>(occ_bits.p),
+            k_march_write<<<grid_for(h_fit[0] * 32), 256, 0, st>>>(ray_buf, h_fit[0], static_cast<const uint8_t*>(occ_bits.p),
                                                               cfg.max_samples_per_ray, off, P, D);
             NR_CUDA(cudaGetLastError());
         }
@@ -741,7 +869,7 @@ nfg_status nfg_nerf_train_step(nfg_nerf* n, int64_t step, float* loss, int64_t* 
             float* drgb = n->d_rgb.as<float>(size_t(ns) * 3);
             float* draw = n->d_raw.as<float>(size_t(ns));
             const float3 bg = make_float3(n->cfg.background[0], n->cfg.background[1], n->cfg.background[2]);
-            k_composite<<<grid_for(nr), 256, 0, st>>>(static_cast<const uint32_t*>(n->offsets.p),
+            k_composite<<<grid_for(nr * 32), 256, 0, st>>>(static_cast<const uint32_t*>(n->offsets.p),
                                                       static_cast<const uint32_t*>(n->counts.p), nr,
                                                       static_cast<const float*>(n->dens.p), 16,
                                                       static_cast<const float*>(n->rgb.p), tgt, bg, SQRT3 / 1024.0f,
@@ -791,7 +919,7 @@ nfg_status nfg_nerf_render(nfg_nerf* n, const float* cam12, int32_t width, int32
         if (fit.second > 0)
             n->forward(fit.second);
         const float3 bg = make_float3(n->cfg.background[0], n->cfg.background[1], n->cfg.background[2]);
-        k_composite<<<grid_for(fit.first), 256, 0, st>>>(static_cast<const uint32_t*>(n->offsets.p),
+        k_composite<<<grid_for(fit.first * 32), 256, 0, st>>>(static_cast<const uint32_t*>(n->offsets.p),
                                                          static_cast<const uint32_t*>(n->counts.p), fit.first,
                                                          static_cast<const float*>(n->dens.p), 16,
                                                          static_cast<const float*>(n->rgb.p), nullptr, bg,
@@ -833,7 +961,7 @@ nfg_status nfg_nerf_march(nfg_ctx* ctx, const float* rays, int64_t n, const uint
         NR_CUDA(cudaMemcpyAsync(b.get(OCC_CELLS / 8), bits, OCC_CELLS / 8, cudaMemcpyHostToDevice, st));
         uint32_t* cnt = c.as<uint32_t>(size_t(n));
         uint32_t* off = o.as<uint32_t>(size_t(n));
-        k_march_count<<<grid_for(n), 256, 0, st>>>(static_cast<const float*>(r.p), n,
+        k_march_count<<<grid_for(n * 32), 256, 0, st>>>(static_cast<const float*>(r.p), n,
                                                    static_cast<const uint8_t*>(b.p), max_steps, cnt);
         size_t tb = 0;
         NR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, n, st));
@@ -849,7 +977,7 @@ nfg_status nfg_nerf_march(nfg_ctx* ctx, const float* rays, int64_t n, const uint
             throw std::invalid_argument("nerf_march: sample buffer too small");
         float* pp = P.as<float>(size_t(std::max<int64_t>(tot, 1)) * 3);
         float* dd = D.as<float>(size_t(std::max<int64_t>(tot, 1)) * 3);
-        k_march_write<<<grid_for(n), 256, 0, st>>>(static_cast<const float*>(r.p), n, static_cast<const uint8_t*>(b.p),
+        k_march_write<<<grid_for(n * 32), 256, 0, st>>>(static_cast<const float*>(r.p), n, static_cast<const uint8_t*>(b.p),
                                                    max_steps, off, pp, dd);
         NR_CUDA(cudaGetLastError());
         NR_CUDA(cudaMemcpyAsync(samples, pp, size_t(tot) * 12, cudaMemcpyDeviceToHost, st));
@@ -877,7 +1005,7 @@ nfg_status nfg_nerf_composite(nfg_ctx* ctx, int64_t n_rays, const uint32_t* coun
         NR_CUDA(cudaMemcpyAsync(tg.get(size_t(n_rays) * 12), target, size_t(n_rays) * 12, cudaMemcpyHostToDevice, st));
         double* L = ls.as<double>(1);
         NR_CUDA(cudaMemsetAsync(L, 0, 8, st));
-        k_composite<<<grid_for(n_rays), 256, 0, st>>>(
+        k_composite<<<grid_for(n_rays * 32), 256, 0, st>>>(
             static_cast<const uint32_t*>(o.p), static_cast<const uint32_t*>(c.p), n_rays, static_cast<const float*>(rw.p),
             1, static_cast<const float*>(rg.p), static_cast<const float*>(tg.p), make_float3(bg[0], bg[1], bg[2]), dt,
             float(1.0 / (3.0 * double(n_rays))), co.as<float>(size_t(n_rays) * 3), dr.as<float>(size_t(ns) * 3),
