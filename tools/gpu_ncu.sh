@@ -11,3 +11,6 @@ for K in k_train k_adam k_infer; do
       python bench.py --steps 3 --warmup 3 --no-cpu-baseline --infer-b 4194304 > gpurun_out/prof_${K}_$TAG.log 2>&1
 done
 ls -la gpurun_out
+# NeRF (config 4) launch list: steps 21-40 of a 40-step run
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 400 -c 200 --csv \
+    --log-file gpurun_out/nerf_launches_$TAG.csv python tools/nerf_prof.py 40 > gpurun_out/nerf_prof_$TAG.log 2>&1

@@ -53,10 +53,7 @@ def launches(path):
         for r in csv.DictReader(lines):
             if r.get("Metric Name") == "gpu__time_duration.sum":
                 name = r["Kernel Name"].split("(")[0].replace("void ", "")
-                for short in ("k_train", "k_adam_check", "k_adam", "k_infer", "k_validate", "k_shadow"):
-                    if short in name:
-                        name = short if "ILi" not in name else f"{short}<{name.split('ILi', 1)[1].split('E', 1)[0]}...>"
-                        break
+                name = name.replace("nfg::", "").replace("<unnamed>::", "")
                 per[name].append(float(r["Metric Value"]) / 1000.0)
     return {k: {"launches": len(v), "mean_us": sum(v) / len(v)} for k, v in per.items()}
 
@@ -74,6 +71,9 @@ def main():
     lp = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
     if os.path.exists(lp):
         out["launch_list_us"] = launches(lp)
+    np_ = os.path.join(ROOT, "gpurun_out", f"nerf_launches_{tag}.csv")
+    if os.path.exists(np_):
+        out["nerf_launch_list_us"] = launches(np_)
     dst = os.path.join(ROOT, "profiles", f"ncu_{tag}.json")
     with open(dst, "w") as f:
         json.dump(out, f, indent=1)
