@@ -139,3 +139,24 @@ def test_fit_image_rejects_tiny_image():   # tasks.cpp:52-53
     t = _task(nf, 1, 5)
     with pytest.raises(ValueError, match="at least 2x2"):
         nf.fit_image(t, 1)
+
+
+def test_fit_image_zero_steps_emits_only_initial_row():   # test_tasks.cpp:201-213
+    nf = _nf()
+    t = nf.ImageTask(image=O.make_test_image(16, 16), width=16, height=16,
+                     cfg=nf.HashEncodingConfig(levels=2, table_size=1 << 8, n_min=4, n_max=0), total_steps=0)
+    r = nf.fit_image(t, 7)
+    assert len(r.report.rows) == 1
+    assert r.report.rows[0].step == 0 and r.report.rows[0].metric > 0
+
+
+def test_fit_image_constant_image_50db():   # test_tasks.cpp:215-235
+    nf = _nf()
+    img = np.full((32 * 32, 3), 0.37, np.float32)
+    t = nf.ImageTask(image=img, width=32, height=32,
+                     cfg=nf.HashEncodingConfig(levels=4, table_size=1 << 10, n_min=4, n_max=16),
+                     batch_size=256, total_steps=500, log_interval=100)
+    r = nf.fit_image(t, 3)
+    assert r.report.rows[-1].metric >= 50.0, r.report.rows[-1]
+    assert r.report.rows[0].step == 0 and r.report.rows[-1].step == 500
+    assert [row.step for row in r.report.rows] == [0, 100, 200, 300, 400, 500]
