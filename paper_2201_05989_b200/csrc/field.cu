@@ -407,7 +407,7 @@ void det_encode_bwd(nfg_field* f, const float* X, int64_t B, const float* dY)
 struct Streamed {
     const unsigned int* ready = nullptr;
     unsigned int epoch = 0;
-    int64_t chunk = 0;
+    int64_t chunk0 = 0, chunk = 0;
 };
 
 void device_backward(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
@@ -446,6 +446,7 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
     a.validate = speculative ? 1 : 0;
     a.ready = sm.ready;
     a.epoch = sm.epoch;
+    a.chunk0 = sm.chunk0;
     a.chunk = sm.chunk;
     if (c->profile)
         c->prof_steps++;
@@ -954,15 +955,19 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
             // overlaps nothing.
             float* dX = static_cast<float*>(c->s0.get(size_t(B) * d * 4));
             float* dT = static_cast<float*>(c->s1.get(size_t(B) * no * 4));
-            const int64_t chunk = std::max<int64_t>(4096, (B + NFG_STREAM_CHUNKS - 1) / NFG_STREAM_CHUNKS);
-            const int64_t nchunks = (B + chunk - 1) / chunk;
+            // a small first chunk so the kernel's first tiles start early, then
+            // NFG_STREAM_CHUNKS - 1 equal chunks
+            const int64_t chunk0 = std::min<int64_t>(B, 4096);
+            const int64_t chunk = std::max<int64_t>(4096, (B - chunk0 + NFG_STREAM_CHUNKS - 2) / (NFG_STREAM_CHUNKS - 1));
+            const int64_t nchunks = 1 + (B - chunk0 + chunk - 1) / chunk;
             const unsigned int epoch = ++f->epoch;
             NFG_CUDA(cudaEventRecord(c->ev_order, c->stream));        // staging buffers free
             NFG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_order, 0));
             int64_t k = 0;
             auto enqueue_copies = [&] {
                 for (; k < nchunks; ++k) {
-                    const int64_t s0 = k * chunk, n = std::min(chunk, B - s0);
+                    const int64_t s0 = k == 0 ? 0 : chunk0 + (k - 1) * chunk;
+                    const int64_t n = std::min(k == 0 ? chunk0 : chunk, B - s0);
                     NFG_CUDA(cudaMemcpyAsync(dX + s0 * d, X + s0 * d, size_t(n) * d * 4, cudaMemcpyHostToDevice,
                                              c->copy_stream));
                     NFG_CUDA(cudaMemcpyAsync(dT + s0 * no, target + s0 * no, size_t(n) * no * 4,
@@ -971,7 +976,7 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
                         throw Fail{ NFG_ECUDA, "cuStreamWriteValue32 failed" };
                 }
             };
-            const Streamed streamed{ f->d_ready, epoch, chunk };
+            const Streamed streamed{ f->d_ready, epoch, chunk0, chunk };
             device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step, streamed);
             try {
                 enqueue_copies();

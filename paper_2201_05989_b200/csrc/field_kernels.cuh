@@ -259,7 +259,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     auto wait_ready = [&](int64_t tl) {
         if (a.ready && tid == 0) {
             const int64_t last = min(a.B, (tl + 1) * TS) - 1;
-            const unsigned int* f = a.ready + last / a.chunk;
+            const unsigned int* f = a.ready + (last < a.chunk0 ? 0 : 1 + (last - a.chunk0) / a.chunk);
             unsigned int v;
             for (;;) {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");

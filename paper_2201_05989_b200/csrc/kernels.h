@@ -51,12 +51,14 @@ struct TrainArgs {
     float* pred;             // optional n_out x B
     StepScratch scratch;
     unsigned long long* phase_clk;   // NFG_PHASE_TIMING builds only
-    // Streamed inputs (host-pointer train_step): tile t may start once
-    // ready[(last sample of t) / chunk] >= epoch (written by the copy stream
-    // after the chunk's H2D). ready == nullptr: inputs already resident.
+    // Streamed inputs (host-pointer train_step): tile t may start once the
+    // flag of the chunk holding its last sample s is >= epoch (written by the
+    // copy stream after the chunk's H2D); chunk of s = s < chunk0 ? 0 :
+    // 1 + (s - chunk0) / chunk. ready == nullptr: inputs already resident.
     const unsigned int* ready;
     unsigned int epoch;
-    int64_t chunk;
+    int64_t chunk0;   // samples in the first (small) chunk
+    int64_t chunk;    // samples in each later chunk
     // 1: check the inputs inside the kernel (grid.hpp:226-229) and flag an
     // invalid batch (flags[3], abort flags[1]); Adam's check kernel then
     // restores the (clean) gradient slab, so no state changes.
