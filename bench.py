@@ -442,8 +442,9 @@ def main():
                 "inference": {"value": qps, "unit": "queries/s", "queries": Bq * world,
                               "ms_per_call": t_inf},
                 "nerf": nerf_line,
-                "phases_ms_per_step": {"train_kernel": phase_ms[0], "adam": phase_ms[1],
-                                       "allreduce": phase_ms[2]},
+                "phases_ms_per_step": ({"train_kernel": phase_ms[0], "adam": phase_ms[1]} if world == 1 else
+                                       {"train_kernel": phase_ms[0],
+                                        "allreduce_pipelined_with_adam": phase_ms[2]}),
                 "roofline": roof, "roofline_adam": roof_adam,
                 "secondary_rates": {"adam_gbs": adam_gbs, "train_l2_gbs": train_l2_gbs,
                                     "train_mlp_tflops": train_tflops},

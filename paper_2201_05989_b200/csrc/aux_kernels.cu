@@ -249,8 +249,11 @@ __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
 {
     if (a.flags[1] != 0u)
         return;   // non-finite gradient: state untouched (the reference throws first)
-    const uint64_t n = a.n_tab + a.n_w + a.n_b;
+    if ((a.mode == 1 && a.flags[0] != 0u) || (a.mode == 2 && a.flags[0] == 0u))
+        return;   // pipelined chunks vs the checked fallback: exactly one of them updates
+    const uint64_t n = a.mode == 1 ? a.hi : a.n_tab + a.n_w + a.n_b;
     const uint64_t n4 = n / 4;
+    const uint64_t q0 = a.mode == 1 ? a.lo / 4 : 0;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     // L2 policy: p, m, v stream through once per step (evict-first); the zeroed
     // gradients and the fp16 table shadow are what the next step's fused kernel
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
     uint64_t pol_stream, pol_keep;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
-    for (uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride) {
+    for (uint64_t q = q0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride) {
         const uint64_t i0 = 4 * q;
         float4 G, P, M, V;
         bool any;
@@ -319,6 +322,27 @@ __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
         }
         a.g[i] = 0.0f;
     }
+}
+
+cudaError_t launch_adam_range(const AdamArgs& a, int num_sms, cudaStream_t st)
+{
+    const uint64_t quads = (a.hi - a.lo + 3) / 4;
+    const int blocks = int(std::max<uint64_t>(1, std::min<uint64_t>((quads + 255) / 256, uint64_t(num_sms) * 8)));
+    AdamArgs r = a;
+    r.mode = 1;
+    k_adam<<<blocks, 256, 0, st>>>(r);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adam_fallback(const AdamArgs& a, int num_sms, cudaStream_t st)
+{
+    const uint64_t n = a.n_tab + a.n_w + a.n_b;
+    const int blocks = int(std::min<uint64_t>((n / 4 + 255) / 256 + 1, uint64_t(num_sms) * 8));
+    AdamArgs r = a;
+    r.mode = 2;
+    k_adam_check<<<num_sms * 4, 256, 0, st>>>(r, 0);
+    k_adam<<<blocks, 256, 0, st>>>(r);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_adam(const AdamArgs& a, bool force_check, int num_sms, cudaStream_t st)

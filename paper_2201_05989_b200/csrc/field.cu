@@ -142,6 +142,11 @@ struct nfg_ctx {
     // stream memory write of its ready flag (copy engine + front end only)
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_order = nullptr;
+    // data parallelism: NCCL runs the gradient all-reduce in chunks on its own
+    // stream while Adam updates the chunks already reduced
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_grads = nullptr;
+    cudaEvent_t ev_chunk[8] = {};
     CUresult (*write_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
     // phase timing (nfg_ctx_set_profiling)
     bool profile = false;
@@ -323,11 +328,11 @@ T* stage(DevBuf& b, const T* host, size_t count, cudaStream_t st)
     return d;
 }
 
-void run_adam(nfg_field* f, float lr_now, bool force_check)
+nfg::AdamArgs adam_args(nfg_field* f, float lr_now)
 {
     const uint64_t next = f->step + 1;
     const nfg::host::AdamScalars s = nfg::host::adam_scalars(f->hyper, next, lr_now);
-    nfg::AdamArgs a;
+    nfg::AdamArgs a{};
     a.p = f->d_p;
     a.g = f->d_g;
     a.m = f->d_m;
@@ -359,6 +364,14 @@ void run_adam(nfg_field* f, float lr_now, bool force_check)
         const bool dense = (double(f->last_batch) * double(1u << f->gcfg.dims)) >= double(f->gcfg.table_size);
         a.eager = forced >= 0 ? forced : (dense ? 1 : 0);
     }
+    a.mode = 0;
+    return a;
+}
+
+void run_adam(nfg_field* f, float lr_now, bool force_check)
+{
+    const nfg::AdamArgs a = adam_args(f, lr_now);
+    const uint64_t next = f->step + 1;
     NFG_CUDA(nfg::launch_adam(a, force_check, f->ctx->num_sms, f->ctx->stream));
     f->ctx->launches += 2;
     f->step = next;
@@ -410,8 +423,22 @@ struct Streamed {
     int64_t chunk0 = 0, chunk = 0;
 };
 
+// Cross-rank reduction of the step scratch: loss sums (sum), the
+// maybe-non-finite and abort flags (max), the first bad group + 1 (min) and the
+// invalid-input flag (max), so every rank takes the same decision.
+void reduce_scratch(nfg_field* f, cudaStream_t st)
+{
+    nfg_ctx* c = f->ctx;
+    const NcclApi& n = nccl();
+    NFG_NCCL(n.all_reduce(&f->d_res->loss_sum, &f->d_res->loss_sum, 1, ncclFloat64, ncclSum, c->comm, st));
+    NFG_NCCL(n.all_reduce(f->d_res->flags, f->d_res->flags, 2, ncclUint32, ncclMax, c->comm, st));
+    NFG_NCCL(n.all_reduce(f->d_res->flags + 2, f->d_res->flags + 2, 1, ncclUint32, ncclMin, c->comm, st));
+    NFG_NCCL(n.all_reduce(f->d_res->flags + 3, f->d_res->flags + 3, 1, ncclUint32, ncclMax, c->comm, st));
+}
+
 void device_backward(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
-                     int loss_kind, const Streamed& sm = Streamed(), bool allow_speculative = true)
+                     int loss_kind, const Streamed& sm = Streamed(), bool allow_speculative = true,
+                     bool reduce_grads = true)
 {
     require(loss_kind >= 0 && loss_kind <= 2, "train_step: unknown loss");
     require(B_local >= 0 && B_global >= B_local, "train_step: invalid batch size");
@@ -486,24 +513,58 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
             c->launches += 3;
         }
     }
-    if (c->comm && c->nranks > 1) {
+    if (c->comm && reduce_grads) {
         Span span(c, 2);
         // Data-parallel exchange: sum of the shards' (globally normalised)
         // gradients == the single-GPU gradient of the global batch; loss sums
-        // and the non-finite flag travel with it.
+        // and the flags travel with it.
         NFG_NCCL(nccl().all_reduce(f->d_g, f->d_g, f->n_total_dev, ncclFloat32, ncclSum, c->comm, c->stream));
-        NFG_NCCL(nccl().all_reduce(&f->d_res->loss_sum, &f->d_res->loss_sum, 1, ncclFloat64, ncclSum, c->comm, c->stream));
-        NFG_NCCL(nccl().all_reduce(f->d_res->flags, f->d_res->flags, 1, ncclUint32, ncclMax, c->comm, c->stream));
+        reduce_scratch(f, c->stream);
     }
 }
 
 void device_train_step(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
                        int loss_kind, int64_t step, const Streamed& sm = Streamed())
 {
-    device_backward(f, X, target, B_local, B_global, loss_kind, sm);
+    nfg_ctx* c = f->ctx;
+    const bool dp = c->comm != nullptr;
+    device_backward(f, X, target, B_local, B_global, loss_kind, sm, true, /*reduce_grads=*/!dp);
     const float lr_now = float(nfg::host::lr_at(f->milestones, f->factor, f->hyper.lr, step));
-    Span span(f->ctx, 1);
-    run_adam(f, lr_now, false);
+    if (!dp) {
+        Span span(c, 1);
+        run_adam(f, lr_now, false);
+        return;
+    }
+    // Data parallel: the gradient slab is all-reduced in chunks on the comm
+    // stream while Adam updates every chunk as soon as it is reduced (comm and
+    // the HBM-bound Adam overlap). The scratch (loss, flags) is reduced first,
+    // so a possibly non-finite gradient anywhere (flags[0]) makes every chunk
+    // kernel stand down and the checked full pass run instead: the reference's
+    // "throw before any update" (adam.hpp:86-90) holds across ranks.
+    Span span(c, 2);
+    reduce_scratch(f, c->stream);
+    nfg::AdamArgs a = adam_args(f, lr_now);
+    NFG_CUDA(cudaEventRecord(c->ev_grads, c->stream));
+    NFG_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_grads, 0));
+    const uint64_t n = f->n_total_dev;
+    const uint64_t kmax = sizeof(c->ev_chunk) / sizeof(c->ev_chunk[0]);
+    const uint64_t nk = std::max<uint64_t>(1, std::min<uint64_t>(kmax, (n + (uint64_t(1) << 20) - 1) >> 20));
+    const uint64_t chunk = ((n + nk - 1) / nk + 63) & ~uint64_t(63);   // 4 MB+ pieces, 256-byte aligned
+    for (uint64_t k = 0; k < nk; ++k) {
+        const uint64_t lo = k * chunk, hi = std::min(n, lo + chunk);
+        if (lo >= hi)
+            break;
+        NFG_NCCL(nccl().all_reduce(f->d_g + lo, f->d_g + lo, hi - lo, ncclFloat32, ncclSum, c->comm, c->comm_stream));
+        NFG_CUDA(cudaEventRecord(c->ev_chunk[k], c->comm_stream));
+        NFG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_chunk[k], 0));
+        a.lo = lo;
+        a.hi = hi;
+        NFG_CUDA(nfg::launch_adam_range(a, c->num_sms, c->stream));
+        c->launches++;
+    }
+    NFG_CUDA(nfg::launch_adam_fallback(a, c->num_sms, c->stream));
+    c->launches += 2;
+    f->step += 1;
 }
 
 nfg::FieldShape make_shape(const nfg_grid_config& g, const nfg_mlp_config& m, const std::vector<nfg_level_spec>& lv, const std::vector<uint64_t>& dev_off,
@@ -643,6 +704,13 @@ nfg_status nfg_ctx_destroy(nfg_ctx* c)
             cudaStreamDestroy(c->copy_stream);
         if (c->ev_order)
             cudaEventDestroy(c->ev_order);
+        if (c->comm_stream)
+            cudaStreamDestroy(c->comm_stream);
+        if (c->ev_grads)
+            cudaEventDestroy(c->ev_grads);
+        for (auto e : c->ev_chunk)
+            if (e)
+                cudaEventDestroy(e);
         delete c;
     });
 }
@@ -699,6 +767,12 @@ nfg_status nfg_ctx_attach_comm(nfg_ctx* c, const uint8_t id[128], int rank, int 
         NFG_NCCL(nccl().comm_init_rank(&c->comm, nranks, u, rank));
         c->rank = rank;
         c->nranks = nranks;
+        if (!c->comm_stream) {
+            NFG_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+            NFG_CUDA(cudaEventCreateWithFlags(&c->ev_grads, cudaEventDisableTiming));
+            for (auto& e : c->ev_chunk)
+                NFG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
     });
 }
 

@@ -104,7 +104,15 @@ struct AdamArgs {
     unsigned int* flags;
     int restore_on_invalid;   // zero the gradient slab if flags[3] (speculative step)
     int eager;                // 1: load p/m/v with g (dense steps), 0: only for non-zero gradient quads
+    // Pipelined data-parallel Adam (field.cu): mode 0 updates [0, n) after
+    // k_adam_check; mode 1 updates [lo, hi) (lo a multiple of 4) as soon as that
+    // chunk is all-reduced, unless a producer flagged a possibly non-finite
+    // gradient (flags[0]); mode 2 is the fallback full pass that runs only then.
+    int mode;
+    uint64_t lo, hi;
 };
+cudaError_t launch_adam_range(const AdamArgs& a, int num_sms, cudaStream_t st);
+cudaError_t launch_adam_fallback(const AdamArgs& a, int num_sms, cudaStream_t st);
 cudaError_t launch_adam(const AdamArgs& a, bool force_check, int num_sms, cudaStream_t st);
 cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cudaStream_t st);
 cudaError_t launch_shadow(const float* p, __half* shadow, uint64_t n, cudaStream_t st);

@@ -1,0 +1,64 @@
+"""Data-parallel path on one GPU through a 1-rank NCCL communicator: the
+chunked all-reduce on the comm stream + per-chunk Adam (and the scratch
+reduction) must take exactly the steps of the single-process path
+(deterministic mode: bit-identical parameters), and abort the same way."""
+import numpy as np
+import pytest
+
+import oracle as O
+from test_gpu_parity import _nf
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(nf, det):
+    import torch  # noqa: F401  (loads torch's libnccl for the communicator)
+    plain = nf.Context(0)
+    dp = nf.Context(0)
+    dp.attach_comm(nf.Context.unique_id(), 0, 1)
+    models = []
+    for ctx in (plain, dp):
+        m = nf.FieldModel(ctx, options=nf.Options(deterministic=det))
+        m.hash_cfg = nf.HashEncodingConfig(dims=3, levels=16, table_size=1 << 19, features=2, n_min=16, n_max=2048)
+        m.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=1)
+        m.hyper = nf.AdamHyper(lr=1e-3)
+        m.init(11)
+        models.append(m)
+    return models, (plain, dp)
+
+
+def test_chunked_allreduce_adam_matches_single_process():
+    nf = _nf()
+    (a, b), ctxs = _pair(nf, det=True)
+    rng = O.Pcg32(3, 3)
+    for step in range(1, 4):
+        X = rng.floats(20000 * 3).reshape(-1, 3)
+        T = O.csg_sdf(X).reshape(-1, 1)
+        la = a.train_step(X, T, nf.LossKind.Mape, step)
+        lb = b.train_step(X, T, nf.LossKind.Mape, step)
+        assert la == lb
+    assert a.adam_state()[0] == b.adam_state()[0] == 3
+    for x, y in ((a.params, b.params), (a.adam_state()[1], b.adam_state()[1]), (a.adam_state()[2], b.adam_state()[2])):
+        assert np.array_equal(np.asarray(x).view(np.uint32), np.asarray(y).view(np.uint32))
+    assert not b.grads.any()   # Adam zeroed every gradient chunk
+
+
+def test_dp_fused_path_and_invalid_input():
+    nf = _nf()
+    (a, b), ctxs = _pair(nf, det=False)
+    rng = O.Pcg32(4, 4)
+    X = rng.floats(3 * (1 << 16)).reshape(-1, 3)
+    T = O.csg_sdf(X).reshape(-1, 1)
+    la = a.train_step(X, T, nf.LossKind.Mape, 1)
+    lb = b.train_step(X, T, nf.LossKind.Mape, 1)
+    assert abs(la - lb) <= 1e-5 * abs(la)
+    d = np.abs(a.params - b.params)
+    assert np.mean(d > 1e-6) < 0.01
+    before = b.params
+    bad = X.copy()
+    bad[7, 1] = 1.5
+    with pytest.raises(ValueError):
+        b.train_step(bad, T, nf.LossKind.Mape, 2)
+    assert np.array_equal(b.params, before) and b.adam_state()[0] == 1 and not b.grads.any()
+    lb2 = b.train_step(X, T, nf.LossKind.Mape, 2)
+    assert np.isfinite(lb2)
