@@ -875,6 +875,8 @@ nfg_status nfg_field_create(nfg_ctx* ctx, const nfg_grid_config* grid, const nfg
             for (float* p : { f->d_p, f->d_g, f->d_m, f->d_v })
                 NFG_CUDA(cudaMemsetAsync(p, 0, bytes, ctx->stream));
             NFG_CUDA(cudaMemsetAsync(f->d_shadow, 0, std::max<uint64_t>(f->n_tab_dev, 1) * sizeof(__half), ctx->stream));
+            reset_scratch(f);   // a check before the first step must read a clean status
+            std::memset(f->h_res, 0, sizeof(StepResult));
             NFG_CUDA(cudaStreamSynchronize(ctx->stream));
         } catch (...) {
             nfg_field_destroy(f);
