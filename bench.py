@@ -172,18 +172,20 @@ def bench_nerf(nf, ctx, steps, warmup, W=128, views=16, samples=1 << 18):
         nerf.train_step(s)
     ctx.synchronize()
     t0 = time.perf_counter()
-    tot_s = tot_r = 0
+    tot_s = tot_r = tot_b = 0
     loss = 0.0
     for s in range(warmup + 1, warmup + steps + 1):
         loss, nr, ns = nerf.train_step(s)
         tot_s += ns
         tot_r += nr
+        tot_b += nerf.last_backward_samples
     ctx.synchronize()
     dt = time.perf_counter() - t0
     nerf.close()
     return {"metric": "NeRF training samples/s (config 4, synthetic scene)", "value": tot_s / dt, "unit": "samples/s",
             "rays_per_s": tot_r / dt, "ms_per_step": 1000.0 * dt / steps, "samples_per_step": tot_s / steps,
-            "rays_per_step": tot_r / steps, "steps": steps, "warmup": warmup, "loss": loss,
+            "rays_per_step": tot_r / steps, "backward_samples_per_step": tot_b / steps, "steps": steps,
+            "warmup": warmup, "loss": loss,
             "config": f"{views} views {W}x{W}, hash L16 F2 T2^19 Nmin16 Nmax2048, occupancy 128^3, "
                       f"dt sqrt(3)/1024, target 2^18 samples/step; timed on the host clock (one sync per step)"}
 

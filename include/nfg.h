@@ -352,6 +352,10 @@ nfg_status nfg_nerf_fields(nfg_nerf* n, nfg_field** density, nfg_field** color);
 nfg_status nfg_nerf_set_dataset(nfg_nerf* n, int32_t n_views, int32_t width, int32_t height, float focal,
                                 const float* cams, const float* rgb);
 nfg_status nfg_nerf_train_step(nfg_nerf* n, int64_t step, float* loss, int64_t* rays_used, int64_t* samples_used);
+/* ... also reporting how many samples reached the backward networks (those
+ * before their ray's transmittance stop, compacted into dense buffers). */
+nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t* rays_used, int64_t* samples_used,
+                                int64_t* samples_backward);
 nfg_status nfg_nerf_update_occupancy(nfg_nerf* n, int64_t step);
 nfg_status nfg_nerf_render(nfg_nerf* n, const float* cam12, int32_t width, int32_t height, float focal, float* rgb);
 nfg_status nfg_nerf_occupancy(nfg_nerf* n, uint8_t* bits, float* density);   /* 128^3/8 bytes, 128^3 floats */

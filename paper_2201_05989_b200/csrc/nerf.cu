@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <memory>
 #include <stdexcept>
@@ -90,16 +91,18 @@ struct Buf {
     void* get(size_t n)
     {
         n = std::max<size_t>(n, 16);
-        if (n > bytes) {
+        if (n > bytes) {   // grow by 1.5x: the per-ray buffers follow an adaptive ray count
             if (p)
                 cudaFree(p);
             p = nullptr;
             bytes = 0;
-            NR_CUDA(cudaMalloc(&p, n));
-            bytes = n;
+            const size_t want = bytes_hint(n);
+            NR_CUDA(cudaMalloc(&p, want));
+            bytes = want;
         }
         return p;
     }
+    static size_t bytes_hint(size_t n) { return n + n / 2; }
     template <class T>
     T* as(size_t count)
     {
@@ -381,7 +384,7 @@ __global__ void k_composite(const uint32_t* __restrict__ offsets, const uint32_t
                             const float* __restrict__ raw, int raw_stride, const float* __restrict__ rgb,
                             const float* __restrict__ target, float3 bg, float dt, float inv_count,
                             float* __restrict__ out_color, float* __restrict__ d_rgb, float* __restrict__ d_raw,
-                            double* loss_sum)
+                            double* loss_sum, uint32_t* __restrict__ used_counts = nullptr)
 {
     const int lane = threadIdx.x & 31;
     const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -391,6 +394,7 @@ __global__ void k_composite(const uint32_t* __restrict__ offsets, const uint32_t
         const uint32_t base = offsets[r], n = counts[r];
         // forward
         float logT = 0.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
+        uint32_t n_used = 0;
         for (uint32_t c0 = 0; c0 < n && __expf(logT) >= 1e-4f; c0 += 32) {
             const uint32_t i = c0 + lane;
             float x = 0.0f, r0 = 0.0f, r1 = 0.0f, r2 = 0.0f;
@@ -411,12 +415,15 @@ __global__ void k_composite(const uint32_t* __restrict__ offsets, const uint32_t
             const bool used = i < n && Ti >= 1e-4f;
             const unsigned um = __ballot_sync(0xffffffffu, used);
             const int last = um ? 31 - __clz(um) : -1;
+            n_used += uint32_t(__popc(um));
             const float incl_last = last >= 0 ? __shfl_sync(0xffffffffu, incl, last) : 0.0f;
             logT -= incl_last;
             if (um != 0xffffffffu)
                 break;   // a sample of this chunk crossed the stop (or the ray ended)
         }
         const float Tend = expf(logT);
+        if (used_counts && lane == 0)
+            used_counts[r] = n_used;   // the used samples are the first n_used of the ray
         const float Cr = cr + Tend * bg.x, Cg = cg + Tend * bg.y, Cb = cb + Tend * bg.z;
         if (out_color && lane == 0) {
             out_color[3 * r] = Cr;
@@ -475,6 +482,37 @@ __global__ void k_composite(const uint32_t* __restrict__ offsets, const uint32_t
             lsum += __shfl_xor_sync(0xffffffffu, lsum, m);
         if (lane == 0)
             atomicAdd(loss_sum, lsum);
+    }
+}
+
+// Second compaction ("compaction of samples into dense buffers"):
+// only the samples before a ray's transmittance stop reach the backward
+// networks. One warp per ray copies its used prefix (position, color input
+// row, dL/dRGB, dL/draw) to the compacted buffers.
+__global__ void k_compact_used(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ used,
+                               const uint32_t* __restrict__ used_off, int64_t n_rays, const float* __restrict__ pos,
+                               const float* __restrict__ Yc, const float* __restrict__ d_rgb,
+                               const float* __restrict__ d_raw, float* __restrict__ pos_c, float* __restrict__ Yc_c,
+                               float* __restrict__ d_rgb_c, float* __restrict__ d_raw_c)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = wid; r < n_rays; r += nw) {
+        const uint32_t src0 = offsets[r], dst0 = used_off[r], n = used[r];
+        for (uint32_t i = lane; i < n; i += 32) {
+            const size_t a = size_t(src0) + i, b = size_t(dst0) + i;
+            for (int k = 0; k < 3; ++k) {
+                pos_c[3 * b + k] = pos[3 * a + k];
+                d_rgb_c[3 * b + k] = d_rgb[3 * a + k];
+            }
+            d_raw_c[b] = d_raw[a];
+            const float4* ys = reinterpret_cast<const float4*>(Yc + 32 * a);
+            float4* yd = reinterpret_cast<float4*>(Yc_c + 32 * b);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                yd[k] = ys[k];
+        }
     }
 }
 
@@ -673,13 +711,17 @@ struct nfg_nerf {
     int n_views = 0, w = 0, h = 0;
     float focal = 1.0f;
     int64_t n_rays = 1 << 13;   // adapted to the sample budget
+    double last_used_frac = 1.0;   // samples before the transmittance stop / marched (previous step)
+    uint32_t* h_used = nullptr;    // pinned
     Buf occ_grid, occ_bits, cams, images;
     Buf rays, target, views, pixels, counts, offsets, fit, scan_tmp, pos, dirs, dens, Yc, rgb, color_out, d_rgb, d_raw,
-        dYc, d_dens, loss;
+        dYc, d_dens, loss, used, used_off, pos_c, Yc_c, d_rgb_c, d_raw_c;
     Buf occ_cells, occ_jit, occ_pos, occ_cell, occ_dens, occ_sum, occ_th;
 
     ~nfg_nerf()
     {
+        if (h_used)
+            cudaFreeHost(h_used);
         if (rng)
             nfg_rng_destroy(rng);
         if (density)
@@ -790,6 +832,24 @@ nfg_status nfg_nerf_create(nfg_ctx* ctx, const nfg_nerf_config* cfg, uint64_t se
         ok(nfg_field_create(ctx, &gc, &mc, &hy, &o, &n->color));
         ok(nfg_field_init(n->color, seed + 7));
         ok(nfg_rng_create(ctx, seed, 0xe7f, &n->rng));
+        NR_CUDA(cudaMallocHost(&n->h_used, sizeof(uint32_t)));
+        *n->h_used = 0;
+        // per-sample buffers sized for the budget once (no reallocation, which
+        // would synchronise, as the ray count adapts)
+        const size_t S = size_t(n->cfg.target_samples);
+        n->pos.get(S * 12);
+        n->dirs.get(S * 12);
+        n->dens.get(S * 64);
+        n->Yc.get(S * 128);
+        n->rgb.get(S * 12);
+        n->d_rgb.get(S * 12);
+        n->d_raw.get(S * 4);
+        n->dYc.get(S * 128);
+        n->d_dens.get(S * 64);
+        n->pos_c.get(S * 12);
+        n->Yc_c.get(S * 128);
+        n->d_rgb_c.get(S * 12);
+        n->d_raw_c.get(S * 4);
         // occupancy: all cells occupied until the first update
         n->occ_grid.get(size_t(OCC_CELLS) * 4);
         n->occ_bits.get(OCC_CELLS / 8);
@@ -835,6 +895,12 @@ nfg_status nfg_nerf_set_dataset(nfg_nerf* n, int32_t n_views, int32_t width, int
 
 nfg_status nfg_nerf_train_step(nfg_nerf* n, int64_t step, float* loss, int64_t* rays_used, int64_t* samples_used)
 {
+    return nfg_nerf_train_step2(n, step, loss, rays_used, samples_used, nullptr);
+}
+
+nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t* rays_used, int64_t* samples_used,
+                                int64_t* samples_backward)
+{
     return run([&] {
         if (n->n_views == 0)
             throw std::invalid_argument("nerf: no dataset");
@@ -869,24 +935,73 @@ nfg_status nfg_nerf_train_step(nfg_nerf* n, int64_t step, float* loss, int64_t* 
             float* drgb = n->d_rgb.as<float>(size_t(ns) * 3);
             float* draw = n->d_raw.as<float>(size_t(ns));
             const float3 bg = make_float3(n->cfg.background[0], n->cfg.background[1], n->cfg.background[2]);
+            uint32_t* used = n->used.as<uint32_t>(size_t(nr) + 1);
+            NR_CUDA(cudaMemsetAsync(used + nr, 0, 4, st));   // scan sentinel: uoff[nr] = total
             k_composite<<<grid_for(nr * 32), 256, 0, st>>>(static_cast<const uint32_t*>(n->offsets.p),
                                                       static_cast<const uint32_t*>(n->counts.p), nr,
                                                       static_cast<const float*>(n->dens.p), 16,
                                                       static_cast<const float*>(n->rgb.p), tgt, bg, SQRT3 / 1024.0f,
-                                                      float(1.0 / (3.0 * double(nr))), nullptr, drgb, draw, ls);
+                                                      float(1.0 / (3.0 * double(nr))), nullptr, drgb, draw, ls,
+                                                      used);
             NR_CUDA(cudaGetLastError());
-            float* dyc = n->dYc.as<float>(size_t(ns) * 32);
-            ok(nfg_mlp_backward_device(n->color, static_cast<const float*>(n->Yc.p), ns, drgb, dyc));
-            float* dd = n->d_dens.as<float>(size_t(ns) * 16);
-            k_density_grad<<<grid_for(ns), 256, 0, st>>>(dyc, draw, ns, dd);
-            NR_CUDA(cudaGetLastError());
-            ok(nfg_field_backward_device(n->density, static_cast<const float*>(n->pos.p), ns, dd));
+            // second compaction: the backward networks see only contributing samples
+            uint32_t* uoff = n->used_off.as<uint32_t>(size_t(nr) + 1);
+            size_t tb = 0;
+            NR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, used, uoff, nr + 1, st));
+            NR_CUDA(cub::DeviceScan::ExclusiveSum(n->scan_tmp.get(tb), tb, used, uoff, nr + 1, st));
+            // Compacting costs a mid-step sync (the launch sizes need the count):
+            // it is done when the previous step found >= 20% of the samples past
+            // their ray's transmittance stop (opaque scenes), else the backward
+            // runs on all samples (their gradients are zero).
+            const char* force = getenv("NFG_NERF_COMPACT");   // "1": always, "0": never (tests, A/B)
+            const bool compact = force ? force[0] == '1' : n->last_used_frac < 0.8;
+            int64_t nu = ns;
+            if (compact) {
+                uint32_t h_nu = 0;
+                NR_CUDA(cudaMemcpyAsync(&h_nu, uoff + nr, 4, cudaMemcpyDeviceToHost, st));
+                NR_CUDA(cudaStreamSynchronize(st));
+                nu = h_nu;
+            }
+            NR_CUDA(cudaMemcpyAsync(n->h_used, uoff + nr, 4, cudaMemcpyDeviceToHost, st));   // read at the end
+            const float* bpos = static_cast<const float*>(n->pos.p);
+            const float* bY = static_cast<const float*>(n->Yc.p);
+            const float* bdrgb = drgb;
+            const float* bdraw = draw;
+            if (compact && nu < ns) {
+                float* pc = n->pos_c.as<float>(size_t(std::max<int64_t>(nu, 1)) * 3);
+                float* yc = n->Yc_c.as<float>(size_t(std::max<int64_t>(nu, 1)) * 32);
+                float* dc = n->d_rgb_c.as<float>(size_t(std::max<int64_t>(nu, 1)) * 3);
+                float* wc = n->d_raw_c.as<float>(size_t(std::max<int64_t>(nu, 1)));
+                k_compact_used<<<grid_for(nr * 32), 256, 0, st>>>(static_cast<const uint32_t*>(n->offsets.p), used,
+                                                                  uoff, nr, bpos, bY, drgb, draw, pc, yc, dc, wc);
+                NR_CUDA(cudaGetLastError());
+                bpos = pc;
+                bY = yc;
+                bdrgb = dc;
+                bdraw = wc;
+            }
+
+            if (nu > 0) {
+                float* dyc = n->dYc.as<float>(size_t(nu) * 32);
+                ok(nfg_mlp_backward_device(n->color, bY, nu, bdrgb, dyc));
+                float* dd = n->d_dens.as<float>(size_t(nu) * 16);
+                k_density_grad<<<grid_for(nu), 256, 0, st>>>(dyc, bdraw, nu, dd);
+                NR_CUDA(cudaGetLastError());
+                ok(nfg_field_backward_device(n->density, bpos, nu, dd));
+            }
             ok(nfg_adam_step_device(n->color, float(n->cfg.lr)));
             ok(nfg_adam_step_device(n->density, float(n->cfg.lr)));
         }
         double h = 0.0;
         NR_CUDA(cudaMemcpyAsync(&h, ls, 8, cudaMemcpyDeviceToHost, st));
         NR_CUDA(cudaStreamSynchronize(st));
+        if (ns > 0) {
+            n->last_used_frac = double(*n->h_used) / double(ns);
+            if (samples_backward)
+                *samples_backward = int64_t(*n->h_used);
+        } else if (samples_backward) {
+            *samples_backward = 0;
+        }
         ok(nfg_field_check(n->color));
         ok(nfg_field_check(n->density));
         if (loss)

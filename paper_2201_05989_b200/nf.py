@@ -748,8 +748,11 @@ class NeRF:
         L.check(self.lib.nfg_nerf_set_dataset(self.h, cams.shape[0], width, height, focal, _ptr(cams), _ptr(rgb)))
 
     def train_step(self, step: int):
-        loss, nr, ns = C.c_float(), C.c_int64(), C.c_int64()
-        L.check(self.lib.nfg_nerf_train_step(self.h, step, C.byref(loss), C.byref(nr), C.byref(ns)))
+        """-> (loss, rays used, samples marched); ``last_backward_samples`` holds the
+        samples that reached the backward networks (before the transmittance stop)."""
+        loss, nr, ns, nb = C.c_float(), C.c_int64(), C.c_int64(), C.c_int64()
+        L.check(self.lib.nfg_nerf_train_step2(self.h, step, C.byref(loss), C.byref(nr), C.byref(ns), C.byref(nb)))
+        self.last_backward_samples = int(nb.value)
         return float(loss.value), int(nr.value), int(ns.value)
 
     def render(self, cam, width: int, height: int, focal: float) -> np.ndarray:

@@ -138,3 +138,22 @@ def test_field_backward_device_fused_matches_staged():   # nfg_field_backward_de
     a, b = grads
     assert np.array_equal(a != 0, b != 0)
     assert np.linalg.norm(a - b) <= 2e-2 * np.linalg.norm(b)
+
+
+def test_backward_compaction_path(monkeypatch):   # second compaction: only pre-stop samples reach the backward
+    nf = _nf()
+    W = H = 48
+    cams, focal = nf.orbit_cameras(8, width=W)
+    images = nf.nerf_scene_render(cams, W, H, focal)
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("NFG_NERF_COMPACT", mode)
+        nerf = nf.NeRF(grid=nf.HashEncodingConfig(levels=16, table_size=1 << 16, features=2, n_min=16, n_max=256,
+                                                  dims=3),
+                       lr=1e-2, target_samples=1 << 15, background=(0.0, 0.0, 0.0), seed=5)
+        nerf.set_dataset(cams, images, W, H, focal)
+        losses = [nerf.train_step(s)[0] for s in range(1, 151)]
+        res[mode] = (np.mean(losses[:5]), np.mean(losses[-10:]), nerf.last_backward_samples)
+    for first, last, nb in res.values():
+        assert last < 0.3 * first and nb > 0
+    assert abs(res["0"][1] - res["1"][1]) <= 0.5 * res["0"][1]
