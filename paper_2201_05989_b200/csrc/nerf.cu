@@ -38,84 +38,26 @@
 #include <vector>
 
 #include "../../include/nfg.h"
+#include "host_common.h"
 
-namespace nfg {
-void set_last_error(const std::string& msg);   // field.cu
-}
 
 namespace {
+
+using nfg::hc::Buf;
+using nfg::hc::Fail;
+using nfg::hc::grid_for;
+using nfg::hc::ok;
+using nfg::hc::run;
 
 constexpr int OCC_RES = 128;
 constexpr int OCC_CELLS = OCC_RES * OCC_RES * OCC_RES;
 constexpr float SQRT3 = 1.7320508075688772f;
 
-struct Fail {
-    nfg_status st;
-    std::string msg;
-};
 
-#define NR_CUDA(call)                                                                                   \
-    do {                                                                                                \
-        const cudaError_t e_ = (call);                                                                  \
-        if (e_ != cudaSuccess)                                                                          \
-            throw Fail{ NFG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_) };                \
-    } while (0)
 
-void ok(nfg_status st)
-{
-    if (st != NFG_OK)
-        throw Fail{ st, nfg_last_error() };
-}
 
-template <class Fn>
-nfg_status run(Fn&& fn)
-{
-    try {
-        fn();
-        return NFG_OK;
-    } catch (const Fail& f) {
-        nfg::set_last_error(f.msg);
-        return f.st;
-    } catch (const std::invalid_argument& e) {
-        nfg::set_last_error(e.what());
-        return NFG_EINVAL;
-    } catch (const std::exception& e) {
-        nfg::set_last_error(e.what());
-        return NFG_ECUDA;
-    }
-}
 
-struct Buf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    void* get(size_t n)
-    {
-        n = std::max<size_t>(n, 16);
-        if (n > bytes) {   // grow by 1.5x: the per-ray buffers follow an adaptive ray count
-            if (p)
-                cudaFree(p);
-            p = nullptr;
-            bytes = 0;
-            const size_t want = bytes_hint(n);
-            NR_CUDA(cudaMalloc(&p, want));
-            bytes = want;
-        }
-        return p;
-    }
-    static size_t bytes_hint(size_t n) { return n + n / 2; }
-    template <class T>
-    T* as(size_t count)
-    {
-        return static_cast<T*>(get(count * sizeof(T)));
-    }
-    ~Buf()
-    {
-        if (p)
-            cudaFree(p);
-    }
-};
 
-unsigned grid_for(int64_t n) { return unsigned(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16))); }
 
 // ---- occupancy grid: 128^3 bits in Morton order ---------
 __host__ __device__ inline uint32_t spread3(uint32_t v)   // 7 bits -> every third bit
@@ -737,22 +679,22 @@ struct nfg_nerf {
         uint32_t* off = offsets.as<uint32_t>(size_t(R));
         k_march_count<<<grid_for(R * 32), 256, 0, st>>>(ray_buf, R, static_cast<const uint8_t*>(occ_bits.p),
                                                    cfg.max_samples_per_ray, cnt);
-        NR_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaGetLastError());
         size_t tb = 0;
-        NR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, R, st));
-        NR_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp.get(tb), tb, cnt, off, R, st));
+        NFG_HC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, R, st));
+        NFG_HC_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp.get(tb), tb, cnt, off, R, st));
         int64_t* f = fit.as<int64_t>(2);
         k_fit_budget<<<1, 1, 0, st>>>(off, cnt, R, budget, f);
         int64_t h_fit[2] = { 0, 0 };
-        NR_CUDA(cudaMemcpyAsync(h_fit, f, sizeof(h_fit), cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaMemcpyAsync(h_fit, f, sizeof(h_fit), cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
         const int64_t ns = h_fit[1];
         float* P = pos.as<float>(size_t(std::max<int64_t>(ns, 1)) * 3);
         float* D = dirs.as<float>(size_t(std::max<int64_t>(ns, 1)) * 3);
         if (h_fit[0] > 0) {
             k_march_write<<<grid_for(h_fit[0] * 32), 256, 0, st>>>(ray_buf, h_fit[0], static_cast<const uint8_t*>(occ_bits.p),
                                                               cfg.max_samples_per_ray, off, P, D);
-            NR_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaGetLastError());
         }
         return { h_fit[0], ns };
     }
@@ -765,7 +707,7 @@ struct nfg_nerf {
         float* c = rgb.as<float>(size_t(ns) * 3);
         ok(nfg_field_evaluate_device(density, static_cast<const float*>(pos.p), ns, dn));
         k_color_input<<<grid_for(ns), 256, 0, st>>>(dn, static_cast<const float*>(dirs.p), ns, y);
-        NR_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaGetLastError());
         ok(nfg_mlp_forward_device(color, y, ns, c));
     }
 
@@ -791,7 +733,7 @@ struct nfg_nerf {
             float* dn = occ_dens.as<float>(size_t(k) * 16);
             ok(nfg_field_evaluate_device(density, p, k, dn));
             k_occ_max<<<grid_for(k), 256, 0, st>>>(grid, cl, dn, k);
-            NR_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaGetLastError());
         }
         constexpr int SUM_BLOCKS = 296;
         double* part = occ_sum.as<double>(SUM_BLOCKS);
@@ -799,7 +741,7 @@ struct nfg_nerf {
         k_occ_sum<<<SUM_BLOCKS, 256, 0, st>>>(grid, part);
         k_occ_thresh<<<1, 1, 0, st>>>(part, SUM_BLOCKS, 0.01f * 1024.0f / SQRT3, th);
         k_occ_bits<<<grid_for(OCC_CELLS / 8), 256, 0, st>>>(grid, static_cast<uint8_t*>(occ_bits.p), th);
-        NR_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaGetLastError());
     }
 };
 
@@ -832,7 +774,7 @@ nfg_status nfg_nerf_create(nfg_ctx* ctx, const nfg_nerf_config* cfg, uint64_t se
         ok(nfg_field_create(ctx, &gc, &mc, &hy, &o, &n->color));
         ok(nfg_field_init(n->color, seed + 7));
         ok(nfg_rng_create(ctx, seed, 0xe7f, &n->rng));
-        NR_CUDA(cudaMallocHost(&n->h_used, sizeof(uint32_t)));
+        NFG_HC_CUDA(cudaMallocHost(&n->h_used, sizeof(uint32_t)));
         *n->h_used = 0;
         // per-sample buffers sized for the budget once (no reallocation, which
         // would synchronise, as the ray count adapts)
@@ -853,9 +795,9 @@ nfg_status nfg_nerf_create(nfg_ctx* ctx, const nfg_nerf_config* cfg, uint64_t se
         // occupancy: all cells occupied until the first update
         n->occ_grid.get(size_t(OCC_CELLS) * 4);
         n->occ_bits.get(OCC_CELLS / 8);
-        NR_CUDA(cudaMemsetAsync(n->occ_grid.p, 0, size_t(OCC_CELLS) * 4, n->st));
-        NR_CUDA(cudaMemsetAsync(n->occ_bits.p, 0xff, OCC_CELLS / 8, n->st));
-        NR_CUDA(cudaStreamSynchronize(n->st));
+        NFG_HC_CUDA(cudaMemsetAsync(n->occ_grid.p, 0, size_t(OCC_CELLS) * 4, n->st));
+        NFG_HC_CUDA(cudaMemsetAsync(n->occ_bits.p, 0xff, OCC_CELLS / 8, n->st));
+        NFG_HC_CUDA(cudaStreamSynchronize(n->st));
         *out = n.release();
     });
 }
@@ -886,10 +828,10 @@ nfg_status nfg_nerf_set_dataset(nfg_nerf* n, int32_t n_views, int32_t width, int
         n->h = height;
         n->focal = focal;
         const size_t npx = size_t(n_views) * width * height;
-        NR_CUDA(cudaMemcpyAsync(n->cams.get(size_t(n_views) * 12 * 4), cams, size_t(n_views) * 12 * 4,
+        NFG_HC_CUDA(cudaMemcpyAsync(n->cams.get(size_t(n_views) * 12 * 4), cams, size_t(n_views) * 12 * 4,
                                 cudaMemcpyHostToDevice, n->st));
-        NR_CUDA(cudaMemcpyAsync(n->images.get(npx * 12), rgb, npx * 12, cudaMemcpyHostToDevice, n->st));
-        NR_CUDA(cudaStreamSynchronize(n->st));
+        NFG_HC_CUDA(cudaMemcpyAsync(n->images.get(npx * 12), rgb, npx * 12, cudaMemcpyHostToDevice, n->st));
+        NFG_HC_CUDA(cudaStreamSynchronize(n->st));
     });
 }
 
@@ -917,7 +859,7 @@ nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t*
         k_train_rays<<<grid_for(R), 256, 0, st>>>(vw, px, R, static_cast<const float*>(n->cams.p),
                                                   static_cast<const float*>(n->images.p), n->w, n->h, n->focal, rays,
                                                   tgt);
-        NR_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaGetLastError());
         const auto fit = n->march_compact(rays, R, n->cfg.target_samples);
         const int64_t nr = fit.first, ns = fit.second;
         // adapt the ray count to the sample budget (measured samples per ray)
@@ -929,26 +871,26 @@ nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t*
         if (samples_used)
             *samples_used = ns;
         double* ls = n->loss.as<double>(1);
-        NR_CUDA(cudaMemsetAsync(ls, 0, 8, st));
+        NFG_HC_CUDA(cudaMemsetAsync(ls, 0, 8, st));
         if (ns > 0) {
             n->forward(ns);
             float* drgb = n->d_rgb.as<float>(size_t(ns) * 3);
             float* draw = n->d_raw.as<float>(size_t(ns));
             const float3 bg = make_float3(n->cfg.background[0], n->cfg.background[1], n->cfg.background[2]);
             uint32_t* used = n->used.as<uint32_t>(size_t(nr) + 1);
-            NR_CUDA(cudaMemsetAsync(used + nr, 0, 4, st));   // scan sentinel: uoff[nr] = total
+            NFG_HC_CUDA(cudaMemsetAsync(used + nr, 0, 4, st));   // scan sentinel: uoff[nr] = total
             k_composite<<<grid_for(nr * 32), 256, 0, st>>>(static_cast<const uint32_t*>(n->offsets.p),
                                                       static_cast<const uint32_t*>(n->counts.p), nr,
                                                       static_cast<const float*>(n->dens.p), 16,
                                                       static_cast<const float*>(n->rgb.p), tgt, bg, SQRT3 / 1024.0f,
                                                       float(1.0 / (3.0 * double(nr))), nullptr, drgb, draw, ls,
                                                       used);
-            NR_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaGetLastError());
             // second compaction: the backward networks see only contributing samples
             uint32_t* uoff = n->used_off.as<uint32_t>(size_t(nr) + 1);
             size_t tb = 0;
-            NR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, used, uoff, nr + 1, st));
-            NR_CUDA(cub::DeviceScan::ExclusiveSum(n->scan_tmp.get(tb), tb, used, uoff, nr + 1, st));
+            NFG_HC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, used, uoff, nr + 1, st));
+            NFG_HC_CUDA(cub::DeviceScan::ExclusiveSum(n->scan_tmp.get(tb), tb, used, uoff, nr + 1, st));
             // Compacting costs a mid-step sync (the launch sizes need the count):
             // it is done when the previous step found >= 20% of the samples past
             // their ray's transmittance stop (opaque scenes), else the backward
@@ -958,11 +900,11 @@ nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t*
             int64_t nu = ns;
             if (compact) {
                 uint32_t h_nu = 0;
-                NR_CUDA(cudaMemcpyAsync(&h_nu, uoff + nr, 4, cudaMemcpyDeviceToHost, st));
-                NR_CUDA(cudaStreamSynchronize(st));
+                NFG_HC_CUDA(cudaMemcpyAsync(&h_nu, uoff + nr, 4, cudaMemcpyDeviceToHost, st));
+                NFG_HC_CUDA(cudaStreamSynchronize(st));
                 nu = h_nu;
             }
-            NR_CUDA(cudaMemcpyAsync(n->h_used, uoff + nr, 4, cudaMemcpyDeviceToHost, st));   // read at the end
+            NFG_HC_CUDA(cudaMemcpyAsync(n->h_used, uoff + nr, 4, cudaMemcpyDeviceToHost, st));   // read at the end
             const float* bpos = static_cast<const float*>(n->pos.p);
             const float* bY = static_cast<const float*>(n->Yc.p);
             const float* bdrgb = drgb;
@@ -974,7 +916,7 @@ nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t*
                 float* wc = n->d_raw_c.as<float>(size_t(std::max<int64_t>(nu, 1)));
                 k_compact_used<<<grid_for(nr * 32), 256, 0, st>>>(static_cast<const uint32_t*>(n->offsets.p), used,
                                                                   uoff, nr, bpos, bY, drgb, draw, pc, yc, dc, wc);
-                NR_CUDA(cudaGetLastError());
+                NFG_HC_CUDA(cudaGetLastError());
                 bpos = pc;
                 bY = yc;
                 bdrgb = dc;
@@ -986,15 +928,15 @@ nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t*
                 ok(nfg_mlp_backward_device(n->color, bY, nu, bdrgb, dyc));
                 float* dd = n->d_dens.as<float>(size_t(nu) * 16);
                 k_density_grad<<<grid_for(nu), 256, 0, st>>>(dyc, bdraw, nu, dd);
-                NR_CUDA(cudaGetLastError());
+                NFG_HC_CUDA(cudaGetLastError());
                 ok(nfg_field_backward_device(n->density, bpos, nu, dd));
             }
             ok(nfg_adam_step_device(n->color, float(n->cfg.lr)));
             ok(nfg_adam_step_device(n->density, float(n->cfg.lr)));
         }
         double h = 0.0;
-        NR_CUDA(cudaMemcpyAsync(&h, ls, 8, cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaMemcpyAsync(&h, ls, 8, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
         if (ns > 0) {
             n->last_used_frac = double(*n->h_used) / double(ns);
             if (samples_backward)
@@ -1013,7 +955,7 @@ nfg_status nfg_nerf_update_occupancy(nfg_nerf* n, int64_t step)
 {
     return run([&] {
         n->update_occupancy(step);
-        NR_CUDA(cudaStreamSynchronize(n->st));
+        NFG_HC_CUDA(cudaStreamSynchronize(n->st));
     });
 }
 
@@ -1024,10 +966,10 @@ nfg_status nfg_nerf_render(nfg_nerf* n, const float* cam12, int32_t width, int32
         cudaStream_t st = n->st;
         const int64_t R = int64_t(width) * height;
         Buf cam, rays, color;
-        NR_CUDA(cudaMemcpyAsync(cam.get(48), cam12, 48, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(cam.get(48), cam12, 48, cudaMemcpyHostToDevice, st));
         float* rb = rays.as<float>(size_t(R) * 6);
         k_view_rays<<<grid_for(R), 256, 0, st>>>(static_cast<const float*>(cam.p), width, height, focal, rb);
-        NR_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaGetLastError());
         const int64_t budget = int64_t(1) << 31;
         const auto fit = n->march_compact(rb, R, std::min<int64_t>(budget, R * int64_t(n->cfg.max_samples_per_ray)));
         float* out = color.as<float>(size_t(R) * 3);
@@ -1039,9 +981,9 @@ nfg_status nfg_nerf_render(nfg_nerf* n, const float* cam12, int32_t width, int32
                                                          static_cast<const float*>(n->dens.p), 16,
                                                          static_cast<const float*>(n->rgb.p), nullptr, bg,
                                                          SQRT3 / 1024.0f, 0.0f, out, nullptr, nullptr, nullptr);
-        NR_CUDA(cudaGetLastError());
-        NR_CUDA(cudaMemcpyAsync(rgb_host, out, size_t(R) * 12, cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaMemcpyAsync(rgb_host, out, size_t(R) * 12, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
         ok(nfg_field_check(n->density));
     });
 }
@@ -1050,18 +992,18 @@ nfg_status nfg_nerf_occupancy(nfg_nerf* n, uint8_t* bits_host, float* density_ho
 {
     return run([&] {
         if (bits_host)
-            NR_CUDA(cudaMemcpyAsync(bits_host, n->occ_bits.p, OCC_CELLS / 8, cudaMemcpyDeviceToHost, n->st));
+            NFG_HC_CUDA(cudaMemcpyAsync(bits_host, n->occ_bits.p, OCC_CELLS / 8, cudaMemcpyDeviceToHost, n->st));
         if (density_host)
-            NR_CUDA(cudaMemcpyAsync(density_host, n->occ_grid.p, size_t(OCC_CELLS) * 4, cudaMemcpyDeviceToHost, n->st));
-        NR_CUDA(cudaStreamSynchronize(n->st));
+            NFG_HC_CUDA(cudaMemcpyAsync(density_host, n->occ_grid.p, size_t(OCC_CELLS) * 4, cudaMemcpyDeviceToHost, n->st));
+        NFG_HC_CUDA(cudaStreamSynchronize(n->st));
     });
 }
 
 nfg_status nfg_nerf_set_occupancy(nfg_nerf* n, const uint8_t* bits_host)
 {
     return run([&] {
-        NR_CUDA(cudaMemcpyAsync(n->occ_bits.p, bits_host, OCC_CELLS / 8, cudaMemcpyHostToDevice, n->st));
-        NR_CUDA(cudaStreamSynchronize(n->st));
+        NFG_HC_CUDA(cudaMemcpyAsync(n->occ_bits.p, bits_host, OCC_CELLS / 8, cudaMemcpyHostToDevice, n->st));
+        NFG_HC_CUDA(cudaStreamSynchronize(n->st));
     });
 }
 
@@ -1072,19 +1014,19 @@ nfg_status nfg_nerf_march(nfg_ctx* ctx, const float* rays, int64_t n, const uint
     return run([&] {
         cudaStream_t st = static_cast<cudaStream_t>(nfg_ctx_stream(ctx));
         Buf r, b, c, o, t, P, D;
-        NR_CUDA(cudaMemcpyAsync(r.get(size_t(n) * 24), rays, size_t(n) * 24, cudaMemcpyHostToDevice, st));
-        NR_CUDA(cudaMemcpyAsync(b.get(OCC_CELLS / 8), bits, OCC_CELLS / 8, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(r.get(size_t(n) * 24), rays, size_t(n) * 24, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(b.get(OCC_CELLS / 8), bits, OCC_CELLS / 8, cudaMemcpyHostToDevice, st));
         uint32_t* cnt = c.as<uint32_t>(size_t(n));
         uint32_t* off = o.as<uint32_t>(size_t(n));
         k_march_count<<<grid_for(n * 32), 256, 0, st>>>(static_cast<const float*>(r.p), n,
                                                    static_cast<const uint8_t*>(b.p), max_steps, cnt);
         size_t tb = 0;
-        NR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, n, st));
-        NR_CUDA(cub::DeviceScan::ExclusiveSum(t.get(tb), tb, cnt, off, n, st));
+        NFG_HC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, n, st));
+        NFG_HC_CUDA(cub::DeviceScan::ExclusiveSum(t.get(tb), tb, cnt, off, n, st));
         std::vector<uint32_t> hc(static_cast<size_t>(n)), ho(static_cast<size_t>(n));
-        NR_CUDA(cudaMemcpyAsync(hc.data(), cnt, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaMemcpyAsync(ho.data(), off, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaMemcpyAsync(hc.data(), cnt, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(ho.data(), off, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
         const int64_t tot = n > 0 ? int64_t(ho[size_t(n) - 1]) + hc[size_t(n) - 1] : 0;
         *total = tot;
         std::copy(hc.begin(), hc.end(), counts);
@@ -1094,9 +1036,9 @@ nfg_status nfg_nerf_march(nfg_ctx* ctx, const float* rays, int64_t n, const uint
         float* dd = D.as<float>(size_t(std::max<int64_t>(tot, 1)) * 3);
         k_march_write<<<grid_for(n * 32), 256, 0, st>>>(static_cast<const float*>(r.p), n, static_cast<const uint8_t*>(b.p),
                                                    max_steps, off, pp, dd);
-        NR_CUDA(cudaGetLastError());
-        NR_CUDA(cudaMemcpyAsync(samples, pp, size_t(tot) * 12, cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaMemcpyAsync(samples, pp, size_t(tot) * 12, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
     });
 }
 
@@ -1113,24 +1055,24 @@ nfg_status nfg_nerf_composite(nfg_ctx* ctx, int64_t n_rays, const uint32_t* coun
             ns += counts[r];
         }
         Buf c, o, rw, rg, tg, co, dr, dw, ls;
-        NR_CUDA(cudaMemcpyAsync(c.get(size_t(n_rays) * 4), counts, size_t(n_rays) * 4, cudaMemcpyHostToDevice, st));
-        NR_CUDA(cudaMemcpyAsync(o.get(size_t(n_rays) * 4), off.data(), size_t(n_rays) * 4, cudaMemcpyHostToDevice, st));
-        NR_CUDA(cudaMemcpyAsync(rw.get(size_t(ns) * 4), raw, size_t(ns) * 4, cudaMemcpyHostToDevice, st));
-        NR_CUDA(cudaMemcpyAsync(rg.get(size_t(ns) * 12), rgb, size_t(ns) * 12, cudaMemcpyHostToDevice, st));
-        NR_CUDA(cudaMemcpyAsync(tg.get(size_t(n_rays) * 12), target, size_t(n_rays) * 12, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(c.get(size_t(n_rays) * 4), counts, size_t(n_rays) * 4, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(o.get(size_t(n_rays) * 4), off.data(), size_t(n_rays) * 4, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(rw.get(size_t(ns) * 4), raw, size_t(ns) * 4, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(rg.get(size_t(ns) * 12), rgb, size_t(ns) * 12, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(tg.get(size_t(n_rays) * 12), target, size_t(n_rays) * 12, cudaMemcpyHostToDevice, st));
         double* L = ls.as<double>(1);
-        NR_CUDA(cudaMemsetAsync(L, 0, 8, st));
+        NFG_HC_CUDA(cudaMemsetAsync(L, 0, 8, st));
         k_composite<<<grid_for(n_rays * 32), 256, 0, st>>>(
             static_cast<const uint32_t*>(o.p), static_cast<const uint32_t*>(c.p), n_rays, static_cast<const float*>(rw.p),
             1, static_cast<const float*>(rg.p), static_cast<const float*>(tg.p), make_float3(bg[0], bg[1], bg[2]), dt,
             float(1.0 / (3.0 * double(n_rays))), co.as<float>(size_t(n_rays) * 3), dr.as<float>(size_t(ns) * 3),
             dw.as<float>(size_t(ns)), L);
-        NR_CUDA(cudaGetLastError());
-        NR_CUDA(cudaMemcpyAsync(color, co.p, size_t(n_rays) * 12, cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaMemcpyAsync(d_rgb, dr.p, size_t(ns) * 12, cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaMemcpyAsync(d_raw, dw.p, size_t(ns) * 4, cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaMemcpyAsync(loss_sum, L, 8, cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaMemcpyAsync(color, co.p, size_t(n_rays) * 12, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(d_rgb, dr.p, size_t(ns) * 12, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(d_raw, dw.p, size_t(ns) * 4, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(loss_sum, L, 8, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
     });
 }
 
@@ -1139,14 +1081,14 @@ nfg_status nfg_nerf_sh4(nfg_ctx* ctx, const float* dirs, int64_t n, float* out)
     return run([&] {
         cudaStream_t st = static_cast<cudaStream_t>(nfg_ctx_stream(ctx));
         Buf d, z, y;
-        NR_CUDA(cudaMemcpyAsync(d.get(size_t(n) * 12), dirs, size_t(n) * 12, cudaMemcpyHostToDevice, st));
-        NR_CUDA(cudaMemsetAsync(z.get(size_t(n) * 64), 0, size_t(n) * 64, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(d.get(size_t(n) * 12), dirs, size_t(n) * 12, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemsetAsync(z.get(size_t(n) * 64), 0, size_t(n) * 64, st));
         float* Y = y.as<float>(size_t(n) * 32);
         k_color_input<<<grid_for(n), 256, 0, st>>>(static_cast<const float*>(z.p), static_cast<const float*>(d.p), n, Y);
-        NR_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaGetLastError());
         std::vector<float> h(static_cast<size_t>(n) * 32);
-        NR_CUDA(cudaMemcpyAsync(h.data(), Y, h.size() * 4, cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaMemcpyAsync(h.data(), Y, h.size() * 4, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
         for (int64_t i = 0; i < n; ++i)
             for (int k = 0; k < 16; ++k)
                 out[16 * i + k] = h[size_t(32 * i + 16 + k)];
@@ -1159,14 +1101,14 @@ nfg_status nfg_nerf_scene_render(nfg_ctx* ctx, const float* cams, int32_t n_view
     return run([&] {
         cudaStream_t st = static_cast<cudaStream_t>(nfg_ctx_stream(ctx));
         Buf c, o;
-        NR_CUDA(cudaMemcpyAsync(c.get(size_t(n_views) * 48), cams, size_t(n_views) * 48, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(c.get(size_t(n_views) * 48), cams, size_t(n_views) * 48, cudaMemcpyHostToDevice, st));
         const int64_t n = int64_t(n_views) * width * height;
         float* out = o.as<float>(size_t(n) * 3);
         k_scene_render<<<grid_for(n), 256, 0, st>>>(static_cast<const float*>(c.p), n_views, width, height, focal,
                                                     make_float3(bg[0], bg[1], bg[2]), out);
-        NR_CUDA(cudaGetLastError());
-        NR_CUDA(cudaMemcpyAsync(rgb, out, size_t(n) * 12, cudaMemcpyDeviceToHost, st));
-        NR_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaMemcpyAsync(rgb, out, size_t(n) * 12, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
     });
 }
 

@@ -24,73 +24,22 @@
 #include <vector>
 
 #include "../../include/nfg.h"
+#include "host_common.h"
 
-namespace nfg {
-void set_last_error(const std::string& msg);   // field.cu
-}
 
 namespace {
 
-struct Fail {
-    nfg_status st;
-    std::string msg;
-};
+using nfg::hc::Buf;
+using nfg::hc::Fail;
+using nfg::hc::grid_for;
+using nfg::hc::ok;
+using nfg::hc::run;
 
-#define RD_CUDA(call)                                                                                   \
-    do {                                                                                                \
-        const cudaError_t e_ = (call);                                                                  \
-        if (e_ != cudaSuccess)                                                                          \
-            throw Fail{ NFG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_) };                \
-    } while (0)
 
-void ok(nfg_status st)
-{
-    if (st != NFG_OK)
-        throw Fail{ st, nfg_last_error() };
-}
 
-template <class Fn>
-nfg_status run(Fn&& fn)
-{
-    try {
-        fn();
-        return NFG_OK;
-    } catch (const Fail& f) {
-        nfg::set_last_error(f.msg);
-        return f.st;
-    } catch (const std::invalid_argument& e) {
-        nfg::set_last_error(e.what());
-        return NFG_EINVAL;
-    } catch (const std::exception& e) {
-        nfg::set_last_error(e.what());
-        return NFG_ECUDA;
-    }
-}
 
-struct Buf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    void* get(size_t n)
-    {
-        n = std::max<size_t>(n, 16);
-        if (n > bytes) {
-            if (p)
-                cudaFree(p);
-            p = nullptr;
-            bytes = 0;
-            RD_CUDA(cudaMalloc(&p, n));
-            bytes = n;
-        }
-        return p;
-    }
-    ~Buf()
-    {
-        if (p)
-            cudaFree(p);
-    }
-};
 
-unsigned grid_for(int64_t n) { return unsigned(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16))); }
+
 
 struct Ray {
     double dir[3];
@@ -266,10 +215,10 @@ struct Evaluator {
         }
         hx.resize(size_t(n) * d);
         hv.resize(size_t(n));
-        RD_CUDA(cudaMemcpyAsync(hx.data(), X_dev, hx.size() * 4, cudaMemcpyDeviceToHost, st));
-        RD_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaMemcpyAsync(hx.data(), X_dev, hx.size() * 4, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
         fn(hx.data(), n, hv.data(), user);
-        RD_CUDA(cudaMemcpyAsync(out_dev, hv.data(), hv.size() * 4, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(out_dev, hv.data(), hv.size() * 4, cudaMemcpyHostToDevice, st));
     }
 };
 
@@ -309,10 +258,10 @@ nfg_status nfg_render_image(nfg_field* f, int32_t width, int32_t height, float* 
         float* x = static_cast<float*>(X.get(size_t(n) * 8));
         float* o = static_cast<float*>(out.get(size_t(n) * m.output_width * 4));
         k_pixel_grid<<<grid_for(n), 256, 0, st>>>(width, height, x);
-        RD_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaGetLastError());
         ok(nfg_field_evaluate_device(f, x, n, o));
-        RD_CUDA(cudaMemcpyAsync(rgb_host, o, size_t(n) * m.output_width * 4, cudaMemcpyDeviceToHost, st));
-        RD_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaMemcpyAsync(rgb_host, o, size_t(n) * m.output_width * 4, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
     });
 }
 
@@ -359,35 +308,35 @@ nfg_status nfg_render_sdf_shaded(nfg_ctx* ctx, nfg_field* field, nfg_field_fn fn
         Evaluator ev{ field, fn, user, st, {}, {} };
 
         k_fill<<<grid_for(npix * 3), 256, 0, st>>>(rgb, npix * 3, 1.0f);   // background
-        RD_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned int), st));
+        NFG_HC_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned int), st));
         k_rays_init<<<grid_for(npix), 256, 0, st>>>(b, width, height, cur, cnt);
-        RD_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaGetLastError());
         unsigned int h_cnt[4] = { 0, 0, 0, 0 };
-        RD_CUDA(cudaMemcpyAsync(h_cnt, cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
-        RD_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaMemcpyAsync(h_cnt, cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
         int64_t active = h_cnt[0];
         for (int iter = 0; iter < kMaxSteps && active > 0; ++iter) {
             k_ray_points<<<grid_for(active), 256, 0, st>>>(b, cur, active, x);
-            RD_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaGetLastError());
             ev.eval(x, active, 3, v);
-            RD_CUDA(cudaMemsetAsync(cnt + 1, 0, sizeof(unsigned int), st));
+            NFG_HC_CUDA(cudaMemsetAsync(cnt + 1, 0, sizeof(unsigned int), st));
             k_ray_step<<<grid_for(active), 256, 0, st>>>(cur, active, v, nxt, cnt + 1, hits, cnt + 2);
-            RD_CUDA(cudaGetLastError());
-            RD_CUDA(cudaMemcpyAsync(h_cnt, cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
-            RD_CUDA(cudaStreamSynchronize(st));
+            NFG_HC_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaMemcpyAsync(h_cnt, cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
+            NFG_HC_CUDA(cudaStreamSynchronize(st));
             active = h_cnt[1];
             std::swap(cur, nxt);
         }
         const int64_t nh = h_cnt[2];
         if (nh > 0) {
             k_probe_points<<<grid_for(nh), 256, 0, st>>>(b, hits, nh, x);
-            RD_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaGetLastError());
             ev.eval(x, nh * 6, 3, v);
             k_shade<<<grid_for(nh), 256, 0, st>>>(hits, nh, v, rgb);
-            RD_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaGetLastError());
         }
-        RD_CUDA(cudaMemcpyAsync(rgb_host, rgb, size_t(npix) * 3 * 4, cudaMemcpyDeviceToHost, st));
-        RD_CUDA(cudaStreamSynchronize(st));
+        NFG_HC_CUDA(cudaMemcpyAsync(rgb_host, rgb, size_t(npix) * 3 * 4, cudaMemcpyDeviceToHost, st));
+        NFG_HC_CUDA(cudaStreamSynchronize(st));
     });
 }
 
@@ -413,11 +362,11 @@ nfg_status nfg_iou(nfg_ctx* ctx, nfg_field* field, nfg_field_fn fn, void* user, 
             ok(nfg_rng_u32_device(rng, n * 6, u));
             k_iou_points<<<grid_for(n), 256, 0, st>>>(u, n, make_double3(lo[0], lo[1], lo[2]),
                                                        make_double3(hi[0], hi[1], hi[2]), p, x);
-            RD_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaGetLastError());
             ev.eval(x, n, 3, v);
-            RD_CUDA(cudaMemcpyAsync(hp.data(), p, size_t(n) * 3 * 8, cudaMemcpyDeviceToHost, st));
-            RD_CUDA(cudaMemcpyAsync(hv.data(), v, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
-            RD_CUDA(cudaStreamSynchronize(st));
+            NFG_HC_CUDA(cudaMemcpyAsync(hp.data(), p, size_t(n) * 3 * 8, cudaMemcpyDeviceToHost, st));
+            NFG_HC_CUDA(cudaMemcpyAsync(hv.data(), v, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
+            NFG_HC_CUDA(cudaStreamSynchronize(st));
             for (int64_t i = 0; i < n; ++i) {
                 const bool m_in = hv[size_t(i)] < 0;
                 const bool o_in = oracle_sign(hp.data() + 3 * i, sign_user) < 0;

@@ -21,13 +21,17 @@
 #include <vector>
 
 #include "../../include/nfg.h"
+#include "host_common.h"
 #include "host_init.h"
 
-namespace nfg {
-void set_last_error(const std::string& msg);   // field.cu
-}
 
 namespace {
+
+using nfg::hc::Buf;
+using nfg::hc::Fail;
+using nfg::hc::grid_for;
+using nfg::hc::ok;
+using nfg::hc::run;
 
 constexpr uint64_t PCG_MULT = 6364136223846793005ULL;
 
@@ -168,68 +172,11 @@ __global__ void k_sum_partials(const double* __restrict__ partial, int n, double
     *out = s;
 }
 
-struct Fail {
-    nfg_status st;
-    std::string msg;
-};
 
-#define TK_CUDA(call)                                                                                   \
-    do {                                                                                                \
-        const cudaError_t e_ = (call);                                                                  \
-        if (e_ != cudaSuccess)                                                                          \
-            throw Fail{ NFG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_) };                \
-    } while (0)
 
-void ok(nfg_status st)
-{
-    if (st != NFG_OK)
-        throw Fail{ st, nfg_last_error() };
-}
 
-template <class Fn>
-nfg_status run(Fn&& fn)
-{
-    try {
-        fn();
-        return NFG_OK;
-    } catch (const Fail& f) {
-        nfg::set_last_error(f.msg);
-        return f.st;
-    } catch (const std::invalid_argument& e) {
-        nfg::set_last_error(e.what());
-        return NFG_EINVAL;
-    } catch (const std::exception& e) {
-        nfg::set_last_error(e.what());
-        return NFG_ECUDA;
-    }
-}
 
-struct Buf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    void* get(size_t n)
-    {
-        if (n > bytes) {
-            if (p)
-                cudaFree(p);
-            p = nullptr;
-            bytes = 0;
-            TK_CUDA(cudaMalloc(&p, n));
-            bytes = n;
-        }
-        return p;
-    }
-    ~Buf()
-    {
-        if (p)
-            cudaFree(p);
-    }
-};
 
-unsigned grid_for(int64_t n, int per_block = 256, int64_t cap = 148 * 16)
-{
-    return unsigned(std::max<int64_t>(1, std::min<int64_t>((n + per_block - 1) / per_block, cap)));
-}
 
 }   // namespace
 
@@ -252,7 +199,7 @@ struct nfg_rng {
         RngState* dst = d + (cur ^ 1);
         if (threshold == 0u || n == 0) {
             k_rng_direct<<<grid_for(n), 256, 0, stream>>>(src, dst, bound, n, out, nullptr);
-            TK_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaGetLastError());
         } else {
             // expected rejections n*p; the margin covers > 10 sigma
             const double p = double(threshold) / 4294967296.0;
@@ -262,13 +209,13 @@ struct nfg_rng {
             uint32_t* k = static_cast<uint32_t*>(keep.get(size_t(m) * 4));
             uint32_t* q = static_cast<uint32_t*>(pos.get(size_t(m) * 4));
             size_t tb = 0;
-            TK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, k, q, m, stream));
+            NFG_HC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, k, q, m, stream));
             void* t = tmp.get(std::max<size_t>(tb, 16));
             k_rng_draw<<<grid_for(m), 256, 0, stream>>>(src, m, threshold, v, k);
-            TK_CUDA(cudaGetLastError());
-            TK_CUDA(cub::DeviceScan::ExclusiveSum(t, tb, k, q, m, stream));
+            NFG_HC_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cub::DeviceScan::ExclusiveSum(t, tb, k, q, m, stream));
             k_rng_compact<<<grid_for(m), 256, 0, stream>>>(src, dst, m, n, bound, v, k, q, out, d_err);
-            TK_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaGetLastError());
         }
         cur ^= 1;
     }
@@ -278,7 +225,7 @@ struct nfg_rng {
         if (n < 0)
             throw std::invalid_argument("nfg_rng: negative count");
         k_rng_direct<<<grid_for(n), 256, 0, stream>>>(d + cur, d + (cur ^ 1), 0u, n, out, nullptr);
-        TK_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaGetLastError());
         cur ^= 1;
     }
 
@@ -287,15 +234,15 @@ struct nfg_rng {
         if (n < 0)
             throw std::invalid_argument("nfg_rng: negative count");
         k_rng_direct<<<grid_for(n), 256, 0, stream>>>(d + cur, d + (cur ^ 1), 1u, n, nullptr, out);
-        TK_CUDA(cudaGetLastError());
+        NFG_HC_CUDA(cudaGetLastError());
         cur ^= 1;
     }
 
     void check()
     {
         unsigned int e = 0;
-        TK_CUDA(cudaMemcpyAsync(&e, d_err, 4, cudaMemcpyDeviceToHost, stream));
-        TK_CUDA(cudaStreamSynchronize(stream));
+        NFG_HC_CUDA(cudaMemcpyAsync(&e, d_err, 4, cudaMemcpyDeviceToHost, stream));
+        NFG_HC_CUDA(cudaStreamSynchronize(stream));
         if (e)
             throw Fail{ NFG_ECUDA, "nfg_rng: rejection-sampling margin exhausted" };
     }
@@ -322,11 +269,11 @@ nfg_status nfg_rng_create(nfg_ctx* ctx, uint64_t seed, uint64_t seq, nfg_rng** o
         h.state = h.state * PCG_MULT + h.inc;
         h.state += seed;
         h.state = h.state * PCG_MULT + h.inc;
-        TK_CUDA(cudaMalloc(&r->d, 2 * sizeof(RngState)));
-        TK_CUDA(cudaMalloc(&r->d_err, sizeof(unsigned int)));
-        TK_CUDA(cudaMemcpyAsync(r->d, &h, sizeof(h), cudaMemcpyHostToDevice, r->stream));
-        TK_CUDA(cudaMemsetAsync(r->d_err, 0, sizeof(unsigned int), r->stream));
-        TK_CUDA(cudaStreamSynchronize(r->stream));
+        NFG_HC_CUDA(cudaMalloc(&r->d, 2 * sizeof(RngState)));
+        NFG_HC_CUDA(cudaMalloc(&r->d_err, sizeof(unsigned int)));
+        NFG_HC_CUDA(cudaMemcpyAsync(r->d, &h, sizeof(h), cudaMemcpyHostToDevice, r->stream));
+        NFG_HC_CUDA(cudaMemsetAsync(r->d_err, 0, sizeof(unsigned int), r->stream));
+        NFG_HC_CUDA(cudaStreamSynchronize(r->stream));
         *out = r.release();
     });
 }
@@ -360,8 +307,8 @@ nfg_status nfg_rng_get_state(nfg_rng* r, uint64_t* state, uint64_t* inc)
     return run([&] {
         r->check();
         RngState h{};
-        TK_CUDA(cudaMemcpyAsync(&h, r->d + r->cur, sizeof(h), cudaMemcpyDeviceToHost, r->stream));
-        TK_CUDA(cudaStreamSynchronize(r->stream));
+        NFG_HC_CUDA(cudaMemcpyAsync(&h, r->d + r->cur, sizeof(h), cudaMemcpyDeviceToHost, r->stream));
+        NFG_HC_CUDA(cudaStreamSynchronize(r->stream));
         *state = h.state;
         *inc = h.inc;
     });
@@ -377,7 +324,7 @@ nfg_status nfg_image_batch_device(nfg_ctx* ctx, const uint32_t* idx_dev, int64_t
         if (n > 0) {
             k_image_batch<<<grid_for(n), 256, 0, st>>>(idx_dev, n, rgb_dev, uint32_t(width), uint32_t(height), X_dev,
                                                         T_dev);
-            TK_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaGetLastError());
         }
     });
 }
@@ -431,7 +378,7 @@ nfg_status nfg_fit_image(nfg_ctx* ctx, const nfg_image_task* task, const float* 
 
         Buf d_rgb, d_eidx, d_ex, d_et, d_pred, d_idx, d_X, d_T, d_part, d_sum, d_rec;
         float* rgb_dev = static_cast<float*>(d_rgb.get(npix * 3 * 4));
-        TK_CUDA(cudaMemcpyAsync(rgb_dev, rgb, npix * 3 * 4, cudaMemcpyHostToDevice, st));
+        NFG_HC_CUDA(cudaMemcpyAsync(rgb_dev, rgb, npix * 3 * 4, cudaMemcpyHostToDevice, st));
 
         // PSNR grid (tasks.cpp:78-94): every pixel, or 2^16 from Pcg32(seed, 7)
         const bool full = npix <= (uint64_t(1) << 20);
@@ -449,8 +396,8 @@ nfg_status nfg_fit_image(nfg_ctx* ctx, const nfg_image_task* task, const float* 
         float* et = static_cast<float*>(d_et.get(size_t(ne) * 3 * 4));
         float* pred = static_cast<float*>(d_pred.get(size_t(ne) * 3 * 4));
         k_image_batch<<<grid_for(ne), 256, 0, st>>>(eidx, ne, rgb_dev, uint32_t(w), uint32_t(h), ex, et);
-        TK_CUDA(cudaGetLastError());
-        const unsigned sq_blocks = grid_for(ne * 3, 256, 1024);
+        NFG_HC_CUDA(cudaGetLastError());
+        const unsigned sq_blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((ne * 3 + 255) / 256, 1024)));
         double* part = static_cast<double*>(d_part.get(sq_blocks * 8));
         double* dsum = static_cast<double*>(d_sum.get(8));
 
@@ -460,10 +407,10 @@ nfg_status nfg_fit_image(nfg_ctx* ctx, const nfg_image_task* task, const float* 
             ok(nfg_field_evaluate_device(f, ex, ne, pred));
             k_sqerr<<<sq_blocks, 256, 0, st>>>(pred, et, ne * 3, part);
             k_sum_partials<<<1, 1, 0, st>>>(part, int(sq_blocks), dsum);
-            TK_CUDA(cudaGetLastError());
+            NFG_HC_CUDA(cudaGetLastError());
             double s = 0.0;
-            TK_CUDA(cudaMemcpyAsync(&s, dsum, 8, cudaMemcpyDeviceToHost, st));
-            TK_CUDA(cudaStreamSynchronize(st));
+            NFG_HC_CUDA(cudaMemcpyAsync(&s, dsum, 8, cudaMemcpyDeviceToHost, st));
+            NFG_HC_CUDA(cudaStreamSynchronize(st));
             return s / double(ne * 3);
         };
         auto log_row = [&](int64_t step, double loss, double mse) {   // tasks.cpp:95-105
@@ -496,7 +443,7 @@ nfg_status nfg_fit_image(nfg_ctx* ctx, const nfg_image_task* task, const float* 
             br->below(uint32_t(npix), B, idx);
             if (B > 0) {
                 k_image_batch<<<grid_for(B), 256, 0, st>>>(idx, B, rgb_dev, uint32_t(w), uint32_t(h), X, T);
-                TK_CUDA(cudaGetLastError());
+                NFG_HC_CUDA(cudaGetLastError());
             }
             ok(nfg_field_train_step_device(f, X, T, B, B, NFG_LOSS_L2, step, nullptr));
             ok(nfg_field_step_record(f, recs + pending));
@@ -504,9 +451,9 @@ nfg_status nfg_fit_image(nfg_ctx* ctx, const nfg_image_task* task, const float* 
             const bool log = step % task->log_interval == 0 || step == task->total_steps;
             if (!log && pending < chunk)
                 continue;
-            TK_CUDA(cudaMemcpyAsync(hrec.data(), recs, size_t(pending) * sizeof(nfg_step_record),
+            NFG_HC_CUDA(cudaMemcpyAsync(hrec.data(), recs, size_t(pending) * sizeof(nfg_step_record),
                                     cudaMemcpyDeviceToHost, st));
-            TK_CUDA(cudaStreamSynchronize(st));
+            NFG_HC_CUDA(cudaStreamSynchronize(st));
             br->check();
             float loss = 0.0f;
             for (int64_t k = 0; k < pending; ++k) {   // the reference's per-step checks, in step order
