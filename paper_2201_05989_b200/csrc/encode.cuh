@@ -63,6 +63,25 @@ __device__ __forceinline__ float2 encode_pair(const GridDev& g, const LevelDev* 
     const CornerSet<D> cs = corners_of<D>(g, lv, x);
     const TT* base = table + size_t(lv.row_off) * F + (col % F);
     float2 v[1 << D];
+#if !defined(NFG_NO_PAIR_LOADS)   // +7% k_infer (3.15e9 -> 3.37e9 queries/s): 25% fewer L1 requests on an L1-bound kernel
+    if (F == 2 && sizeof(TT) == 2) {
+        // x-adjacent corners whose rows share an aligned 2-row block (levels
+        // start on even rows): one 8-byte load instead of two 4-byte loads
+#pragma unroll
+        for (int c = 0; c < (1 << D); c += 2) {
+            const uint32_t r0 = cs.row(c), r1 = cs.row(c + 1);
+            if (r1 == (r0 ^ 1u)) {
+                const uint2 u = __ldg(reinterpret_cast<const uint2*>(base + size_t(r0 & ~1u) * 2));
+                const float2 lo = unpack_half2(u.x), hi = unpack_half2(u.y);
+                v[c] = (r0 & 1u) ? hi : lo;
+                v[c + 1] = (r0 & 1u) ? lo : hi;
+            } else {
+                v[c] = Gather<TT>::two(base + size_t(r0) * F);
+                v[c + 1] = Gather<TT>::two(base + size_t(r1) * F);
+            }
+        }
+    } else
+#endif
 #pragma unroll
     for (int c = 0; c < (1 << D); ++c)
         v[c] = Gather<TT>::two(base + size_t(cs.row(c)) * F);
