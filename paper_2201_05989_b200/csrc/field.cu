@@ -232,6 +232,9 @@ struct nfg_field {
     // undo by re-zeroing; otherwise k_validate runs first.
     bool grads_clean = true;
     int64_t last_batch = 0;            // global batch of the last backward (Adam's dense/sparse choice)
+    // the step scratch was already reset at the end of the previous synchronous
+    // train_step (after its status was read), so the next step skips it
+    bool scratch_ready = false;
     unsigned int* d_ready = nullptr;   // NFG_MAX_CHUNKS chunk-ready flags
     unsigned int epoch = 0;
     DevBuf det_part, det_loss, det_sort;   // deterministic mode scratch
@@ -254,6 +257,7 @@ nfg::StepScratch scratch_of(nfg_field* f)
 
 void reset_scratch(nfg_field* f)
 {
+    f->scratch_ready = false;   // any other user dirties it after this reset
     cudaStream_t st = f->ctx->stream;
     NFG_CUDA(cudaMemsetAsync(f->d_res, 0, sizeof(StepResult), st));
     NFG_CUDA(cudaMemsetAsync(&f->d_res->flags[2], 0xff, sizeof(unsigned int), st));
@@ -309,14 +313,27 @@ bool launches_serialized()
 }
 
 // True for page-locked (cudaHostAlloc / cudaHostRegister) host memory.
+// The answer only steers the streamed-copy heuristic (a pageable source is
+// still copied correctly), so the last few answers are cached per thread to
+// keep cudaPointerGetAttributes off the per-step path.
 bool is_pinned(const void* p)
 {
+    thread_local const void* cache_p[4] = { nullptr, nullptr, nullptr, nullptr };
+    thread_local bool cache_v[4] = { false, false, false, false };
+    thread_local int next = 0;
+    for (int i = 0; i < 4; ++i)
+        if (cache_p[i] == p)
+            return cache_v[i];
     cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    bool v = false;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess)
         cudaGetLastError();
-        return false;
-    }
-    return at.type == cudaMemoryTypeHost;
+    else
+        v = at.type == cudaMemoryTypeHost;
+    cache_p[next] = p;
+    cache_v[next] = v;
+    next = (next + 1) & 3;
+    return v;
 }
 
 template <class T>
@@ -443,7 +460,9 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
     require(loss_kind >= 0 && loss_kind <= 2, "train_step: unknown loss");
     require(B_local >= 0 && B_global >= B_local, "train_step: invalid batch size");
     nfg_ctx* c = f->ctx;
-    reset_scratch(f);
+    if (!f->scratch_ready)
+        reset_scratch(f);
+    f->scratch_ready = false;
     // encode_forward's input checks (grid.hpp:226-229). With a clean gradient
     // slab the fused kernel checks its own inputs and Adam's check kernel
     // undoes the step on failure (re-zeroing); otherwise a separate k_validate
@@ -1067,6 +1086,8 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
             device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step);
         }
         fetch_result(f);
+        reset_scratch(f);   // for the next step, off its critical path (h_res holds this one)
+        f->scratch_ready = true;
         if (f->h_res->flags[1]) {
             f->step = before;   // the reference throws before incrementing (adam.hpp:86-92)
             // invalid input on a clean slab was undone by re-zeroing; a
