@@ -373,6 +373,29 @@ nfg_status nfg_nerf_sh4(nfg_ctx* ctx, const float* dirs, int64_t n, float* out);
 nfg_status nfg_nerf_scene_render(nfg_ctx* ctx, const float* cams, int32_t n_views, int32_t width, int32_t height,
                                  float focal, const float* bg, float* rgb);
 
+/* fit_sdf (tasks.cpp:133-193) on the ANALYTIC CSG target of BASELINE config 2
+ * (sphere r=0.3 at the centre union a torus R=0.25, r=0.08 in the xz-plane):
+ * uniform points from Pcg32(seed, 2) replace the reference's mesh sampling
+ * (geometry is out of scope), the metric column is the interior IoU against
+ * the analytic sign on iou_eval_points from Pcg32(seed, 11) (tasks.cpp:163-171),
+ * row 0 has loss 0 (tasks.cpp:173). */
+typedef struct {
+    nfg_grid_config cfg;     /* dims forced to 3 */
+    int32_t hidden_layers;
+    int32_t hidden_width;
+    int32_t batch_size;
+    int32_t loss;            /* nfg_loss_kind; the reference's SdfTask default is MAPE */
+    int64_t total_steps;
+    int64_t log_interval;
+    int64_t iou_eval_points;
+    double lr;
+    double lr_decay;
+} nfg_sdf_task;
+nfg_status nfg_fit_sdf_analytic(nfg_ctx* ctx, const nfg_sdf_task* task, uint64_t seed, const nfg_options* opts,
+                                nfg_field** model_out, nfg_report_row* rows, int64_t rows_cap, int64_t* n_rows);
+/* The config-2 CSG SDF at n points (X: n x 3 device), in the oracle's fp32 order. */
+nfg_status nfg_csg_sdf_device(nfg_ctx* ctx, const float* X_dev, int64_t n, float* out_dev);
+
 nfg_status nfg_host_alloc(size_t bytes, void** out);
 nfg_status nfg_host_free(void* p);
 

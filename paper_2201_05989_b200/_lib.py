@@ -45,6 +45,13 @@ class nfg_image_task(C.Structure):
                 ("total_steps", C.c_int64), ("log_interval", C.c_int64), ("lr", C.c_double), ("lr_decay", C.c_double)]
 
 
+class nfg_sdf_task(C.Structure):
+    _fields_ = [("cfg", nfg_grid_config), ("hidden_layers", C.c_int32), ("hidden_width", C.c_int32),
+                ("batch_size", C.c_int32), ("loss", C.c_int32), ("total_steps", C.c_int64),
+                ("log_interval", C.c_int64), ("iou_eval_points", C.c_int64), ("lr", C.c_double),
+                ("lr_decay", C.c_double)]
+
+
 class nfg_report_row(C.Structure):
     _fields_ = [("step", C.c_int64), ("time_s", C.c_double), ("loss", C.c_double), ("metric", C.c_double),
                 ("lr", C.c_double)]
@@ -153,6 +160,9 @@ SIGNATURES = {
                                      C.POINTER(C.c_double)]),
     "nfg_nerf_sh4": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
     "nfg_nerf_scene_render": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int32, C.c_float, _vp, _vp]),
+    "nfg_fit_sdf_analytic": (C.c_int, [_vp, C.POINTER(nfg_sdf_task), C.c_uint64, C.POINTER(nfg_options),
+                                       C.POINTER(_vp), C.POINTER(nfg_report_row), C.c_int64, _i64p]),
+    "nfg_csg_sdf_device": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
     "nfg_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
     "nfg_host_free": (C.c_int, [_vp]),
 }

@@ -178,6 +178,72 @@ __global__ void k_sum_partials(const double* __restrict__ partial, int n, double
 
 
 
+// ---- fit_sdf on the analytic CSG target (BASELINE config 2) -----------------
+// The CSG SDF of the synthetic SDF scene (sphere r=.3 at the cube centre union a
+// torus R=.25, r=.08 in the xz-plane), in the oracle's exact fp32 operation
+// order (oracle/nf_oracle.hpp csg_sdf).
+template <class S>
+__device__ __forceinline__ S csg_sdf(S x, S y, S z)
+{
+    const S cx = x - S(0.5), cy = y - S(0.5), cz = z - S(0.5);
+    const S sphere = sqrt(cx * cx + cy * cy + cz * cz) - S(0.3);
+    const S q = sqrt(cx * cx + cz * cz) - S(0.25);
+    const S torus = sqrt(q * q + cy * cy) - S(0.08);
+    return sphere < torus ? sphere : torus;
+}
+
+__device__ __forceinline__ float csg_sdf_f(float x, float y, float z)
+{
+    const float cx = __fsub_rn(x, 0.5f), cy = __fsub_rn(y, 0.5f), cz = __fsub_rn(z, 0.5f);
+    const float sphere =
+        __fsub_rn(__fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(cx, cx), __fmul_rn(cy, cy)), __fmul_rn(cz, cz))), 0.3f);
+    const float q = __fsub_rn(__fsqrt_rn(__fadd_rn(__fmul_rn(cx, cx), __fmul_rn(cz, cz))), 0.25f);
+    const float torus = __fsub_rn(__fsqrt_rn(__fadd_rn(__fmul_rn(q, q), __fmul_rn(cy, cy))), 0.08f);
+    return fminf(sphere, torus);
+}
+
+__global__ void k_csg_target(const float* __restrict__ X, int64_t n, float* __restrict__ T)
+{
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        T[i] = csg_sdf_f(X[3 * i], X[3 * i + 1], X[3 * i + 2]);
+}
+
+// iou points (Pcg32::uniform<double> in [0,1]^3 from 6 draws) and the
+// analytic interior test in double on the double point, as the reference's
+// oracle_sign gets the double point (tasks.cpp:338-350)
+__global__ void k_iou_points_csg(const uint32_t* __restrict__ u, int64_t n, float* __restrict__ X,
+                                 uint8_t* __restrict__ inside)
+{
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        double p[3];
+        for (int k = 0; k < 3; ++k) {
+            const uint64_t a = u[6 * i + 2 * k], b = u[6 * i + 2 * k + 1];
+            p[k] = 0.0 + (1.0 - 0.0) * (double((a << 21) ^ b) * 0x1p-53);
+            X[3 * i + k] = float(p[k]);
+        }
+        inside[i] = csg_sdf<double>(p[0], p[1], p[2]) < 0.0 ? 1 : 0;
+    }
+}
+
+__global__ void k_iou_count(const float* __restrict__ pred, const uint8_t* __restrict__ inside, int64_t n,
+                            unsigned long long* both_either)
+{
+    unsigned long long b = 0, e = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const bool m = pred[i] < 0.0f, o = inside[i] != 0;
+        b += (m && o) ? 1 : 0;
+        e += (m || o) ? 1 : 0;
+    }
+    for (int s = 16; s > 0; s >>= 1) {
+        b += __shfl_xor_sync(0xffffffffu, b, s);
+        e += __shfl_xor_sync(0xffffffffu, e, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(both_either, b);
+        atomicAdd(both_either + 1, e);
+    }
+}
+
 }   // namespace
 
 struct nfg_rng {
@@ -466,6 +532,141 @@ nfg_status nfg_fit_image(nfg_ctx* ctx, const nfg_image_task* task, const float* 
             first_pending = step + 1;
             if (log)
                 log_row(step, double(loss), mse_now());
+        }
+        if (task->total_steps > 0)
+            ok(nfg_field_check(f));
+        const int64_t nr = int64_t(report.size());
+        for (int64_t i = 0; i < std::min(nr, rows_cap); ++i)
+            rows[i] = report[size_t(i)];
+        if (n_rows)
+            *n_rows = nr;
+        *model_out = model.release();
+    });
+}
+
+nfg_status nfg_csg_sdf_device(nfg_ctx* ctx, const float* X_dev, int64_t n, float* out_dev)
+{
+    return run([&] {
+        if (n > 0) {
+            k_csg_target<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(nfg_ctx_stream(ctx))>>>(X_dev, n, out_dev);
+            NFG_HC_CUDA(cudaGetLastError());
+        }
+    });
+}
+
+nfg_status nfg_fit_sdf_analytic(nfg_ctx* ctx, const nfg_sdf_task* task, uint64_t seed, const nfg_options* opts,
+                                nfg_field** model_out, nfg_report_row* rows, int64_t rows_cap, int64_t* n_rows)
+{
+    return run([&] {
+        *model_out = nullptr;
+        if (n_rows)
+            *n_rows = 0;
+        if (task->batch_size < 0 || task->total_steps < 0 || task->log_interval <= 0 || task->iou_eval_points < 0)
+            throw std::invalid_argument("fit_sdf: invalid task");
+        if (task->loss < 0 || task->loss > 2)
+            throw std::invalid_argument("fit_sdf: unknown loss");
+        cudaStream_t st = static_cast<cudaStream_t>(nfg_ctx_stream(ctx));
+        // model configuration (tasks.cpp:140-158)
+        nfg_grid_config g = task->cfg;
+        g.dims = 3;
+        nfg_mlp_config m{};
+        m.hidden_layers = task->hidden_layers;
+        m.hidden_width = task->hidden_width;
+        m.output_width = 1;
+        m.output_activation = NFG_ACT_LINEAR;
+        nfg_adam_hyper hy{ task->lr, 0.9, 0.99, 1e-15, 1e-6 };
+        nfg_options o = opts ? *opts : nfg_options{ 0, 1, 0 };
+        nfg_field* f = nullptr;
+        ok(nfg_field_create(ctx, &g, &m, &hy, &o, &f));
+        std::unique_ptr<nfg_field, nfg_status (*)(nfg_field*)> model(f, nfg_field_destroy);
+        ok(nfg_field_init(f, seed));
+        std::vector<int64_t> ms;
+        {
+            const int64_t total = task->total_steps;
+            int64_t next = int64_t(0.65 * double(total));
+            const int64_t stride = int64_t(0.30 * double(total));
+            while (next < total && stride > 0) {
+                ms.push_back(next);
+                next += stride;
+            }
+        }
+        ok(nfg_field_set_schedule(f, ms.empty() ? nullptr : ms.data(), int32_t(ms.size()), task->lr_decay));
+
+        Buf d_u, d_xi, d_in, d_pred, d_cnt, d_X, d_T, d_rec;
+        std::vector<nfg_report_row> report;
+        const auto t0 = std::chrono::steady_clock::now();
+        auto iou_now = [&]() {   // tasks.cpp:163-171: Pcg32(seed, 11), same points every row
+            nfg_rng* ir = nullptr;
+            ok(nfg_rng_create(ctx, seed, 11, &ir));
+            std::unique_ptr<nfg_rng, nfg_status (*)(nfg_rng*)> irg(ir, nfg_rng_destroy);
+            unsigned long long* cnt = d_cnt.as<unsigned long long>(2);
+            NFG_HC_CUDA(cudaMemsetAsync(cnt, 0, 16, st));
+            const int64_t chunk = int64_t(1) << 16;
+            for (int64_t done = 0; done < task->iou_eval_points; done += chunk) {
+                const int64_t k = std::min(chunk, task->iou_eval_points - done);
+                uint32_t* u = d_u.as<uint32_t>(size_t(k) * 6);
+                float* xi = d_xi.as<float>(size_t(k) * 3);
+                uint8_t* in = d_in.as<uint8_t>(size_t(k));
+                float* pr = d_pred.as<float>(size_t(k));
+                ir->u32(k * 6, u);
+                k_iou_points_csg<<<grid_for(k), 256, 0, st>>>(u, k, xi, in);
+                NFG_HC_CUDA(cudaGetLastError());
+                ok(nfg_field_evaluate_device(f, xi, k, pr));
+                k_iou_count<<<grid_for(k), 256, 0, st>>>(pr, in, k, cnt);
+                NFG_HC_CUDA(cudaGetLastError());
+            }
+            unsigned long long h[2] = { 0, 0 };
+            NFG_HC_CUDA(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, st));
+            NFG_HC_CUDA(cudaStreamSynchronize(st));
+            return h[1] == 0 ? 1.0 : double(h[0]) / double(h[1]);
+        };
+        auto log_row = [&](int64_t step, double loss) {
+            nfg_report_row r{};
+            r.step = step;
+            r.time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            r.loss = loss;
+            r.metric = iou_now();
+            r.lr = nfg_lr_at(ms.empty() ? nullptr : ms.data(), int32_t(ms.size()), task->lr_decay, task->lr, step);
+            report.push_back(r);
+        };
+        log_row(0, 0.0);   // tasks.cpp:173
+
+        nfg_rng* sr = nullptr;   // Pcg32(seed, 2) (tasks.cpp:175)
+        ok(nfg_rng_create(ctx, seed, 2, &sr));
+        std::unique_ptr<nfg_rng, nfg_status (*)(nfg_rng*)> srg(sr, nfg_rng_destroy);
+        const int64_t B = task->batch_size;
+        float* X = d_X.as<float>(std::max<size_t>(size_t(B) * 3, 4));
+        float* T = d_T.as<float>(std::max<size_t>(size_t(B), 4));
+        const int64_t chunk = std::min<int64_t>(task->log_interval, std::max<int64_t>(task->total_steps, 1));
+        nfg_step_record* recs = d_rec.as<nfg_step_record>(size_t(chunk));
+        std::vector<nfg_step_record> hrec(static_cast<size_t>(chunk));
+        int64_t pending = 0, first_pending = 1;
+        for (int64_t step = 1; step <= task->total_steps; ++step) {
+            sr->floats(B * 3, X);   // uniform points in [0,1]^3 (analytic target: no mesh sampling)
+            if (B > 0) {
+                k_csg_target<<<grid_for(B), 256, 0, st>>>(X, B, T);
+                NFG_HC_CUDA(cudaGetLastError());
+            }
+            ok(nfg_field_train_step_device(f, X, T, B, B, task->loss, step, nullptr));
+            ok(nfg_field_step_record(f, recs + pending));
+            ++pending;
+            const bool log = step % task->log_interval == 0 || step == task->total_steps;
+            if (!log && pending < chunk)
+                continue;
+            NFG_HC_CUDA(cudaMemcpyAsync(hrec.data(), recs, size_t(pending) * sizeof(nfg_step_record),
+                                        cudaMemcpyDeviceToHost, st));
+            NFG_HC_CUDA(cudaStreamSynchronize(st));
+            sr->check();
+            float loss = 0.0f;
+            for (int64_t k = 0; k < pending; ++k) {
+                ok(nfg_step_record_check(f, &hrec[size_t(k)], B, &loss));
+                if (!std::isfinite(loss))   // tasks.cpp:187-188
+                    throw Fail{ NFG_ENONFINITE, "fit_sdf: non-finite loss at step " + std::to_string(first_pending + k) };
+            }
+            pending = 0;
+            first_pending = step + 1;
+            if (log)
+                log_row(step, double(loss));
         }
         if (task->total_steps > 0)
             ok(nfg_field_check(f));

@@ -605,6 +605,20 @@ class ImageTask:   # tasks.hpp:16-31 (hash encoder)
 
 
 @dataclass
+class SdfTask:   # tasks.hpp:33-50 (hash encoder; analytic CSG target instead of a mesh)
+    cfg: HashEncodingConfig = field(default_factory=HashEncodingConfig)
+    hidden_layers: int = 2
+    hidden_width: int = 64
+    batch_size: int = 1 << 13
+    total_steps: int = 10000
+    log_interval: int = 1000
+    lr: float = 1e-4
+    lr_decay: float = 0.33
+    loss: LossKind = LossKind.Mape
+    iou_eval_points: int = 1 << 16
+
+
+@dataclass
 class FitResult:   # tasks.hpp:58-61
     model: "FieldModel"
     report: TrainReport
@@ -627,19 +641,7 @@ def fit_image(task: ImageTask, seed: int, options: Optional[Options] = None,
     opts = options or Options()
     L.check(ctx.lib.nfg_fit_image(ctx.h, C.byref(t), _ptr(rgb), seed, C.byref(opts.c()), C.byref(h), rows, cap,
                                   C.byref(n)))
-    model = FieldModel(ctx, opts)
-    model.h = h
-    g, m = L.nfg_grid_config(), L.nfg_mlp_config()
-    L.check(ctx.lib.nfg_field_get_config(h, C.byref(g), C.byref(m)))
-    model.hash_cfg = HashEncodingConfig(g.levels, g.table_size, g.features, g.n_min, g.n_max, g.dims,
-                                        Interpolation(g.interpolation))
-    model.mlp_cfg = MlpConfig(m.input_width, m.hidden_layers, m.hidden_width, m.output_width,
-                              OutputActivation(m.output_activation))
-    model.hyper = AdamHyper(lr=task.lr)
-    model.schedule = default_schedule(task.total_steps, task.lr_decay)
-    sz = (C.c_uint64 * 3)()
-    L.check(ctx.lib.nfg_field_sizes(h, sz))
-    model._sizes = tuple(int(x) for x in sz)
+    model = _adopt_field(ctx, h, opts, task.lr, task.total_steps, task.lr_decay)
     rep = TrainReport([TrainReportRow(int(r.step), r.time_s, r.loss, r.metric, r.lr)
                        for r in rows[:min(n.value, cap)]])
     return FitResult(model, rep)
@@ -829,6 +831,42 @@ def nerf_scene_render(cams, width: int, height: int, focal: float, bg=(1.0, 1.0,
     L.check(ctx.lib.nfg_nerf_scene_render(ctx.h, _ptr(cams), cams.shape[0], width, height, focal, _ptr(bgv),
                                           _ptr(out)))
     return out
+
+
+def _adopt_field(ctx: Context, h, opts: "Options", lr: float, total_steps: int, lr_decay: float) -> "FieldModel":
+    model = FieldModel(ctx, opts)
+    model.h = h
+    g, m = L.nfg_grid_config(), L.nfg_mlp_config()
+    L.check(ctx.lib.nfg_field_get_config(h, C.byref(g), C.byref(m)))
+    model.hash_cfg = HashEncodingConfig(g.levels, g.table_size, g.features, g.n_min, g.n_max, g.dims,
+                                        Interpolation(g.interpolation))
+    model.mlp_cfg = MlpConfig(m.input_width, m.hidden_layers, m.hidden_width, m.output_width,
+                              OutputActivation(m.output_activation))
+    model.hyper = AdamHyper(lr=lr)
+    model.schedule = default_schedule(total_steps, lr_decay)
+    sz = (C.c_uint64 * 3)()
+    L.check(ctx.lib.nfg_field_sizes(h, sz))
+    model._sizes = tuple(int(x) for x in sz)
+    return model
+
+
+def fit_sdf_analytic(task: SdfTask, seed: int, options: Optional[Options] = None,
+                     ctx: Optional[Context] = None) -> FitResult:   # tasks.cpp:133-193 on the config-2 CSG target
+    ctx = ctx or default_context()
+    g = task.cfg
+    cfg = HashEncodingConfig(g.levels, g.table_size, g.features, g.n_min, g.n_max, 3, g.interpolation)
+    t = L.nfg_sdf_task(cfg.c(), task.hidden_layers, task.hidden_width, task.batch_size, int(task.loss),
+                       task.total_steps, task.log_interval, task.iou_eval_points, task.lr, task.lr_decay)
+    cap = task.total_steps // max(task.log_interval, 1) + 2
+    rows = (L.nfg_report_row * cap)()
+    n = C.c_int64()
+    h = C.c_void_p()
+    opts = options or Options()
+    L.check(ctx.lib.nfg_fit_sdf_analytic(ctx.h, C.byref(t), seed, C.byref(opts.c()), C.byref(h), rows, cap,
+                                         C.byref(n)))
+    model = _adopt_field(ctx, h, opts, task.lr, task.total_steps, task.lr_decay)
+    rep = TrainReport([TrainReportRow(int(r.step), r.time_s, r.loss, r.metric, r.lr) for r in rows[:min(n.value, cap)]])
+    return FitResult(model, rep)
 
 
 class PinnedBuffer:

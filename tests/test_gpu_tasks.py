@@ -180,3 +180,45 @@ def test_criterion_9_determinism():   # acceptance.cpp:661-711 on the GPU path
     m1, m2 = nf.fit_image(t, 2718), nf.fit_image(t, 2718)
     worst = max(abs(x.metric - y.metric) / max(abs(x.metric), 1e-12) for x, y in zip(m1.report.rows, m2.report.rows))
     assert worst < 3e-2, worst
+
+
+def _csg_double(p):   # the analytic interior in double (tasks.cpp iou oracle_sign)
+    import math
+    cx, cy, cz = p[0] - 0.5, p[1] - 0.5, p[2] - 0.5
+    sphere = math.sqrt(cx * cx + cy * cy + cz * cz) - 0.3
+    q = math.sqrt(cx * cx + cz * cz) - 0.25
+    torus = math.sqrt(q * q + cy * cy) - 0.08
+    return -1 if min(sphere, torus) < 0 else 1
+
+
+def test_fit_sdf_analytic_device_loop_equals_host_loop():   # tasks.cpp:133-193 (analytic target)
+    nf = _nf()
+    cfg = nf.HashEncodingConfig(levels=8, table_size=1 << 14, features=2, n_min=8, n_max=128, dims=3)
+    task = nf.SdfTask(cfg=cfg, batch_size=4096, total_steps=40, log_interval=20, lr=1e-3, iou_eval_points=3000)
+    res = nf.fit_sdf_analytic(task, 5, nf.Options(deterministic=True))
+    m = nf.FieldModel(options=nf.Options(deterministic=True))
+    m.hash_cfg = cfg
+    m.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=1)
+    m.hyper = nf.AdamHyper(lr=1e-3)
+    m.schedule = nf.default_schedule(task.total_steps)
+    m.init(5)
+    rng = O.Pcg32(5, 2)
+    losses = {}
+    for step in range(1, 41):
+        X = rng.floats(4096 * 3).reshape(-1, 3)
+        losses[step] = m.train_step(X, O.csg_sdf(X).reshape(-1, 1), nf.LossKind.Mape, step)
+    assert np.array_equal(res.model.params.view(np.uint32), m.params.view(np.uint32))
+    assert [r.step for r in res.report.rows] == [0, 20, 40]
+    assert res.report.rows[0].loss == 0.0 and res.report.rows[2].loss == pytest.approx(losses[40], rel=1e-6)
+    iou = O.iou(lambda X: m.evaluate(X), _csg_double, 3000, O.Pcg32(5, 11))
+    assert res.report.rows[-1].metric == iou
+
+
+def test_fit_sdf_analytic_improves_iou():   # test_tasks.cpp:237-258
+    nf = _nf()
+    task = nf.SdfTask(cfg=nf.HashEncodingConfig(levels=8, table_size=1 << 14, n_min=8, n_max=128, dims=3),
+                      batch_size=1 << 14, total_steps=300, log_interval=100, lr=1e-2, iou_eval_points=1 << 14)
+    r = nf.fit_sdf_analytic(task, 5)
+    assert len(r.report.rows) >= 2
+    assert r.report.rows[-1].metric > r.report.rows[0].metric and r.report.rows[-1].metric > 0.5
+    assert np.isfinite(r.report.rows[-1].loss)
