@@ -458,7 +458,7 @@ def main():
 
     # ---- config 3: gigapixel image, tables beyond L2 (one GPU) ----------------------
     giga_line = None
-    if not args.no_nerf:
+    if rank == 0 and not args.no_nerf:   # secondary, single-GPU numbers: rank 0 only
         try:
             giga_line = bench_gigapixel(nf, ctx, steps=max(5, args.steps // 2), warmup=3)
         except Exception as e:
@@ -466,7 +466,7 @@ def main():
 
     # ---- config 4: NeRF training (occupancy-grid marching, compacted samples) ----
     nerf_line = None
-    if not args.no_nerf:
+    if rank == 0 and not args.no_nerf:
         try:
             nerf_line = bench_nerf(nf, ctx, steps=max(10, args.steps), warmup=40)
         except Exception as e:   # secondary number: never lose the headline line
