@@ -456,6 +456,26 @@ def main():
         t_inf = float(tt.item())
     qps = world * Bq / (t_inf / 1000.0)
 
+    # config-5 sweep 2^16 .. 2^26 queries per GPU (same model, device-resident queries)
+    sweep = []
+    if rank == 0 and not args.no_nerf:
+        for lg in (16, 18, 20, 22, 24, 26):
+            nq = 1 << lg
+            Xs_ = Xq[:nq] if nq <= Bq else torch.rand(nq, 3, device="cuda", generator=gen)
+            o_ = torch.empty(nq, 1, device="cuda")
+            for _ in range(2):
+                model.evaluate_device(Xs_, nq, o_)
+            ctx.synchronize()
+            reps = max(3, min(50, (1 << 24) // nq))
+            ev0.record(stream)
+            for _ in range(reps):
+                model.evaluate_device(Xs_, nq, o_)
+            ev1.record(stream)
+            ctx.synchronize()
+            ms_ = ev0.elapsed_time(ev1) / reps
+            sweep.append({"queries": nq, "queries_per_s": nq / (ms_ / 1000.0), "ms_per_call": ms_})
+            del Xs_, o_
+
     # ---- config 3: gigapixel image, tables beyond L2 (one GPU) ----------------------
     giga_line = None
     if rank == 0 and not args.no_nerf:   # secondary, single-GPU numbers: rank 0 only
@@ -524,7 +544,7 @@ def main():
                 "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": B_TRAIN * 16,
                         "d2h_bytes_per_step": 32, "steps": e2e_steps},
                 "inference": {"value": qps, "unit": "queries/s", "queries": Bq * world,
-                              "ms_per_call": t_inf},
+                              "ms_per_call": t_inf, "sweep_one_gpu": sweep},
                 "gigapixel": giga_line,
                 "nerf": nerf_line,
                 "phases_ms_per_step": ({"train_kernel": phase_ms[0], "adam": phase_ms[1]} if world == 1 else
