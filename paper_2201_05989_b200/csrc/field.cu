@@ -235,6 +235,7 @@ struct nfg_field {
     // the step scratch was already reset at the end of the previous synchronous
     // train_step (after its status was read), so the next step skips it
     bool scratch_ready = false;
+    bool fused_ok = true;   // fused encode+MLP kernels exist for this shape
     unsigned int* d_ready = nullptr;   // NFG_MAX_CHUNKS chunk-ready flags
     unsigned int epoch = 0;
     DevBuf det_part, det_loss, det_sort;   // deterministic mode scratch
@@ -877,6 +878,13 @@ nfg_status nfg_field_create(nfg_ctx* ctx, const nfg_grid_config* grid, const nfg
             f->n_total_dev = f->n_tab_dev + nw + nb;
             f->n_alloc = (f->n_total_dev + 63) & ~uint64_t(63);
             f->shape = make_shape(f->gcfg, f->mcfg, f->levels, f->dev_row_off, f->opts);
+            // shapes without a fused instantiation run the staged kernels
+            // (encode -> MLP -> encode backward as separate launches)
+            if (!nfg::staged_supported(f->shape))
+                throw Fail{ NFG_EUNSUPPORTED, "sm_100a MLP kernels are not built for this input width / depth" };
+            f->fused_ok = nfg::fused_supported(f->shape);
+            if (!f->fused_ok)
+                f->opts.fused_train = 0;
             NFG_CUDA(cudaSetDevice(ctx->device));
             const size_t bytes = f->n_alloc * sizeof(float);
             NFG_CUDA(cudaMalloc(&f->d_p, bytes));
@@ -1188,8 +1196,18 @@ nfg_status nfg_field_evaluate_device(nfg_field* f, const float* X, int64_t B, fl
         a.b = f->d_p + f->n_tab_dev + f->n_w;
         a.out = out;
         Span span(f->ctx, 3);
-        NFG_CUDA(nfg::launch_infer(f->shape, f->d_levels, nfg::SRC_ENCODE, a, f->ctx->num_sms, f->ctx->stream));
-        f->ctx->launches++;
+        if (f->fused_ok) {
+            NFG_CUDA(nfg::launch_infer(f->shape, f->d_levels, nfg::SRC_ENCODE, a, f->ctx->num_sms, f->ctx->stream));
+            f->ctx->launches++;
+        } else if (B > 0) {   // staged: encode into scratch, then the MLP
+            float* Y = static_cast<float*>(f->comp_y.get(size_t(B) * size_t(f->shape.in_real) * 4));
+            NFG_CUDA(nfg::launch_encode_fwd_lv(f->shape, f->d_levels, X, B, table_ptr(f), Y, nullptr, nullptr,
+                                               f->ctx->stream));
+            a.X = nullptr;
+            a.Y = Y;
+            NFG_CUDA(nfg::launch_infer(f->shape, nullptr, nfg::SRC_LOAD_Y, a, f->ctx->num_sms, f->ctx->stream));
+            f->ctx->launches += 2;
+        }
     });
 }
 

@@ -34,6 +34,19 @@ cudaError_t NFG_CAT(launch_fused_train_d, NFG_D)(const FieldShape& s, const Leve
     return cudaErrorNotSupported;
 }
 
+// Whether a fused instantiation exists for this shape (the field falls back to
+// the staged kernels otherwise).
+bool NFG_CAT(fused_supported_d, NFG_D)(const FieldShape& s)
+{
+    const bool f32 = s.table_fp32 != 0;
+#define X(F_, TT_, IS_, NH_)                                                                               \
+    if (s.grid.F == F_ && f32 == (sizeof(TT_) == 4) && s.in_steps == IS_ && s.hidden_layers == NH_)         \
+        return true;
+    NFG_FUSED_LIST(X)
+#undef X
+    return false;
+}
+
 // Fused backward with an external dLoss/dOutput (nfg_field_backward_device:
 // the NeRF density network, 3D, L*F = 32, 1 or 2 hidden layers).
 cudaError_t NFG_CAT(launch_fused_dout_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,

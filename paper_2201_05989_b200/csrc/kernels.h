@@ -123,6 +123,8 @@ cudaError_t launch_encode_bwd_det(const FieldShape& s, const LevelDev* lv, const
 cudaError_t launch_reduce_partials(const float* part, int nparts, int64_t n, float* out, const double* part_loss,
                                    int nloss, double* loss_sum, const unsigned int* flags, cudaStream_t st);
 int train_warps_per_cta();
+bool fused_supported(const FieldShape& s);    // fused encode+MLP kernels built for this shape
+bool staged_supported(const FieldShape& s);   // staged MLP kernels built for this shape
 cudaError_t launch_loss_out(const double* loss_sum, const unsigned int* flags, double count, float* out,
                             cudaStream_t st);
 cudaError_t launch_loss(int kind, const float* pred, const float* target, int64_t n, float count, float* dpred,

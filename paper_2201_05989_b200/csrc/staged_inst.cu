@@ -58,6 +58,24 @@ cudaError_t launch_train(const FieldShape& s, const LevelDev* lv, int src, int g
 
 int train_warps_per_cta() { return TW; }
 
+bool fused_supported_d2(const FieldShape&);
+bool fused_supported_d3(const FieldShape&);
+
+bool fused_supported(const FieldShape& s)
+{
+    return s.grid.d == 2 ? fused_supported_d2(s) : fused_supported_d3(s);
+}
+
+bool staged_supported(const FieldShape& s)
+{
+#define X(IS_, NH_)                                                                                         \
+    if (s.in_steps == IS_ && s.hidden_layers == NH_)                                                         \
+        return true;
+    NFG_STAGED_LIST(X)
+#undef X
+    return false;
+}
+
 cudaError_t launch_infer(const FieldShape& s, const LevelDev* lv, int src, const InferArgs& a, int num_sms,
                          cudaStream_t st)
 {

@@ -404,3 +404,24 @@ def test_image_loss_curve_parity():   # loss curves, config-1 s
     # the chaotic middle of the run differs run to run; the end does not)
     assert abs(mse(rg[-1][2]) - mse(ro[-1][2])) <= 0.25 * mse(ro[-1][2]), (rg[-1], ro[-1])
     assert rg[-1][2] > 60.0 and ro[-1][2] > 60.0
+
+
+@pytest.mark.parametrize("levels,hidden", [(24, 2), (32, 1), (32, 3)])
+def test_wide_encodings_fall_back_to_staged_kernels(levels, hidden):   # L*F = 48 / 64: no fused instantiation
+    nf = _nf()
+    g = _grid(nf, dims=3, levels=levels, table_size=1 << 14, features=2, n_min=8, n_max=512)
+    m = _model(nf, g, hidden_layers=hidden, n_out=1, table_fp32=True, lr=1e-3)
+    f = O.Field(_ocfg(g), O.MlpCfg(hidden_layers=hidden, hidden_width=64, output_width=1), O.Hyper(lr=1e-3))
+    f.init(1337)
+    assert np.array_equal(m.params, f.params)
+    rng = O.Pcg32(8, 8)
+    for step in (1, 2):
+        X = rng.floats(2000 * 3).reshape(-1, 3)
+        T = O.csg_sdf(X).reshape(-1, 1)
+        lg = m.train_step(X, T, nf.LossKind.Mape, step)
+        lo = f.train_step(X, T, O.LOSS_MAPE, step)
+        assert abs(lg - lo) <= 1e-3 * abs(lo)
+    f.params[:] = m.params
+    Xq = rng.floats(500 * 3).reshape(-1, 3)
+    a, b = m.evaluate(Xq), f.evaluate(Xq)
+    assert np.abs(a - b).max() <= 5e-3 * np.abs(b).max() + 1e-5
