@@ -94,6 +94,34 @@ def spatial_hash(coords: Sequence[int], dims: int, table_size: int) -> int:   # 
     return int(L.load().nfg_spatial_hash(c, dims, table_size))
 
 
+def grid_vertex_index(spec: GridLevelSpec, coords: Sequence[int], dims: int, table_size: int) -> int:
+    """grid.hpp:100-110: row-major (first coordinate fastest, stride N+1) at dense
+    levels, the spatial hash otherwise."""
+    if spec.dense:
+        idx, stride = 0, 1
+        for i in range(dims):
+            idx += int(coords[i]) * stride
+            stride *= spec.resolution + 1
+        return idx & 0xFFFFFFFF
+    return spatial_hash(coords, dims, table_size)
+
+
+def psnr(a, b) -> float:   # losses.hpp:63-71 (host metric)
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.shape != b.shape:
+        raise L.NfgInvalidArgument(L.NFG_EINVAL, "psnr: shape mismatch")
+    mse = float(((a - b) ** 2).sum() / a.size) if a.size else 0.0
+    return 100.0 if mse <= 0 else min(100.0, -10.0 * np.log10(mse))
+
+
+def set_threads(n: int) -> None:   # tasks.cpp:17-25
+    """The reference caps OpenMP/Eigen threads (1 = deterministic mode). On the
+    GPU path the equivalent switch is Options(deterministic=True); this is a
+    no-op kept for API parity."""
+    del n
+
+
 @dataclass
 class MlpConfig:   # mlp.hpp:15-40
     input_width: int = 32

@@ -92,3 +92,21 @@ def test_context_fails_loudly_without_gpu():
     from paper_2201_05989_b200._lib import NfgError
     with pytest.raises(NfgError):
         nf.Context(0)
+
+
+def test_host_mirror_functions_match_oracle(kats):   # grid.hpp:100-110, losses.hpp:63-71
+    import numpy as np
+    import oracle as O
+    from paper_2201_05989_b200 import nf
+    cfg = nf.HashEncodingConfig(levels=6, table_size=1 << 10, features=2, n_min=4, n_max=64, dims=3)
+    specs = nf.level_resolutions(cfg)
+    ospecs = O.level_resolutions(O.GridCfg(levels=6, table_size=1 << 10, features=2, n_min=4, n_max=64, dims=3))
+    rng = np.random.default_rng(1)
+    for s, o in zip(specs, ospecs):
+        for _ in range(50):
+            c = rng.integers(0, s.resolution + 1, 3)
+            assert nf.grid_vertex_index(s, c, 3, 1 << 10) == O.grid_vertex_index(o.resolution, o.dense, c, 3, 1 << 10)
+    a = rng.uniform(size=(40, 3)).astype(np.float32)
+    b = rng.uniform(size=(40, 3)).astype(np.float32)
+    assert abs(nf.psnr(a, b) - O.psnr(a, b)) < 1e-9
+    assert nf.psnr(a, a) == 100.0
