@@ -1,0 +1,193 @@
+// lsu_bench.cu — the throughput ceiling of k_train's memory instructions.
+// k_train's table traffic is L2-resident (tables 32 MB fp16 + grads 64 MB fp32
+// at config 2), so HBM does not bound it. What bounds it is the per-SM rate of
+// DIVERGENT lane operations: every 4-byte corner gather and every v2/v4
+// gradient reduction goes to its own 32-byte sector. This tool measures that
+// rate at full occupancy on uniformly random L2-resident addresses:
+//   cp.async 4 B (k_train's gather), ld.global 4 B / 8 B (k_infer's),
+//   red.global.add.v2.f32 / .v4.f32 (k_train's scatter).
+// It reports ns per lane-op per SM, which tools/ncu counts turn into a bound.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/lsu_bench.cu -o tools/lsu_bench
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#define CK(x)                                                                                        \
+    do {                                                                                             \
+        cudaError_t e = (x);                                                                         \
+        if (e != cudaSuccess) {                                                                      \
+            std::printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__);      \
+            std::exit(1);                                                                            \
+        }                                                                                            \
+    } while (0)
+
+constexpr int TPB = 256;
+constexpr int UNROLL = 8;
+
+__device__ __forceinline__ uint32_t mix(uint32_t x)
+{
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+
+template <int OP>   // 0: cp.async 4 B, 1: ld 4 B, 2: ld 8 B, 3: red v2.f32, 4: red v4.f32,
+                    // 5: ld 4 B on even lanes only, 6: ld 4 B with lane pairs sharing a sector,
+                    // 7: red v2 on even lanes only, 8: red v2 with lane pairs sharing a sector,
+                    // 9: cp.async 8 B, 10: cp.async 16 B, 11: cp.async 4 B on even lanes only
+__global__ void __launch_bounds__(TPB) k_lsu(uint32_t* table, float* grads, uint32_t mask_words, int iters,
+                                             uint32_t* sink)
+{
+    __shared__ __align__(16) uint32_t stage[UNROLL][TPB * 4];
+    const uint32_t tid = blockIdx.x * TPB + threadIdx.x;
+    uint32_t acc = 0;
+    uint32_t s = mix(tid * 0x9E3779B9u + 1u);
+    for (int it = 0; it < iters; ++it) {
+        uint32_t a[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            s = mix(s + u);
+            a[u] = s & mask_words;
+        }
+        if constexpr (OP == 0) {
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint32_t dst = uint32_t(__cvta_generic_to_shared(&stage[u][threadIdx.x]));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(table + a[u]) : "memory");
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u)
+                acc += stage[u][threadIdx.x];
+        } else if constexpr (OP == 9 || OP == 10 || OP == 11) {
+            constexpr int SZ = OP == 9 ? 8 : OP == 10 ? 16 : 4;
+            if (OP != 11 || (threadIdx.x & 1) == 0) {
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    const uint32_t dst = uint32_t(__cvta_generic_to_shared(&stage[u][threadIdx.x * (SZ / 4)]));
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst),
+                                 "l"(table + (a[u] & ~uint32_t(SZ / 4 - 1))), "n"(SZ)
+                                 : "memory");
+                }
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u)
+                acc += stage[u][threadIdx.x * (SZ / 4)];
+        } else if constexpr (OP == 1) {
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u)
+                acc += __ldg(table + a[u]);
+        } else if constexpr (OP == 2) {
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(table + (a[u] & ~1u)));
+                acc += v.x ^ v.y;
+            }
+        } else if constexpr (OP == 3) {
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                float* p = grads + ((a[u] << 1) & (2 * mask_words + 1) & ~1u);
+                asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(1.0f), "f"(2.0f) : "memory");
+            }
+        } else if constexpr (OP == 5) {
+            if ((threadIdx.x & 1) == 0) {
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u)
+                    acc += __ldg(table + a[u]);
+            }
+        } else if constexpr (OP == 6) {
+            const uint32_t other = threadIdx.x & 1;
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint32_t b = __shfl_sync(0xffffffffu, a[u], (threadIdx.x & 31) & ~1u);
+                acc += __ldg(table + ((b & ~1u) | other));
+            }
+        } else if constexpr (OP == 7) {
+            if ((threadIdx.x & 1) == 0) {
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    float* p = grads + ((a[u] << 1) & (2 * mask_words + 1) & ~1u);
+                    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(1.0f), "f"(2.0f) : "memory");
+                }
+            }
+        } else if constexpr (OP == 8) {
+            const uint32_t other = threadIdx.x & 1;
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint32_t b = __shfl_sync(0xffffffffu, a[u], (threadIdx.x & 31) & ~1u);
+                float* p = grads + ((((b << 1) & (2 * mask_words + 1)) & ~3u) | (other << 1));
+                asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(1.0f), "f"(2.0f) : "memory");
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                float* p = grads + ((a[u] << 1) & (2 * mask_words + 1) & ~3u);
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(1.0f), "f"(2.0f),
+                             "f"(3.0f), "f"(4.0f)
+                             : "memory");
+            }
+        }
+    }
+    if (acc == 0x12345678u)
+        sink[0] = acc;
+}
+
+int main(int argc, char** argv)
+{
+    const int iters = argc > 1 ? std::atoi(argv[1]) : 64;
+    int sms = 0, clk_khz = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
+    const uint32_t words = 1u << 23;   // 32 MB table of 4-byte entries (config 2: 2^19 x 16 levels x fp16x2)
+    uint32_t *table, *sink;
+    float* grads;                      // 64 MB fp32 grads (2 floats per entry)
+    CK(cudaMalloc(&table, size_t(words) * 4));
+    CK(cudaMalloc(&grads, size_t(words) * 8));
+    CK(cudaMalloc(&sink, 4));
+    CK(cudaMemset(table, 1, size_t(words) * 4));
+    CK(cudaMemset(grads, 0, size_t(words) * 8));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const char* names[12] = { "cp.async 4B gather", "ld.global 4B gather", "ld.global 8B gather", "red.v2.f32 scatter",
+                             "red.v4.f32 scatter", "ld 4B, even lanes", "ld 4B, lane pairs/sector",
+                             "red.v2, even lanes", "red.v2, lane pairs/16B", "cp.async 8B", "cp.async 16B",
+                             "cp.async 4B, even lanes" };
+    auto run = [&](int op, auto kern) {
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TPB, 0));
+        const int grid = sms * occ;
+        kern<<<grid, TPB>>>(table, grads, words - 1, 4, sink);   // warm L2
+        CK(cudaDeviceSynchronize());
+        cudaEventRecord(e0);
+        kern<<<grid, TPB>>>(table, grads, words - 1, iters, sink);
+        cudaEventRecord(e1);
+        CK(cudaDeviceSynchronize());
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double ops = double(grid) * TPB * iters * UNROLL;
+        const double ns_per_op_sm = ms * 1e6 / (ops / sms);
+        std::printf("%-22s %2d CTAs/SM: %7.3f ms, %.3g lane-ops/s, %.3f ns per lane-op per SM (%.2f cycles at %d MHz "
+                    "nominal)\n",
+                    names[op], occ, ms, ops / (ms * 1e-3), ns_per_op_sm, ns_per_op_sm * clk_khz * 1e-6, clk_khz / 1000);
+    };
+    run(0, k_lsu<0>);
+    run(1, k_lsu<1>);
+    run(2, k_lsu<2>);
+    run(3, k_lsu<3>);
+    run(4, k_lsu<4>);
+    run(5, k_lsu<5>);
+    run(6, k_lsu<6>);
+    run(7, k_lsu<7>);
+    run(8, k_lsu<8>);
+    run(9, k_lsu<9>);
+    run(10, k_lsu<10>);
+    run(11, k_lsu<11>);
+    return 0;
+}
