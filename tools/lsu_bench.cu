@@ -39,11 +39,12 @@ __device__ __forceinline__ uint32_t mix(uint32_t x)
 template <int OP>   // 0: cp.async 4 B, 1: ld 4 B, 2: ld 8 B, 3: red v2.f32, 4: red v4.f32,
                     // 5: ld 4 B on even lanes only, 6: ld 4 B with lane pairs sharing a sector,
                     // 7: red v2 on even lanes only, 8: red v2 with lane pairs sharing a sector,
-                    // 9: cp.async 8 B, 10: cp.async 16 B, 11: cp.async 4 B on even lanes only
+                    // 9: cp.async 8 B, 10: cp.async 16 B, 11: cp.async 4 B on even lanes only,
+                    // 12: ld 16 B, 13: ld 32 B (LDG.256)
 __global__ void __launch_bounds__(TPB) k_lsu(uint32_t* table, float* grads, uint32_t mask_words, int iters,
                                              uint32_t* sink)
 {
-    __shared__ __align__(16) uint32_t stage[UNROLL][TPB * 4];
+    extern __shared__ __align__(16) uint32_t stage_raw[];   // cp.async variants: UNROLL x TPB x (SZ/4) words
     const uint32_t tid = blockIdx.x * TPB + threadIdx.x;
     uint32_t acc = 0;
     uint32_t s = mix(tid * 0x9E3779B9u + 1u);
@@ -57,19 +58,19 @@ __global__ void __launch_bounds__(TPB) k_lsu(uint32_t* table, float* grads, uint
         if constexpr (OP == 0) {
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {
-                const uint32_t dst = uint32_t(__cvta_generic_to_shared(&stage[u][threadIdx.x]));
+                const uint32_t dst = uint32_t(__cvta_generic_to_shared(&stage_raw[u * TPB + threadIdx.x]));
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(table + a[u]) : "memory");
             }
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u)
-                acc += stage[u][threadIdx.x];
+                acc += stage_raw[u * TPB + threadIdx.x];
         } else if constexpr (OP == 9 || OP == 10 || OP == 11) {
             constexpr int SZ = OP == 9 ? 8 : OP == 10 ? 16 : 4;
             if (OP != 11 || (threadIdx.x & 1) == 0) {
 #pragma unroll
                 for (int u = 0; u < UNROLL; ++u) {
-                    const uint32_t dst = uint32_t(__cvta_generic_to_shared(&stage[u][threadIdx.x * (SZ / 4)]));
+                    const uint32_t dst = uint32_t(__cvta_generic_to_shared(&stage_raw[(u * TPB + threadIdx.x) * (SZ / 4)]));
                     asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst),
                                  "l"(table + (a[u] & ~uint32_t(SZ / 4 - 1))), "n"(SZ)
                                  : "memory");
@@ -78,7 +79,23 @@ __global__ void __launch_bounds__(TPB) k_lsu(uint32_t* table, float* grads, uint
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u)
-                acc += stage[u][threadIdx.x * (SZ / 4)];
+                acc += stage_raw[(u * TPB + threadIdx.x) * (SZ / 4)];
+        } else if constexpr (OP == 12) {
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(table + (a[u] & ~3u)));
+                acc += v.x ^ v.y ^ v.z ^ v.w;
+            }
+        } else if constexpr (OP == 13) {
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                uint32_t r[8];
+                asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                               "=r"(r[7])
+                             : "l"(table + (a[u] & ~7u)));
+                acc += r[0] ^ r[1] ^ r[2] ^ r[3] ^ r[4] ^ r[5] ^ r[6] ^ r[7];
+            }
         } else if constexpr (OP == 1) {
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u)
@@ -155,18 +172,20 @@ int main(int argc, char** argv)
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const char* names[12] = { "cp.async 4B gather", "ld.global 4B gather", "ld.global 8B gather", "red.v2.f32 scatter",
+    const char* names[14] = { "cp.async 4B gather", "ld.global 4B gather", "ld.global 8B gather", "red.v2.f32 scatter",
                              "red.v4.f32 scatter", "ld 4B, even lanes", "ld 4B, lane pairs/sector",
                              "red.v2, even lanes", "red.v2, lane pairs/16B", "cp.async 8B", "cp.async 16B",
-                             "cp.async 4B, even lanes" };
+                             "cp.async 4B, even lanes", "ld.global 16B gather", "ld.global 32B gather" };
     auto run = [&](int op, auto kern) {
+        const int sz = op == 0 || op == 11 ? 4 : op == 9 ? 8 : op == 10 ? 16 : 0;
+        const int smem = UNROLL * TPB * sz;
         int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TPB, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TPB, smem));
         const int grid = sms * occ;
-        kern<<<grid, TPB>>>(table, grads, words - 1, 4, sink);   // warm L2
+        kern<<<grid, TPB, smem>>>(table, grads, words - 1, 4, sink);   // warm L2
         CK(cudaDeviceSynchronize());
         cudaEventRecord(e0);
-        kern<<<grid, TPB>>>(table, grads, words - 1, iters, sink);
+        kern<<<grid, TPB, smem>>>(table, grads, words - 1, iters, sink);
         cudaEventRecord(e1);
         CK(cudaDeviceSynchronize());
         float ms = 0;
@@ -189,5 +208,7 @@ int main(int argc, char** argv)
     run(9, k_lsu<9>);
     run(10, k_lsu<10>);
     run(11, k_lsu<11>);
+    run(12, k_lsu<12>);
+    run(13, k_lsu<13>);
     return 0;
 }
