@@ -212,6 +212,70 @@ __device__ __forceinline__ float2 gather_blend(const GridDev& g, const LevelDev*
     return acc;
 }
 
+// ---- lane-pair gathers and reductions (F == 2) -----------------------------
+// In the mma fragment layout lanes 2i and 2i+1 own levels l and l+1 (l even)
+// of the same two samples. Per (sample, level) of such a pair, the even lane
+// handles the corners with x-offset 0 and the odd lane those with x-offset 1,
+// so both corners of every x-adjacent pair sit in the SAME warp instruction
+// and the L1 merges them when they share a 32-byte sector: 7/8 of pairs for
+// fp16 rows, 3/4 for fp32 gradient rows (pi_1 = 1: hashed rows of x and x+1
+// differ in the low bits only; dense rows are consecutive). A divergent L1
+// access costs per distinct sector (profiles/lsu_r1.md), so this cuts the
+// gather sectors per sample from 128 to ~72 and the reductions from ~98 to ~80.
+template <int D>
+struct LanePair {
+    static constexpr int HC = (1 << D) / 2;   // corners per lane and (sample, level)
+};
+
+// Issue this lane's half of the corner loads of levels (l & ~1) and (l | 1):
+// slot k0 + q*HC + m holds corner 2m + par of level (l & ~1) + q.
+template <int D, int F, typename TT, class Slots>
+__device__ __forceinline__ void gather_issue_lp(const GridDev& g, const LevelDev* lvs, const float* x, int col,
+                                                const TT* __restrict__ table, const Slots& slots, int k0)
+{
+    static_assert(F == 2, "lane pairs map one level per lane");
+    constexpr int SB = Stage<F, TT>::SB, HC = LanePair<D>::HC;
+    const int par = (col / F) & 1, lb = (col / F) & ~1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        if (lb + q >= g.L)
+            continue;
+        const LevelDev lv = lvs[lb + q];
+        const CornerSet<D> cs = corners_of<D>(g, lv, x);
+#pragma unroll
+        for (int m = 0; m < HC; ++m)
+            cp_async<SB>(slots.ptr(k0 + q * HC + m), table + (size_t(lv.row_off) + cs.row(2 * m + par)) * F);
+    }
+}
+
+// Blend of this lane's own level: corners of its parity from its own slots,
+// the others from the partner lane's (same warp; call after the copies have
+// completed on both lanes and a __syncwarp). Same summation order as
+// gather_blend.
+template <int D, int F, typename TT, class Slots>
+__device__ __forceinline__ float2 gather_blend_lp(const GridDev& g, const LevelDev* lvs, const float* x, int col,
+                                                  const Slots& slots, int k0)
+{
+    constexpr int SB = Stage<F, TT>::SB, HC = LanePair<D>::HC;
+    const int l = col / F, par = l & 1;
+    if (l >= g.L)
+        return make_float2(0.0f, 0.0f);
+    const LevelDev lv = lvs[l];
+    const CornerSet<D> cs = corners_of<D>(g, lv, x);
+    const int pdelta = par ? -SB : SB;
+    float a = 0.0f, b = 0.0f;
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        const unsigned char* s = slots.ptr(k0 + par * HC + c / 2) + ((c & 1) == par ? 0 : pdelta);
+        const float w = cs.weight(c);
+        const float2 v = sizeof(TT) == 2 ? unpack_half2(*reinterpret_cast<const uint32_t*>(s))
+                                         : *reinterpret_cast<const float2*>(s);
+        a = fmaf(w, v.x, a);
+        b = fmaf(w, v.y, b);
+    }
+    return make_float2(a, b);
+}
+
 __device__ __forceinline__ void red_add2(float* p, float a, float b)
 {
     // vector reduction to global memory (sm_90+): one L2 atomic for both features
@@ -273,6 +337,32 @@ __device__ __forceinline__ void scatter_pair(const GridDev& g, const LevelDev* l
     for (int c = 0; c < (1 << D); ++c) {
         const float w = cs.weight(c);
         red_add2(base + size_t(cs.row(c)) * F, w * dy.x, w * dy.y);
+    }
+}
+
+// Lane-pair backward (F == 2): this lane's corner half of levels (l & ~1) and
+// (l | 1) of one sample; dy_own is this lane's level gradient, dy_partner the
+// partner lane's (exchanged by the caller with __shfl_xor_sync(.., 1)).
+template <int D>
+__device__ __forceinline__ void scatter_pair_lp(const GridDev& g, const LevelDev* lvs, const float* x, int col,
+                                                float2 dy_own, float2 dy_partner, float* __restrict__ grads)
+{
+    constexpr int F = 2, HC = LanePair<D>::HC;
+    const int par = (col / F) & 1, lb = (col / F) & ~1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        if (lb + q >= g.L)
+            continue;
+        const LevelDev lv = lvs[lb + q];
+        const CornerSet<D> cs = corners_of<D>(g, lv, x);
+        const float2 dy = q == par ? dy_own : dy_partner;
+        float* base = grads + size_t(lv.row_off) * F;
+#pragma unroll
+        for (int m = 0; m < HC; ++m) {
+            const int c = 2 * m + par;
+            const float w = cs.weight(c);
+            red_add2(base + size_t(cs.row(c)) * F, w * dy.x, w * dy.y);
+        }
     }
 }
 

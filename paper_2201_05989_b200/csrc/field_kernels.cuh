@@ -201,6 +201,12 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     float* red = reinterpret_cast<float*>(sm + SM::RED_OFF);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    // lane-pair gathers / reductions (encode.cuh): one level per lane (F == 2)
+#ifdef NFG_NO_LANE_PAIRS
+    constexpr bool LPG = false, LPS = false;
+#else
+    constexpr bool LPG = SRC == SRC_ENCODE && F == 2, LPS = SINK == SINK_SCATTER && F == 2;
+#endif
     if (a.scratch.flags[3] != 0u)
         return;   // invalid input (k_validate): the reference throws before any update
     const MlpShape msh{ s.in_real, s.n_out, s.sigmoid };
@@ -290,10 +296,17 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             for (int h = 0; h < 2; ++h) {
                 const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
                 const int p = (sl * 2 + h) * 2;
-                if (s0 + sl < IN_STEPS && v)
-                    gather_issue<D, F, TT>(s.grid, lvs, x, col, tab, slots, p * SG::NE);
-                if (s0 + sl < IN_STEPS && v8)
-                    gather_issue<D, F, TT>(s.grid, lvs, x8, col, tab, slots, (p + 1) * SG::NE);
+                if constexpr (LPG) {
+                    if (s0 + sl < IN_STEPS && v)
+                        gather_issue_lp<D, F, TT>(s.grid, lvs, x, col, tab, slots, p * SG::NE);
+                    if (s0 + sl < IN_STEPS && v8)
+                        gather_issue_lp<D, F, TT>(s.grid, lvs, x8, col, tab, slots, (p + 1) * SG::NE);
+                } else {
+                    if (s0 + sl < IN_STEPS && v)
+                        gather_issue<D, F, TT>(s.grid, lvs, x, col, tab, slots, p * SG::NE);
+                    if (s0 + sl < IN_STEPS && v8)
+                        gather_issue<D, F, TT>(s.grid, lvs, x8, col, tab, slots, (p + 1) * SG::NE);
+                }
             }
     };
     auto blend_pass = [&](int s0, const auto& slots, const float* x, const float* x8, bool v, bool v8,
@@ -306,10 +319,18 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                     continue;
                 const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
                 const int p = (sl * 2 + h) * 2;
-                const float2 e0 = v ? gather_blend<D, F, TT>(s.grid, lvs, x, col, slots, p * SG::NE)
-                                    : make_float2(0.f, 0.f);
-                const float2 e8 = v8 ? gather_blend<D, F, TT>(s.grid, lvs, x8, col, slots, (p + 1) * SG::NE)
-                                     : make_float2(0.f, 0.f);
+                float2 e0 = make_float2(0.f, 0.f), e8 = make_float2(0.f, 0.f);
+                if constexpr (LPG) {
+                    if (v)
+                        e0 = gather_blend_lp<D, F, TT>(s.grid, lvs, x, col, slots, p * SG::NE);
+                    if (v8)
+                        e8 = gather_blend_lp<D, F, TT>(s.grid, lvs, x8, col, slots, (p + 1) * SG::NE);
+                } else {
+                    if (v)
+                        e0 = gather_blend<D, F, TT>(s.grid, lvs, x, col, slots, p * SG::NE);
+                    if (v8)
+                        e8 = gather_blend<D, F, TT>(s.grid, lvs, x8, col, slots, (p + 1) * SG::NE);
+                }
                 fr[s0 + sl][2 * h] = pack_half2(e0.x, e0.y);
                 fr[s0 + sl][2 * h + 1] = pack_half2(e8.x, e8.y);
             }
@@ -351,6 +372,8 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 for (int s0 = 0; s0 < IN_STEPS; s0 += SG::STS) {
                     issue_pass(s0, slots, xg, xg8, vg, vg8);
                     cp_async_wait_all();
+                    if (LPG)
+                        __syncwarp();   // the partner lane's copies landed too
                     blend_pass(s0, slots, xg, xg8, vg, vg8, afr);
                     if (SA::ON && s0 + SG::STS < IN_STEPS)
                         __syncwarp();   // next pass reuses the warp's rows
@@ -358,6 +381,8 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             };
             if constexpr (SA::PREFETCH) {
                 cp_async_wait_all();   // this tile's loads, issued during the previous tile
+                if (LPG)
+                    __syncwarp();
                 blend_pass(0, lin_slots, xg, xg8, vg, vg8, afr);
             } else if constexpr (SA::ON) {
                 SlotsChunked<SA::ROWS, HS * 2, 4> slots;
@@ -493,6 +518,17 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             const float2 d0 = make_float2(ay[j][0] * dysc, ay[j][1] * dysc);
             const float2 d8 = make_float2(ay[j][2] * dysc, ay[j][3] * dysc);
             bad |= !(sane(d0.x) && sane(d0.y) && sane(d8.x) && sane(d8.y));
+            if constexpr (LPS) {   // levels >= L (cols >= in_real) are skipped per level inside
+                const float2 p0 = make_float2(__shfl_xor_sync(0xffffffffu, d0.x, 1),
+                                              __shfl_xor_sync(0xffffffffu, d0.y, 1));
+                const float2 p8 = make_float2(__shfl_xor_sync(0xffffffffu, d8.x, 1),
+                                              __shfl_xor_sync(0xffffffffu, d8.y, 1));
+                if (vg)
+                    scatter_pair_lp<D>(s.grid, lvs, xg, col, d0, p0, a.table_grad);
+                if (vg8)
+                    scatter_pair_lp<D>(s.grid, lvs, xg8, col, d8, p8, a.table_grad);
+                continue;
+            }
             if (col >= s.in_real)
                 continue;
 #ifdef NFG_EXP_SKIP_LEVELS   // experiment builds only (tools/kbench.cu): drop coarse-level reductions

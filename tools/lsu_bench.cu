@@ -40,7 +40,10 @@ template <int OP>   // 0: cp.async 4 B, 1: ld 4 B, 2: ld 8 B, 3: red v2.f32, 4: 
                     // 5: ld 4 B on even lanes only, 6: ld 4 B with lane pairs sharing a sector,
                     // 7: red v2 on even lanes only, 8: red v2 with lane pairs sharing a sector,
                     // 9: cp.async 8 B, 10: cp.async 16 B, 11: cp.async 4 B on even lanes only,
-                    // 12: ld 16 B, 13: ld 32 B (LDG.256)
+                    // 12: ld 16 B, 13: ld 32 B (LDG.256),
+                    // 14: cp.async 4 B, lane pairs in one sector (adjacent words),
+                    // 15: red v2, lane pairs in one sector but different 16-byte halves,
+                    // 16: cp.async 4 B, lane pairs at the two ends of one sector
 __global__ void __launch_bounds__(TPB) k_lsu(uint32_t* table, float* grads, uint32_t mask_words, int iters,
                                              uint32_t* sink)
 {
@@ -80,6 +83,27 @@ __global__ void __launch_bounds__(TPB) k_lsu(uint32_t* table, float* grads, uint
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u)
                 acc += stage_raw[(u * TPB + threadIdx.x) * (SZ / 4)];
+        } else if constexpr (OP == 14 || OP == 16) {
+            const uint32_t other = threadIdx.x & 1;
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint32_t b = __shfl_sync(0xffffffffu, a[u], (threadIdx.x & 31) & ~1u);
+                const uint32_t wi = OP == 14 ? ((b & ~1u) | other) : ((b & ~7u) | (other * 7u));
+                const uint32_t dst = uint32_t(__cvta_generic_to_shared(&stage_raw[u * TPB + threadIdx.x]));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(table + wi) : "memory");
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u)
+                acc += stage_raw[u * TPB + threadIdx.x];
+        } else if constexpr (OP == 15) {
+            const uint32_t other = threadIdx.x & 1;
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint32_t b = __shfl_sync(0xffffffffu, a[u], (threadIdx.x & 31) & ~1u);
+                float* p = grads + ((((b << 1) & (2 * mask_words + 1)) & ~7u) | (other << 2));
+                asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(1.0f), "f"(2.0f) : "memory");
+            }
         } else if constexpr (OP == 12) {
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {
@@ -172,12 +196,13 @@ int main(int argc, char** argv)
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const char* names[14] = { "cp.async 4B gather", "ld.global 4B gather", "ld.global 8B gather", "red.v2.f32 scatter",
+    const char* names[17] = { "cp.async 4B gather", "ld.global 4B gather", "ld.global 8B gather", "red.v2.f32 scatter",
                              "red.v4.f32 scatter", "ld 4B, even lanes", "ld 4B, lane pairs/sector",
                              "red.v2, even lanes", "red.v2, lane pairs/16B", "cp.async 8B", "cp.async 16B",
-                             "cp.async 4B, even lanes", "ld.global 16B gather", "ld.global 32B gather" };
+                             "cp.async 4B, even lanes", "ld.global 16B gather", "ld.global 32B gather",
+                             "cp.async 4B, lane pairs/sector", "red.v2, lane pairs/sector", "cp.async 4B, pairs 28B apart" };
     auto run = [&](int op, auto kern) {
-        const int sz = op == 0 || op == 11 ? 4 : op == 9 ? 8 : op == 10 ? 16 : 0;
+        const int sz = op == 0 || op == 11 || op == 14 || op == 16 ? 4 : op == 9 ? 8 : op == 10 ? 16 : 0;
         const int smem = UNROLL * TPB * sz;
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TPB, smem));
@@ -210,5 +235,8 @@ int main(int argc, char** argv)
     run(11, k_lsu<11>);
     run(12, k_lsu<12>);
     run(13, k_lsu<13>);
+    run(14, k_lsu<14>);
+    run(15, k_lsu<15>);
+    run(16, k_lsu<16>);
     return 0;
 }
