@@ -227,6 +227,43 @@ struct LanePair {
     static constexpr int HC = (1 << D) / 2;   // corners per lane and (sample, level)
 };
 
+// Register-path lane-pair encode (k_infer): this lane gathers its x-parity
+// corners of both levels of the pair, blends them into two partial sums and
+// swaps the partner's partial with one shuffle. Every lane of the warp must
+// call it (invalid samples with x = 0 and the result discarded).
+template <int D, int F, typename TT>
+__device__ __forceinline__ float2 encode_pair_lp(const GridDev& g, const LevelDev* lvs, const float* x, int col,
+                                                 const TT* __restrict__ table)
+{
+    static_assert(F == 2, "lane pairs map one level per lane");
+    constexpr int HC = LanePair<D>::HC;
+    const int par = (col / F) & 1, lb = (col / F) & ~1;
+    float2 part[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        part[q] = make_float2(0.0f, 0.0f);
+        if (lb + q >= g.L)
+            continue;
+        const LevelDev lv = lvs[lb + q];
+        const CornerSet<D> cs = corners_of<D>(g, lv, x);
+        const TT* base = table + size_t(lv.row_off) * F;
+        float2 v[HC];
+#pragma unroll
+        for (int m = 0; m < HC; ++m)
+            v[m] = Gather<TT>::two(base + size_t(cs.row(2 * m + par)) * F);
+#pragma unroll
+        for (int m = 0; m < HC; ++m) {
+            const float w = cs.weight(2 * m + par);
+            part[q].x = fmaf(w, v[m].x, part[q].x);
+            part[q].y = fmaf(w, v[m].y, part[q].y);
+        }
+    }
+    const float2 give = par ? part[0] : part[1];   // the partner level's partial
+    const float2 got = make_float2(__shfl_xor_sync(0xffffffffu, give.x, 1), __shfl_xor_sync(0xffffffffu, give.y, 1));
+    const float2 own = par ? part[1] : part[0];
+    return make_float2(own.x + got.x, own.y + got.y);
+}
+
 // Issue this lane's half of the corner loads of levels (l & ~1) and (l | 1):
 // slot k0 + q*HC + m holds corner 2m + par of level (l & ~1) + q.
 template <int D, int F, typename TT, class Slots>

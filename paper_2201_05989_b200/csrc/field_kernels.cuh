@@ -146,10 +146,22 @@ __device__ __forceinline__ void input_frags(uint32_t (&afr)[IN_STEPS][4], const 
             float2 e0 = make_float2(0.f, 0.f), e8 = make_float2(0.f, 0.f);
             if (SRC == SRC_ENCODE) {
                 const TT* tab = static_cast<const TT*>(table);
-                if (vg)
-                    e0 = encode_pair<D, F, TT>(s.grid, lvs, xg, col, tab);
-                if (vg8)
-                    e8 = encode_pair<D, F, TT>(s.grid, lvs, xg8, col, tab);
+#ifndef NFG_NO_LANE_PAIRS
+                if constexpr (F == 2) {   // warp-uniform: invalid samples encode x = 0, discarded
+                    e0 = encode_pair_lp<D, F, TT>(s.grid, lvs, xg, col, tab);
+                    e8 = encode_pair_lp<D, F, TT>(s.grid, lvs, xg8, col, tab);
+                    if (!vg)
+                        e0 = make_float2(0.f, 0.f);
+                    if (!vg8)
+                        e8 = make_float2(0.f, 0.f);
+                } else
+#endif
+                {
+                    if (vg)
+                        e0 = encode_pair<D, F, TT>(s.grid, lvs, xg, col, tab);
+                    if (vg8)
+                        e8 = encode_pair<D, F, TT>(s.grid, lvs, xg8, col, tab);
+                }
             } else {
                 const int w = s.in_real;
                 if (vg) {
