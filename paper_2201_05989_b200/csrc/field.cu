@@ -216,7 +216,7 @@ struct nfg_field {
     nfg::FieldShape shape{};
     nfg::LevelDev* d_levels = nullptr;
     uint64_t n_tab = 0, n_w = 0, n_b = 0, n_total = 0, n_alloc = 0;   // reference (API) layout counts
-    uint64_t n_tab_dev = 0, n_total_dev = 0;   // device layout: each level starts on an even row
+    uint64_t n_tab_dev = 0, n_total_dev = 0;   // device layout: each level starts on an 8-row multiple
     std::vector<uint64_t> dev_row_off;        // per-level first row in the device layout
     float* d_p = nullptr;
     float* d_g = nullptr;
@@ -615,7 +615,7 @@ nfg::FieldShape make_shape(const nfg_grid_config& g, const nfg_mlp_config& m, co
 }
 
 // Copies a reference-layout range [off, off + n) of one flat buffer between the
-// host and the device layout (levels padded to even rows; see nfg_field_create).
+// host and the device layout (levels padded to 8-row multiples; see nfg_field_create).
 void copy_ref(nfg_field* f, float* dev, uint64_t off, uint64_t n, float* host, cudaMemcpyKind kind)
 {
     const uint64_t F = uint64_t(f->gcfg.features), end = off + n;
@@ -864,15 +864,18 @@ nfg_status nfg_field_create(nfg_ctx* ctx, const nfg_grid_config* grid, const nfg
             f->n_w = nw;
             f->n_b = nb;
             f->n_total = f->n_tab + nw + nb;
-            // Device layout: every level starts on an even row, so x-adjacent
-            // corner pairs {2k, 2k+1} are 16-byte aligned in the fp32 gradient
-            // slab (one vector reduction per pair). Padding rows carry zero
-            // gradients, which the skip-zero Adam group never touches.
+            // Device layout: every level starts on a multiple of 8 rows, so
+            // the relative row blocks of a level are the absolute 32-byte
+            // sectors of the fp16 tables (8 rows) and of the fp32 gradients (4
+            // rows): the lane-pair gathers / reductions merge x-adjacent
+            // corners per sector, and aligned pairs {2k, 2k+1} take one
+            // 16-byte vector reduction. Padding rows carry zero gradients,
+            // which the skip-zero Adam group never touches.
             uint64_t drow = 0;
             f->dev_row_off.clear();
             for (const auto& s : f->levels) {
                 f->dev_row_off.push_back(drow);
-                drow += (uint64_t(s.table_len) + 1u) & ~uint64_t(1);
+                drow += (uint64_t(s.table_len) + 7u) & ~uint64_t(7);
             }
             f->n_tab_dev = drow * uint64_t(f->gcfg.features);
             f->n_total_dev = f->n_tab_dev + nw + nb;
@@ -1008,7 +1011,7 @@ nfg_status nfg_field_device_buffer(nfg_field* f, int32_t which, float** dev, uin
 {
     return guard([&] {
         *dev = buffer_of(f, which);
-        *count = f->n_total_dev;   // device layout (levels start on even rows)
+        *count = f->n_total_dev;   // device layout (levels start on 8-row multiples)
     });
 }
 

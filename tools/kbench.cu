@@ -28,7 +28,11 @@ int main(int argc, char** argv)
     nfg_grid_config g{ 16, 1u << 19, 2, 16, 2048, 3, 0 };
     nfg_mlp_config m{ 32, 2, 64, 1, 0 };
     const auto lv = nfg::host::level_resolutions(g);
-    const uint64_t rows = lv.back().row_offset + lv.back().table_len;
+    // KB_EVEN=1: levels start on even rows; KB_ALIGN=a: on multiples of a rows (the library's device layout)
+    const uint32_t align = getenv("KB_ALIGN") ? uint32_t(std::atoi(getenv("KB_ALIGN"))) : (getenv("KB_EVEN") ? 2u : 1u);
+    uint64_t rows = 0;
+    for (const auto& e : lv)
+        rows += (e.table_len + align - 1) / align * align;
     const uint64_t n_tab = rows * 2, n_w = 64 * 32 + 64 * 64 + 64, n_b = 64 + 64 + 1;
 
     nfg::FieldShape s{};
@@ -43,15 +47,14 @@ int main(int argc, char** argv)
     s.n_out = 1;
     s.sigmoid = 0;
     s.table_fp32 = 0;
-    const bool even_off = getenv("KB_EVEN") != nullptr;   // pad level offsets to even rows
     uint64_t off = 0;
     for (int l = 0; l < 16; ++l) {
         s.grid.lv[l].res = lv[l].resolution;
         s.grid.lv[l].res_f = float(lv[l].resolution);
         s.grid.lv[l].stride = lv[l].resolution + 1;
         s.grid.lv[l].dense = lv[l].dense;
-        s.grid.lv[l].row_off = even_off ? uint32_t(off) : uint32_t(lv[l].row_offset);
-        off += (lv[l].table_len + 1) & ~1u;
+        s.grid.lv[l].row_off = uint32_t(off);
+        off += (lv[l].table_len + align - 1) / align * align;
         s.grid.lv[l].len = lv[l].table_len;
     }
 
