@@ -217,6 +217,11 @@ def bench_gigapixel(nf, ctx, steps, warmup, T_log2=24):
     m.check()
     torch.cuda.synchronize()
     ctx.synchronize()
+    import ctypes as C
+    prof = (C.c_double * 4)()
+    nst = C.c_int64()
+    ctx.lib.nfg_ctx_set_profiling(ctx.h, 1)
+    ctx.lib.nfg_ctx_read_profile(ctx.h, prof, C.byref(nst))   # reset
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(steps):
@@ -224,12 +229,15 @@ def bench_gigapixel(nf, ctx, steps, warmup, T_log2=24):
     e1.record(stream)
     ctx.synchronize()
     torch.cuda.synchronize()
+    ctx.lib.nfg_ctx_read_profile(ctx.h, prof, C.byref(nst))
+    ctx.lib.nfg_ctx_set_profiling(ctx.h, 0)
     m.check()
     ms = e0.elapsed_time(e1) / steps
     n = m.parameter_count()
     m.close()
     return {"metric": "gigapixel-image training samples/s (config 3, one GPU)", "value": B_TRAIN / (ms / 1000.0),
             "unit": "samples/s", "ms_per_step": ms, "params": n, "steps": steps, "warmup": warmup,
+            "phases_ms_per_step": {"train_kernel": prof[0] / steps, "adam": prof[1] / steps},
             "config": f"2D hash L16 F2 T2^{T_log2} Nmin16 Nmax8192, MLP 32-64-64-3 sigmoid, L2, batch 2^18 random "
                       "points of the procedural image (helpers.hpp:99-125) evaluated on the fly"}
 

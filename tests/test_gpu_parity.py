@@ -159,9 +159,15 @@ def test_loss_gradients_bit_exact(kind):   # losses.hpp:10-59
     assert abs(loss - lo) <= 1e-5 * abs(lo)
 
 
-def test_adam_bit_exact_and_skip_zero():   # adam.hpp:78-122, SPEC decisions on skip-zero
+ADAM_GRIDS = [dict(dims=2, levels=4, table_size=1 << 8, features=2, n_min=4, n_max=32),
+              # >= 2^20 parameters and a sparse step: the scan + list passes (aux_kernels.cu)
+              dict(dims=3, levels=16, table_size=1 << 17, features=2, n_min=16, n_max=2048)]
+
+
+@pytest.mark.parametrize("gk", ADAM_GRIDS)
+def test_adam_bit_exact_and_skip_zero(gk):   # adam.hpp:78-122, SPEC decisions on skip-zero
     nf = _nf()
-    g = _grid(nf, dims=2, levels=4, table_size=1 << 8, features=2, n_min=4, n_max=32)
+    g = _grid(nf, **gk)
     m = _model(nf, g, hidden_layers=1)
     f = _oracle_field(m)
     n = m.parameter_count()
@@ -193,10 +199,11 @@ def f_lib_adam(f, lr_now):
     f.step = st.step
 
 
-def test_adam_nonfinite_names_group():   # adam.hpp:86-90; state untouched
+@pytest.mark.parametrize("gk", ADAM_GRIDS)
+def test_adam_nonfinite_names_group(gk):   # adam.hpp:86-90; state untouched
     nf = _nf()
     from paper_2201_05989_b200._lib import NfgNonFinite
-    g = _grid(nf, dims=2, levels=4, table_size=1 << 8, features=2, n_min=4, n_max=32)
+    g = _grid(nf, **gk)
     m = _model(nf, g, hidden_layers=1)
     before = m.params
     grads = np.zeros(m.parameter_count(), np.float32)
