@@ -32,7 +32,10 @@ using namespace mlp;
 constexpr int TW = NFG_TW;          // warps per training CTA
 constexpr int TS = 16 * NFG_TW;     // samples per training tile (16 per warp)
 #ifndef NFG_IW
-#define NFG_IW 32   // 2 CTAs of 32 warps per SM: 2 copies of the weights instead of 8 leave more L1 to the gathers (+6%)
+// One CTA of 24 warps per SM: one copy of the weights leaves the L1 to the
+// gathers (+6% over 8 CTAs x 4 warps), and with lane-pair gathers 24 warps at
+// 76 registers beat 32 warps at the 64-register cap (+2%, tools/exp_iw.sh).
+#define NFG_IW 24
 #endif
 constexpr int IW = NFG_IW;   // warps per inference CTA
 
