@@ -1,13 +1,16 @@
 // field_kernels.cuh — the fused training and inference kernels (templates).
 //
-// k_train: one persistent CTA of 8 warps loops over 128-sample tiles. Per tile:
-//   encode fwd (grid.hpp:245-271)   straight into mma A fragments (+ smem copy)
+// k_train: persistent, two CTAs of 4 warps per SM loop over 64-sample tiles.
+// Per tile:
+//   encode fwd (grid.hpp:245-271)   cp.async corner gathers split over lane
+//                                   pairs (encode.cuh), blended straight into
+//                                   mma A fragments (+ smem copy)
 //   MLP fwd (mlp.hpp:113-123)       activations in registers, smem copy for dW
 //   loss + dPred (losses.hpp)       fused in the output epilogue
 //   MLP bwd (mlp.hpp:146-157)       dz chain in registers, dz copies in smem
 //   encode bwd (grid.hpp:286-294)   straight out of the dY C fragments as
 //                                   float2 vector reductions into fp32 grads
-//   dW/db                           K = 128-sample MMA from smem, accumulated in
+//   dW/db                           K = 64-sample MMA from smem, accumulated in
 //                                   registers across all tiles of the CTA and
 //                                   flushed once per CTA.
 // Backward operands are fp16 with a per-tile power-of-two scale (chosen from
