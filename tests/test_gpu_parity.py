@@ -287,6 +287,9 @@ def test_invalid_and_unsupported():   # grid.hpp:224-229, NFG_EUNSUPPORTED
     (dict(dims=3, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=512), 1, 1, False),
     (dict(dims=2, levels=16, table_size=1 << 12, features=2, n_min=16, n_max=256), 0, 3, True),
     (dict(dims=3, levels=16, table_size=1 << 12, features=2, n_min=8, n_max=128, interpolation=1), 2, 1, False),
+    # odd level counts: the last lane pair has one level past L (lane-pair gathers / reductions)
+    (dict(dims=3, levels=15, table_size=1 << 13, features=2, n_min=16, n_max=512), 1, 1, False),
+    (dict(dims=2, levels=11, table_size=1 << 12, features=2, n_min=8, n_max=256), 0, 3, True),
 ])
 def test_train_step_parity(case, kind, n_out, sig, fused):   # model.cpp:111-138
     """Gradients of one step vs the oracle composition, then 3 full steps:
@@ -368,11 +371,12 @@ def test_full_size_config2_properties():   # BASELINE config 2 at full size (B =
     assert loss2 < loss
 
 
+@pytest.mark.parametrize("levels", [16, 15])   # 15: the last lane pair has one level past L
 @pytest.mark.parametrize("fp32", [True, False])
-def test_evaluate_parity(fp32):   # model.cpp:102-109 (fused encode + MLP inference)
+def test_evaluate_parity(fp32, levels):   # model.cpp:102-109 (fused encode + MLP inference)
     nf = _nf()
-    g = _grid(nf, dims=3, levels=16, table_size=1 << 19, features=2, n_min=16, n_max=2048)
-    m = _model(nf, g, n_out=1)
+    g = _grid(nf, dims=3, levels=levels, table_size=1 << 19, features=2, n_min=16, n_max=2048)
+    m = _model(nf, g, n_out=1, table_fp32=fp32)
     f = _oracle_field(m)
     # train a few steps so the tables are not ~1e-4 noise
     rng = O.Pcg32(2, 2)
