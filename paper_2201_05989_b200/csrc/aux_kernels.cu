@@ -245,6 +245,42 @@ __device__ __forceinline__ void st4_hint(float* p, float4 v, uint64_t pol)
                  : "memory");
 }
 
+// One full quad [i0, i0 + 4): the update of adam.hpp:78-122 per element, then
+// p/m/v streamed back (unchanged values for skipped elements), the gradient
+// zeroed for the next step and the fp16 table shadow refreshed (both kept in L2).
+__device__ __forceinline__ void adam_quad(const AdamArgs& a, uint64_t i0, float4 G, float4 P, float4 M, float4 V,
+                                          uint64_t pol_stream, uint64_t pol_keep)
+{
+    const bool any = G.x != 0.0f || G.y != 0.0f || G.z != 0.0f || G.w != 0.0f;
+    float pg[4] = { P.x, P.y, P.z, P.w }, gq[4] = { G.x, G.y, G.z, G.w };
+    float mq[4] = { M.x, M.y, M.z, M.w }, vq[4] = { V.x, V.y, V.z, V.w };
+    bool w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        adam_one(a, i0 + e, pg[e], gq[e], mq[e], vq[e], w[e]);
+    st4_hint(a.p + i0, make_float4(pg[0], pg[1], pg[2], pg[3]), pol_stream);
+    st4_hint(a.m + i0, make_float4(mq[0], mq[1], mq[2], mq[3]), pol_stream);
+    st4_hint(a.v + i0, make_float4(vq[0], vq[1], vq[2], vq[3]), pol_stream);
+    if (any)
+        st4_hint(a.g + i0, make_float4(0.f, 0.f, 0.f, 0.f), pol_keep);
+    if (a.shadow && i0 < a.n_tab) {
+        if (i0 + 3 < a.n_tab && w[0] && w[1] && w[2] && w[3]) {
+            const uint2 h = make_uint2(pack_half2(pg[0], pg[1]), pack_half2(pg[2], pg[3]));
+            asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(a.shadow + i0), "r"(h.x),
+                         "r"(h.y), "l"(pol_keep)
+                         : "memory");
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (w[e] && i0 + e < a.n_tab)
+                    a.shadow[i0 + e] = __float2half_rn(pg[e]);
+        }
+    }
+}
+
+#ifndef NFG_ADAM_QUAD_GROUP
+#define NFG_ADAM_QUAD_GROUP 2   // quads per thread on sparse steps (tools/exp_adam_sp.sh)
+#endif
 __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
 {
     if (a.flags[1] != 0u)
@@ -262,6 +298,50 @@ __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
     uint64_t pol_stream, pol_keep;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    if (!a.eager && a.mode == 0) {
+        // Sparse steps: a thread owns QG consecutive quads (QG * 16 bytes of
+        // each stream). When any of them has a gradient it reads and writes
+        // them all, so p/m/v move in whole sectors (untouched neighbours are
+        // written back unchanged) instead of isolated 16-byte pieces.
+        constexpr int QG = NFG_ADAM_QUAD_GROUP;
+        const uint64_t ng = n / (4 * QG);
+        for (uint64_t o = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < ng; o += stride) {
+            const uint64_t i0 = 4 * QG * o;
+            float4 G[QG];
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < QG; ++k) {
+                G[k] = ld4_hint(a.g + i0 + 4 * k, pol_stream);
+                any |= G[k].x != 0.0f || G[k].y != 0.0f || G[k].z != 0.0f || G[k].w != 0.0f;
+            }
+            if (!any && i0 + 4 * QG - 1 < a.n_tab)
+                continue;
+            float4 P[QG], M[QG], V[QG];
+#pragma unroll
+            for (int k = 0; k < QG; ++k) {
+                P[k] = ld4_hint(a.p + i0 + 4 * k, pol_stream);
+                M[k] = ld4_hint(a.m + i0 + 4 * k, pol_stream);
+                V[k] = ld4_hint(a.v + i0 + 4 * k, pol_stream);
+            }
+#pragma unroll
+            for (int k = 0; k < QG; ++k)
+                adam_quad(a, i0 + 4 * k, G[k], P[k], M[k], V[k], pol_stream, pol_keep);
+        }
+        for (uint64_t i = 4 * QG * ng + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+            float p = a.p[i], g = a.g[i], m = a.m[i], v = a.v[i];
+            bool w;
+            adam_one(a, i, p, g, m, v, w);
+            if (w) {
+                a.p[i] = p;
+                a.m[i] = m;
+                a.v[i] = v;
+                if (a.shadow && i < a.n_tab)
+                    a.shadow[i] = __float2half_rn(p);
+            }
+            a.g[i] = 0.0f;
+        }
+        return;
+    }
     for (uint64_t q = q0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride) {
         const uint64_t i0 = 4 * q;
         float4 G, P, M, V;
@@ -283,30 +363,7 @@ __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
             M = ld4_hint(a.m + 4 * q, pol_stream);
             V = ld4_hint(a.v + 4 * q, pol_stream);
         }
-        float pg[4] = { P.x, P.y, P.z, P.w }, gq[4] = { G.x, G.y, G.z, G.w };
-        float mq[4] = { M.x, M.y, M.z, M.w }, vq[4] = { V.x, V.y, V.z, V.w };
-        bool w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            adam_one(a, i0 + e, pg[e], gq[e], mq[e], vq[e], w[e]);
-        st4_hint(a.p + 4 * q, make_float4(pg[0], pg[1], pg[2], pg[3]), pol_stream);
-        st4_hint(a.m + 4 * q, make_float4(mq[0], mq[1], mq[2], mq[3]), pol_stream);
-        st4_hint(a.v + 4 * q, make_float4(vq[0], vq[1], vq[2], vq[3]), pol_stream);
-        if (any)
-            st4_hint(a.g + 4 * q, make_float4(0.f, 0.f, 0.f, 0.f), pol_keep);
-        if (a.shadow && i0 < a.n_tab) {
-            if (i0 + 3 < a.n_tab && w[0] && w[1] && w[2] && w[3]) {
-                const uint2 h = make_uint2(pack_half2(pg[0], pg[1]), pack_half2(pg[2], pg[3]));
-                asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(a.shadow + i0), "r"(h.x),
-                             "r"(h.y), "l"(pol_keep)
-                             : "memory");
-            } else {
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (w[e] && i0 + e < a.n_tab)
-                        a.shadow[i0 + e] = __float2half_rn(pg[e]);
-            }
-        }
+        adam_quad(a, i0, G, P, M, V, pol_stream, pol_keep);
     }
     // tail
     for (uint64_t i = 4 * n4 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
