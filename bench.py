@@ -31,6 +31,12 @@ WORKLOAD = "config2: 3D SDF hash L16 F2 T2^19 Nmin16 Nmax2048, MLP 32-64-64-1 Re
 
 # algorithmic work per unit
 ADAM_BYTES_PER_PARAM = 34          # r: p g m v; w: p m v g(=0) + fp16 shadow
+# L1 sector model of k_train (profiles/lsu_r1.md, profiles/ncu_r1.json, final round-1 build)
+L1_GATHER_SECTORS_PER_SAMPLE = 71.9
+L2_RED_REQUESTS_PER_SAMPLE = 68.8
+LSU_CYC_PER_GATHER_SECTOR = 1.04
+LSU_CYC_PER_RED = 1.58
+N_SMS = 148
 ENC_FWD_L2_BYTES_PER_SAMPLE = 2304  # 72 sectors x 32 B (3D, fp16 rows)
 ENC_BWD_L2_BYTES_PER_SAMPLE = 2560  # 80 sectors x 32 B (fp32 F=2 rows, RED)
 MLP_TRAIN_FLOP_PER_SAMPLE = 37248
@@ -545,6 +551,18 @@ def main():
                         "CUDA-event kernel time; the kernel is L2-atomic/latency bound (tables+grads stay "
                         "L2-resident: traffic = DRAM bytes per launch from ncu), so the HBM copy peak is only "
                         "the nearest measured denominator"}
+        # The binding resource is the L1's per-sector cost of divergent accesses
+        # (profiles/lsu_r1.md): sectors per sample from ncu, SM cycles per sector
+        # from tools/lsu_bench.cu, converted at the measured SM clock.
+        mhz = clocks.get("sm_mhz") or 1965.0
+        model_us = ((L1_GATHER_SECTORS_PER_SAMPLE * LSU_CYC_PER_GATHER_SECTOR +
+                     L2_RED_REQUESTS_PER_SAMPLE * LSU_CYC_PER_RED) * B_TRAIN / N_SMS / mhz)
+        roof["l1_sector_model"] = {
+            "gather_sectors_per_sample": L1_GATHER_SECTORS_PER_SAMPLE, "red_requests_per_sample":
+            L2_RED_REQUESTS_PER_SAMPLE, "sm_cycles_per_gather_sector": LSU_CYC_PER_GATHER_SECTOR,
+            "sm_cycles_per_red": LSU_CYC_PER_RED, "bound_us": model_us, "kernel_us": train_ms * 1000.0,
+            "frac": model_us / (train_ms * 1000.0) if train_ms > 0 else None,
+            "source": "profiles/ncu_r1.json counts, profiles/lsu_r1.md per-sector costs"}
     else:
         dominant = "k_adam"
         roof = {"bound": "hbm", "kernel": dominant, "achieved": adam_gbs, "peak": hbm_peak, "unit": "GB/s",
