@@ -235,6 +235,11 @@ struct nfg_field {
     // the step scratch was already reset at the end of the previous synchronous
     // train_step (after its status was read), so the next step skips it
     bool scratch_ready = false;
+    // Streamed host-pointer steps start only after one plain step of this field
+    // has run: with CUDA's lazy module loading, the first launch of a kernel
+    // (Adam's) can block the host until the device idles, while the already
+    // running fused kernel waits for copies the host has not enqueued yet.
+    bool stream_warm = false;
     bool fused_ok = true;   // fused encode+MLP kernels exist for this shape
     unsigned int* d_ready = nullptr;   // NFG_MAX_CHUNKS chunk-ready flags
     unsigned int epoch = 0;
@@ -1048,8 +1053,8 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
         const int d = f->gcfg.dims, no = f->mcfg.output_width;
         const uint64_t before = f->step;
         const bool was_clean = f->grads_clean;
-        if (f->grads_clean && f->opts.fused_train && !f->opts.deterministic && c->write_value32 && B >= (int64_t(1) << 15) &&
-            !launches_serialized() && is_pinned(X) && is_pinned(target)) {
+        if (f->stream_warm && f->grads_clean && f->opts.fused_train && !f->opts.deterministic && c->write_value32 &&
+            B >= (int64_t(1) << 15) && !launches_serialized() && is_pinned(X) && is_pinned(target)) {
             // Overlap the H2D of the batch with the step: the fused kernel is
             // launched first and waits per tile for its chunk's ready flag,
             // which the copy stream writes (cuStreamWriteValue32) after each
@@ -1107,6 +1112,7 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
             raise_if_aborted(f);
         }
         f->grads_clean = true;   // Adam zeroed every gradient (adam.hpp:118-120)
+        f->stream_warm = true;   // every kernel of the step is loaded now
         const double count = double(B) * c->nranks * no;
         if (loss)
             *loss = count > 0 ? float(f->h_res->loss_sum / count) : 0.0f;

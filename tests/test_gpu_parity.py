@@ -264,6 +264,78 @@ def test_streamed_batch_invalid_tail_and_parity():
         assert abs(lg - lo) <= 1e-3 * abs(lo), (step, lg, lo)
 
 
+_FIRST_STREAMED = """
+import sys, numpy as np
+sys.path[:0] = [{root!r}]
+from paper_2201_05989_b200 import nf
+m = nf.FieldModel()
+m.hash_cfg = nf.HashEncodingConfig(dims=3, levels=16, table_size=1 << 19, features=2, n_min=16, n_max=2048)
+m.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=1)
+m.init(1)
+B = 1 << 15
+X, T = nf.PinnedBuffer((B, 3)), nf.PinnedBuffer((B, 1))
+X.array[:] = np.random.default_rng(0).random((B, 3))
+T.array[:] = 0.5
+for s in range(1, 4):
+    print(m.train_step_host_ptr(X.ptr, T.ptr, B, nf.LossKind.Mape, s), flush=True)
+"""
+
+
+def test_streamed_first_step_on_fresh_field_completes():
+    """Regression: the very first pinned host-pointer step of a fresh field
+    (B >= 2^15) used to deadlock under CUDA lazy module loading (the fused
+    kernel waited for chunks while the host blocked loading Adam). Run in a
+    child process with a timeout so a regression fails instead of hanging."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _FIRST_STREAMED.format(root=root)], capture_output=True, text=True,
+                       timeout=240)
+    assert r.returncode == 0, r.stderr[-2000:]
+    losses = [float(v) for v in r.stdout.split()]
+    assert len(losses) == 3 and all(np.isfinite(losses))
+
+
+def test_streamed_steps_parity_and_invalid_last_chunk():
+    """Pinned host buffers with B >= 2^15 take the streamed path (chunked H2D
+    under the fused kernel, speculative in-kernel input checks): losses match
+    the oracle step by step, and an inf in the LAST chunk leaves parameters,
+    gradients, moments and the step untouched (grid.hpp:226-229)."""
+    nf = _nf()
+    from paper_2201_05989_b200._lib import NfgInvalidArgument
+    g = _grid(nf, dims=3, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=512)
+    m = _model(nf, g, hidden_layers=2, table_fp32=True, lr=1e-3)
+    f = _oracle_field(m, lr=1e-3)
+    B = 1 << 16
+    Xh, Th = nf.PinnedBuffer((B, 3)), nf.PinnedBuffer((B, 1))
+    try:
+        for step in range(1, 4):   # step 1 warms the field up (plain path), steps 2-3 stream
+            X = _points(B, 3, seed=10 + step)
+            Xh.array[:] = X
+            Th.array[:] = O.csg_sdf(X).reshape(B, 1)
+            lg = m.train_step_host_ptr(Xh.ptr, Th.ptr, B, nf.LossKind.Mape, step)
+            lo = f.train_step(X, Th.array.copy(), O.LOSS_MAPE, step)
+            assert abs(lg - lo) <= 1e-3 * abs(lo), (step, lg, lo)
+        before = m.params
+        _, m0, v0 = m.adam_state()
+        Xh.array[B - 5, 2] = np.inf
+        with pytest.raises(NfgInvalidArgument, match="non-finite"):
+            m.train_step_host_ptr(Xh.ptr, Th.ptr, B, nf.LossKind.Mape, 4)
+        assert np.array_equal(m.params, before) and (m.grads == 0).all() and m.step == 3
+        _, m1, v1 = m.adam_state()
+        assert np.array_equal(m0, m1) and np.array_equal(v0, v1)
+        X = _points(B, 3, seed=20)
+        Xh.array[:] = X
+        Th.array[:] = O.csg_sdf(X).reshape(B, 1)
+        lg = m.train_step_host_ptr(Xh.ptr, Th.ptr, B, nf.LossKind.Mape, 4)
+        lo = f.train_step(X, Th.array.copy(), O.LOSS_MAPE, 4)
+        assert abs(lg - lo) <= 1e-3 * abs(lo), (lg, lo)
+    finally:
+        Xh.free()
+        Th.free()
+
+
 def test_invalid_and_unsupported():   # grid.hpp:224-229, NFG_EUNSUPPORTED
     nf = _nf()
     from paper_2201_05989_b200._lib import NfgInvalidArgument, NfgUnsupported
