@@ -297,7 +297,8 @@ def test_streamed_first_step_on_fresh_field_completes():
     assert len(losses) == 3 and all(np.isfinite(losses))
 
 
-def test_streamed_steps_parity_and_invalid_last_chunk():
+@pytest.mark.parametrize("B", [1 << 16, (1 << 15) + 77])   # ragged: the last chunk and tile are partial
+def test_streamed_steps_parity_and_invalid_last_chunk(B):
     """Pinned host buffers with B >= 2^15 take the streamed path (chunked H2D
     under the fused kernel, speculative in-kernel input checks): losses match
     the oracle step by step, and an inf in the LAST chunk leaves parameters,
@@ -307,7 +308,6 @@ def test_streamed_steps_parity_and_invalid_last_chunk():
     g = _grid(nf, dims=3, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=512)
     m = _model(nf, g, hidden_layers=2, table_fp32=True, lr=1e-3)
     f = _oracle_field(m, lr=1e-3)
-    B = 1 << 16
     Xh, Th = nf.PinnedBuffer((B, 3)), nf.PinnedBuffer((B, 1))
     try:
         for step in range(1, 4):   # step 1 warms the field up (plain path), steps 2-3 stream
