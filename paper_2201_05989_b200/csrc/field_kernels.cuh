@@ -638,6 +638,9 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     // ---- flush per-CTA dW / db (x 1/count) ----------------------------------
     const float ic = a.inv_count;
     auto flush = [&](const float (&cq)[2][4], int mt, int np, int out_k, int in_k, size_t woff) {
+#ifdef NFG_EXP_NO_FLUSH   // experiment builds only (tools/kbench.cu): upper bound of the dW flush cost
+        return;
+#endif
 #pragma unroll
         for (int q = 0; q < 2; ++q)
 #pragma unroll
