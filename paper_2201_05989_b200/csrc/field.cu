@@ -548,12 +548,14 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
     }
 }
 
+template <class AfterBackward>
 void device_train_step(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
-                       int loss_kind, int64_t step, const Streamed& sm = Streamed())
+                       int loss_kind, int64_t step, const Streamed& sm, AfterBackward&& after_backward)
 {
     nfg_ctx* c = f->ctx;
     const bool dp = c->comm != nullptr;
     device_backward(f, X, target, B_local, B_global, loss_kind, sm, true, /*reduce_grads=*/!dp);
+    after_backward();   // streamed steps: enqueue the batch copies before the optimizer launches
     const float lr_now = float(nfg::host::lr_at(f->milestones, f->factor, f->hyper.lr, step));
     if (!dp) {
         Span span(c, 1);
@@ -590,6 +592,12 @@ void device_train_step(nfg_field* f, const float* X, const float* target, int64_
     NFG_CUDA(nfg::launch_adam_fallback(a, c->num_sms, c->stream));
     c->launches += 2;
     f->step += 1;
+}
+
+void device_train_step(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
+                       int loss_kind, int64_t step, const Streamed& sm = Streamed())
+{
+    device_train_step(f, X, target, B_local, B_global, loss_kind, step, sm, [] {});
 }
 
 nfg::FieldShape make_shape(const nfg_grid_config& g, const nfg_mlp_config& m, const std::vector<nfg_level_spec>& lv, const std::vector<uint64_t>& dev_off,
@@ -1088,11 +1096,21 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
                 }
             };
             const Streamed streamed{ f->d_ready, epoch, chunk0, chunk };
-            device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step, streamed);
+            // the copies are enqueued right after the fused kernel's launch,
+            // ahead of the optimizer launches, so its first tiles wait less
+            auto copies = [&] {
+                try {
+                    enqueue_copies();
+                } catch (...) {
+                    for (; k < nchunks; ++k)   // never leave the kernel waiting
+                        c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0);
+                    throw;
+                }
+            };
             try {
-                enqueue_copies();
+                device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step, streamed, copies);
             } catch (...) {
-                for (; k < nchunks; ++k)   // never leave the kernel waiting
+                for (; k < nchunks; ++k)   // a failure before or after the copies: release every chunk
                     c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0);
                 throw;
             }
