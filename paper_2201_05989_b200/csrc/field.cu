@@ -1074,9 +1074,14 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
             // overlaps nothing.
             float* dX = static_cast<float*>(c->s0.get(size_t(B) * d * 4));
             float* dT = static_cast<float*>(c->s1.get(size_t(B) * no * 4));
-            // a small first chunk so the kernel's first tiles start early, then
+            // a first chunk covering the persistent kernel's first wave of tiles
+            // (2 CTAs x 64 samples per SM; NFG_STREAM_CHUNK0 overrides), then
             // NFG_STREAM_CHUNKS - 1 equal chunks
-            const int64_t chunk0 = std::min<int64_t>(B, 4096);
+            static const int64_t chunk0_env = [] {
+                const char* e = getenv("NFG_STREAM_CHUNK0");
+                return e ? int64_t(atoll(e)) : int64_t(0);
+            }();
+            const int64_t chunk0 = std::min<int64_t>(B, chunk0_env > 0 ? chunk0_env : int64_t(c->num_sms) * 128);
             const int64_t chunk = std::max<int64_t>(4096, (B - chunk0 + NFG_STREAM_CHUNKS - 2) / (NFG_STREAM_CHUNKS - 1));
             const int64_t nchunks = 1 + (B - chunk0 + chunk - 1) / chunk;
             const unsigned int epoch = ++f->epoch;
