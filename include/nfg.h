@@ -105,6 +105,11 @@ typedef struct nfg_field nfg_field;
 
 /* ---- context ---------------------------------------------------------- */
 const char* nfg_last_error(void);
+/* Diagnostics (no reference equivalent): the template instantiation of the
+ * last fused train (which = 0) or inference (which = 1) kernel this thread
+ * launched, e.g. "k_train ... table=f16 ... stage_alias=1". Lets parity tests
+ * assert they exercised the exact variant bench.py measures. Thread-local. */
+const char* nfg_last_kernel_variant(int32_t which);
 int nfg_abi_version(void);
 nfg_status nfg_ctx_create(int device, nfg_ctx** out);
 nfg_status nfg_ctx_destroy(nfg_ctx* ctx);

@@ -172,6 +172,42 @@ __global__ void __launch_bounds__(256) k_validate(const float* __restrict__ X, i
     }
 }
 
+// ---- start of a step: the step scratch and the sticky abort word ----------------
+// Asynchronous (device-pointer) steps are checked by the host only later
+// (nfg_field_check). A step that aborted (non-finite gradient: adam.hpp:86-90;
+// invalid input: grid.hpp:226-229) must then keep every LATER step from
+// touching the state, as the reference would have thrown at it. With inherit
+// set (unchecked steps pending), the previous step's abort is latched into
+// sticky[0..2] (flag, first bad group + 1, invalid-input bits); while latched,
+// each new step starts already aborted with flags[3] = 4 ("stood down"), so
+// k_train / encode / Adam all return early. sticky[3] counts the Adam launches
+// that did not apply since the host last read the results (k_adam).
+__global__ void k_step_begin(double* loss_sum, unsigned int* flags, float* dy_max, unsigned int* sticky, int inherit)
+{
+    if (!inherit) {   // the host has read every earlier result
+        sticky[0] = sticky[1] = sticky[2] = sticky[3] = 0u;
+    } else if (sticky[0] == 0u && flags[1] != 0u) {
+        sticky[0] = 1u;
+        sticky[1] = flags[2];
+        sticky[2] = flags[3];
+    }
+    *loss_sum = 0.0;
+    dy_max[0] = 0.0f;
+    dy_max[1] = 0.0f;
+    const bool down = sticky[0] != 0u;
+    flags[0] = 0u;
+    flags[1] = down ? 1u : 0u;
+    flags[2] = 0xffffffffu;
+    flags[3] = down ? 4u : 0u;
+}
+
+cudaError_t launch_step_begin(double* loss_sum, unsigned int* flags, float* dy_max, unsigned int* sticky, int inherit,
+                              cudaStream_t st)
+{
+    k_step_begin<<<1, 1, 0, st>>>(loss_sum, flags, dy_max, sticky, inherit);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cudaStream_t st)
 {
     if (n <= 0)
@@ -187,7 +223,7 @@ cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cuda
 __global__ void __launch_bounds__(256) k_adam_check(const AdamArgs a, int force)
 {
     const uint64_t nn = a.n_tab + a.n_w + a.n_b;
-    if (a.restore_on_invalid && a.flags[3] != 0u) {
+    if (a.restore_on_invalid && (a.flags[3] & 3u) != 0u) {
         // invalid batch detected inside the speculative fused kernel: the slab
         // was all-zero before the step, so zeroing restores it exactly
         for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nn;
@@ -283,8 +319,14 @@ __device__ __forceinline__ void adam_quad(const AdamArgs& a, uint64_t i0, float4
 #endif
 __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
 {
-    if (a.flags[1] != 0u)
-        return;   // non-finite gradient: state untouched (the reference throws first)
+    if (a.flags[1] != 0u) {   // non-finite gradient: state untouched (the reference throws first)
+        // every Adam step that does not apply (the aborting one and those standing
+        // down behind it, k_step_begin) is counted once, so nfg_field_check can
+        // restore the host step counter
+        if (a.sticky && a.mode != 1 && blockIdx.x == 0 && threadIdx.x == 0)
+            a.sticky[3] += 1u;
+        return;
+    }
     if ((a.mode == 1 && a.flags[0] != 0u) || (a.mode == 2 && a.flags[0] == 0u))
         return;   // pipelined chunks vs the checked fallback: exactly one of them updates
     const uint64_t n = a.mode == 1 ? a.hi : a.n_tab + a.n_w + a.n_b;

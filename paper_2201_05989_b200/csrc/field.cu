@@ -18,6 +18,13 @@
 #include "host_init.h"
 #include "kernels.h"
 
+namespace nfg {
+namespace {
+thread_local std::string g_variant[2];
+}
+void note_kernel_variant(int which, const char* desc) { g_variant[which & 1] = desc; }
+}   // namespace nfg
+
 namespace {
 
 thread_local std::string g_err;
@@ -223,8 +230,9 @@ struct nfg_field {
     float* d_m = nullptr;
     float* d_v = nullptr;
     __half* d_shadow = nullptr;
-    StepResult* d_res = nullptr;
-    StepResult* h_res = nullptr;   // pinned
+    StepResult* d_res = nullptr;   // followed in the same allocation by the 4-word sticky abort state
+    StepResult* h_res = nullptr;   // pinned, same layout
+    unsigned int* d_sticky = nullptr;   // [0] latched abort, [1] its group + 1, [2] its input flags, [3] Adam stand-downs
     uint64_t step = 0;
     uint64_t pending_steps = 0;    // device steps not yet checked (async API)
     // The gradient slab is all-zero (after init / a completed Adam step). Then a
@@ -261,13 +269,20 @@ nfg::StepScratch scratch_of(nfg_field* f)
     return s;
 }
 
+// Starts a step's scratch (k_step_begin). With unchecked asynchronous steps
+// pending, a previous abort is latched into the sticky word and this step
+// stands down; otherwise (the host has read every result) the sticky word is
+// cleared too.
 void reset_scratch(nfg_field* f)
 {
     f->scratch_ready = false;   // any other user dirties it after this reset
-    cudaStream_t st = f->ctx->stream;
-    NFG_CUDA(cudaMemsetAsync(f->d_res, 0, sizeof(StepResult), st));
-    NFG_CUDA(cudaMemsetAsync(&f->d_res->flags[2], 0xff, sizeof(unsigned int), st));
+    const int inherit = f->pending_steps > 0 ? 1 : 0;
+    NFG_CUDA(nfg::launch_step_begin(&f->d_res->loss_sum, f->d_res->flags, &f->d_res->dy_max, f->d_sticky, inherit,
+                                    f->ctx->stream));
+    f->ctx->launches++;
 }
+
+const unsigned int* sticky_host(const nfg_field* f) { return reinterpret_cast<const unsigned int*>(f->h_res + 1); }
 
 const char* group_name(unsigned g)
 {
@@ -280,12 +295,16 @@ const char* group_name(unsigned g)
 
 void fetch_result(nfg_field* f)
 {
-    NFG_CUDA(cudaMemcpyAsync(f->h_res, f->d_res, sizeof(StepResult), cudaMemcpyDeviceToHost, f->ctx->stream));
+    NFG_CUDA(cudaMemcpyAsync(f->h_res, f->d_res, sizeof(StepResult) + 4 * sizeof(unsigned int), cudaMemcpyDeviceToHost,
+                             f->ctx->stream));
     NFG_CUDA(cudaStreamSynchronize(f->ctx->stream));
 }
 
 void raise_if_aborted(nfg_field* f)
 {
+    if (f->h_res->flags[3] == 4u)
+        throw std::logic_error("train_step: skipped because an earlier asynchronous step aborted "
+                               "(nfg_field_check reports it)");
     if (f->h_res->flags[3] & 1u)
         throw std::invalid_argument("encode_forward: non-finite input");
     if (f->h_res->flags[3] & 2u)
@@ -294,6 +313,32 @@ void raise_if_aborted(nfg_field* f)
         const unsigned g = f->h_res->flags[2] == 0xffffffffu ? 0u : f->h_res->flags[2] - 1u;
         throw Fail{ NFG_ENONFINITE, std::string("adam_step: non-finite gradient in group '") + group_name(g) + "'" };
     }
+}
+
+// Reads back the asynchronous steps issued since the last check. The first
+// abort among them (latched in the sticky word, or the last step's own) is
+// reported like the reference's throw; every step that stood down behind it
+// left the state untouched, and the host step counter drops by the number of
+// Adam launches that did not apply (sticky[3]).
+void settle_pending(nfg_field* f)
+{
+    fetch_result(f);
+    f->pending_steps = 0;
+    const unsigned int* sk = sticky_host(f);
+    if (sk[0] == 0u && f->h_res->flags[1] == 0u)
+        return;
+    f->step -= sk[3];
+    if (sk[0]) {
+        f->h_res->flags[1] = 1u;
+        f->h_res->flags[2] = sk[1];
+        f->h_res->flags[3] = sk[2];
+    }
+    // invalid input on a clean slab was undone by re-zeroing; a non-finite
+    // gradient stays in the slab (the reference throws before zeroing)
+    f->grads_clean = (f->h_res->flags[3] & 3u) != 0;
+    reset_scratch(f);   // pending == 0: clears the sticky word as well
+    f->scratch_ready = true;
+    raise_if_aborted(f);
 }
 
 const void* table_ptr(nfg_field* f) { return f->opts.table_fp32 ? static_cast<const void*>(f->d_p) : f->d_shadow; }
@@ -388,6 +433,7 @@ nfg::AdamArgs adam_args(nfg_field* f, float lr_now)
         a.eager = forced >= 0 ? forced : (dense ? 1 : 0);
     }
     a.mode = 0;
+    a.sticky = f->d_sticky;
     return a;
 }
 
@@ -684,6 +730,7 @@ float* buffer_of(nfg_field* f, int which)
 extern "C" {
 
 const char* nfg_last_error(void) { return g_err.c_str(); }
+const char* nfg_last_kernel_variant(int32_t which) { return nfg::g_variant[which & 1].c_str(); }
 int nfg_abi_version(void) { return NFG_ABI_VERSION; }
 
 nfg_status nfg_ctx_create(int device, nfg_ctx** out)
@@ -909,17 +956,19 @@ nfg_status nfg_field_create(nfg_ctx* ctx, const nfg_grid_config* grid, const nfg
             NFG_CUDA(cudaMalloc(&f->d_v, bytes));
             NFG_CUDA(cudaMalloc(&f->d_shadow, std::max<uint64_t>(f->n_tab_dev, 1) * sizeof(__half)));
             NFG_CUDA(cudaMalloc(&f->d_levels, sizeof(nfg::LevelDev) * NFG_MAX_LEVELS));
-            NFG_CUDA(cudaMalloc(&f->d_res, sizeof(StepResult)));
+            NFG_CUDA(cudaMalloc(&f->d_res, sizeof(StepResult) + 4 * sizeof(unsigned int)));
+            f->d_sticky = reinterpret_cast<unsigned int*>(f->d_res + 1);
+            NFG_CUDA(cudaMemset(f->d_sticky, 0, 4 * sizeof(unsigned int)));
             NFG_CUDA(cudaMalloc(&f->d_ready, NFG_MAX_CHUNKS * sizeof(unsigned int)));
             NFG_CUDA(cudaMemset(f->d_ready, 0, NFG_MAX_CHUNKS * sizeof(unsigned int)));
-            NFG_CUDA(cudaMallocHost(&f->h_res, sizeof(StepResult)));
+            NFG_CUDA(cudaMallocHost(&f->h_res, sizeof(StepResult) + 4 * sizeof(unsigned int)));
             NFG_CUDA(cudaMemcpy(f->d_levels, f->shape.grid.lv, sizeof(nfg::LevelDev) * NFG_MAX_LEVELS,
                                 cudaMemcpyHostToDevice));
             for (float* p : { f->d_p, f->d_g, f->d_m, f->d_v })
                 NFG_CUDA(cudaMemsetAsync(p, 0, bytes, ctx->stream));
             NFG_CUDA(cudaMemsetAsync(f->d_shadow, 0, std::max<uint64_t>(f->n_tab_dev, 1) * sizeof(__half), ctx->stream));
             reset_scratch(f);   // a check before the first step must read a clean status
-            std::memset(f->h_res, 0, sizeof(StepResult));
+            std::memset(f->h_res, 0, sizeof(StepResult) + 4 * sizeof(unsigned int));
             NFG_CUDA(cudaStreamSynchronize(ctx->stream));
         } catch (...) {
             nfg_field_destroy(f);
@@ -1058,6 +1107,8 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
 {
     return guard([&] {
         nfg_ctx* c = f->ctx;
+        if (f->pending_steps)
+            settle_pending(f);   // a deferred abort of earlier asynchronous steps surfaces here
         const int d = f->gcfg.dims, no = f->mcfg.output_width;
         const uint64_t before = f->step;
         const bool was_clean = f->grads_clean;
@@ -1131,7 +1182,7 @@ nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* targe
             f->step = before;   // the reference throws before incrementing (adam.hpp:86-92)
             // invalid input on a clean slab was undone by re-zeroing; a
             // non-finite gradient leaves the accumulated gradients in place
-            f->grads_clean = was_clean && (f->h_res->flags[3] != 0);
+            f->grads_clean = was_clean && (f->h_res->flags[3] & 3u) != 0;
             raise_if_aborted(f);
         }
         f->grads_clean = true;   // Adam zeroed every gradient (adam.hpp:118-120)
@@ -1147,7 +1198,8 @@ nfg_status nfg_field_gradients(nfg_field* f, const float* X, const float* target
 {
     return guard([&] {
         nfg_ctx* c = f->ctx;
-
+        if (f->pending_steps)
+            settle_pending(f);
         const float* dX = stage(c->s0, X, size_t(B) * f->gcfg.dims, c->stream);
         const float* dT = stage(c->s1, target, size_t(B) * f->mcfg.output_width, c->stream);
         device_backward(f, dX, dT, B, B * c->nranks, loss_kind, Streamed(), false);
@@ -1206,15 +1258,7 @@ nfg_status nfg_step_record_check(nfg_field* f, const nfg_step_record* rec, int64
 
 nfg_status nfg_field_check(nfg_field* f)
 {
-    return guard([&] {
-        fetch_result(f);
-        f->pending_steps = 0;
-        if (f->h_res->flags[1]) {
-            f->step -= 1;
-            f->grads_clean = f->h_res->flags[3] != 0;
-            raise_if_aborted(f);
-        }
-    });
+    return guard([&] { settle_pending(f); });
 }
 
 nfg_status nfg_field_evaluate_device(nfg_field* f, const float* X, int64_t B, float* out)
@@ -1384,6 +1428,8 @@ nfg_status nfg_loss(nfg_ctx* c, int32_t kind, const float* pred, const float* ta
 nfg_status nfg_adam_step(nfg_field* f, float lr_now)
 {
     return guard([&] {
+        if (f->pending_steps)
+            settle_pending(f);
         reset_scratch(f);
         const uint64_t before = f->step;
         run_adam(f, lr_now, true);

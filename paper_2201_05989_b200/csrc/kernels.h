@@ -22,7 +22,9 @@ struct FieldShape {
 // Gradient-side device scratch of one training step.
 struct StepScratch {
     double* loss_sum;        // [1]
-    unsigned int* flags;     // [0]: maybe non-finite; [1]: abort; [2]: first bad group (+1); [3]: fp16 saturations
+    unsigned int* flags;     // [0]: maybe non-finite; [1]: abort; [2]: first bad group (+1);
+                             // [3]: invalid input (1 non-finite, 2 outside [0,1]^d), 4 = stood down behind an
+                             // earlier asynchronous abort (k_step_begin)
     float* dy_max;           // [1] max |dY| (as float bits, non-negative)
 };
 
@@ -110,11 +112,14 @@ struct AdamArgs {
     // gradient (flags[0]); mode 2 is the fallback full pass that runs only then.
     int mode;
     uint64_t lo, hi;
+    unsigned int* sticky;     // sticky abort word (k_step_begin); counts stood-down steps in [3]
 };
 cudaError_t launch_adam_range(const AdamArgs& a, int num_sms, cudaStream_t st);
 cudaError_t launch_adam_fallback(const AdamArgs& a, int num_sms, cudaStream_t st);
 cudaError_t launch_adam(const AdamArgs& a, bool force_check, int num_sms, cudaStream_t st);
 cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cudaStream_t st);
+cudaError_t launch_step_begin(double* loss_sum, unsigned int* flags, float* dy_max, unsigned int* sticky, int inherit,
+                              cudaStream_t st);
 cudaError_t launch_shadow(const float* p, __half* shadow, uint64_t n, cudaStream_t st);
 size_t encode_bwd_det_scratch(int64_t B, int d);
 cudaError_t launch_encode_bwd_det(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
@@ -123,6 +128,10 @@ cudaError_t launch_encode_bwd_det(const FieldShape& s, const LevelDev* lv, const
 cudaError_t launch_reduce_partials(const float* part, int nparts, int64_t n, float* out, const double* part_loss,
                                    int nloss, double* loss_sum, const unsigned int* flags, cudaStream_t st);
 int train_warps_per_cta();
+// Records the template instantiation a launch helper just launched (which: 0 =
+// train, 1 = infer), so tests can assert that the benchmarked variant is the
+// one they checked (nfg_last_kernel_variant).
+void note_kernel_variant(int which, const char* desc);
 bool fused_supported(const FieldShape& s);    // fused encode+MLP kernels built for this shape
 bool staged_supported(const FieldShape& s);   // staged MLP kernels built for this shape
 cudaError_t launch_loss_out(const double* loss_sum, const unsigned int* flags, double count, float* out,

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "field_kernels.cuh"
@@ -30,6 +31,12 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
             return e;
         per_sm = std::max(n, 1);
     }
+    static char desc[160];
+    if (!desc[0])
+        snprintf(desc, sizeof(desc), "k_train src=%d grad=%d sink=%d d=%d F=%d table=%s in_steps=%d hidden=%d "
+                 "stage_alias=%d ctas_per_sm=%d", SRC, GRAD, SINK, D, F, sizeof(TT) == 2 ? "f16" : "f32", IS, NH,
+                 int(StageAlias<SRC, D, F, TT, IS, NH>::ON), per_sm);
+    note_kernel_variant(0, desc);
     const int64_t ntiles = (a.B + TS - 1) / TS;
     if (ntiles <= 0)
         return cudaSuccess;
@@ -56,6 +63,11 @@ cudaError_t run_infer(const FieldShape& s, const LevelDev* lv, const InferArgs& 
             return e;
         per_sm = std::max(n, 1);
     }
+    static char desc[160];
+    if (!desc[0])
+        snprintf(desc, sizeof(desc), "k_infer src=%d d=%d F=%d table=%s in_steps=%d hidden=%d warps=%d", SRC, D, F,
+                 sizeof(TT) == 2 ? "f16" : "f32", IS, NH, IW);
+    note_kernel_variant(1, desc);
     const int64_t tiles = (a.B + 15) / 16;
     if (tiles <= 0)
         return cudaSuccess;

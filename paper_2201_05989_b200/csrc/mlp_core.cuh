@@ -50,11 +50,14 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// Saturating fp16 pack for backward operands (scaled gradients): never inf.
+// Saturating fp16 pack for backward operands (scaled gradients): a finite
+// overflow saturates instead of becoming inf, but a NaN stays NaN, so a
+// non-finite loss gradient still reaches the gradient slab and Adam's scan
+// rejects the step like the reference (adam.hpp:86-90).
 __device__ __forceinline__ uint32_t pack_sat(float a, float b)
 {
-    a = fminf(fmaxf(a, -65504.0f), 65504.0f);
-    b = fminf(fmaxf(b, -65504.0f), 65504.0f);
+    a = a != a ? a : fminf(fmaxf(a, -65504.0f), 65504.0f);
+    b = b != b ? b : fminf(fmaxf(b, -65504.0f), 65504.0f);
     return pack_half2(a, b);
 }
 

@@ -260,13 +260,59 @@ def _ptr(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
-def _dptr(t) -> Optional[int]:
-    """Device pointer of a torch CUDA tensor (or a raw int)."""
+def _dptr(t, what: str = "tensor", dtype: str = "float32") -> Optional[int]:
+    """Device pointer of a torch CUDA tensor (or a raw int, taken as is).
+    Tensors must be CUDA, contiguous and of the expected dtype: the library
+    reads them as flat arrays."""
     if t is None:
         return None
     if isinstance(t, int):
         return t
+    import torch
+    if not t.is_cuda:
+        raise L.NfgInvalidArgument(L.NFG_EINVAL, f"{what}: expected a CUDA tensor")
+    if t.dtype != getattr(torch, dtype):
+        raise L.NfgInvalidArgument(L.NFG_EINVAL, f"{what}: expected dtype {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise L.NfgInvalidArgument(L.NFG_EINVAL, f"{what}: expected a contiguous tensor")
     return int(t.data_ptr())
+
+
+class _StreamOrder:
+    """Orders the library's stream against torch's current stream around a
+    device-pointer call: the library waits for torch's pending writes of the
+    inputs, and torch's stream waits for the library before it reads the
+    outputs or its caching allocator reuses any of the buffers. A no-op when
+    no torch tensor is involved (raw pointers: the caller orders)."""
+
+    _ext = {}
+
+    def __init__(self, ctx: "Context", *tensors):
+        self.ctx = ctx
+        self.on = any(t is not None and not isinstance(t, int) for t in tensors)
+
+    def __enter__(self):
+        if self.on:
+            import torch
+            key = (self.ctx.device, self.ctx.stream)
+            ext = _StreamOrder._ext.get(key)
+            if ext is None:
+                ext = _StreamOrder._ext[key] = torch.cuda.ExternalStream(self.ctx.stream, device=self.ctx.device)
+            self.lib_stream = ext
+            self.torch_stream = torch.cuda.current_stream(self.ctx.device)
+            if self.torch_stream.cuda_stream != ext.cuda_stream:
+                ev = torch.cuda.Event()
+                ev.record(self.torch_stream)
+                ext.wait_event(ev)
+        return self
+
+    def __exit__(self, *exc):
+        if self.on and self.torch_stream.cuda_stream != self.lib_stream.cuda_stream:
+            import torch
+            ev = torch.cuda.Event()
+            ev.record(self.lib_stream)
+            self.torch_stream.wait_event(ev)
+        return False
 
 
 BUF_PARAMS, BUF_GRADS, BUF_ADAM_M, BUF_ADAM_V = range(4)
@@ -439,13 +485,23 @@ class FieldModel:
         L.check(self.lib.nfg_field_train_step(self.h, x_ptr, t_ptr, B, int(loss), step, C.byref(out)))
         return float(out.value)
 
-    def train_step_device(self, X, target, B_local: int, B_global: int, loss: LossKind, step: int) -> None:
-        """Asynchronous step on device pointers (torch CUDA tensors or ints)."""
-        L.check(self.lib.nfg_field_train_step_device(self.h, _dptr(X), _dptr(target), B_local, B_global, int(loss),
-                                                     step, None))
+    def train_step_device(self, X, target, B_local: int, B_global: int, loss: LossKind, step: int,
+                          loss_out=None) -> None:
+        """Asynchronous step on device pointers (torch CUDA tensors or ints),
+        stream-ordered against torch's current stream. ``loss_out`` (optional,
+        one float on the device) receives the step's loss; deferred errors are
+        reported by check()."""
+        with _StreamOrder(self.ctx, X, target, loss_out):
+            L.check(self.lib.nfg_field_train_step_device(self.h, _dptr(X, "X"), _dptr(target, "target"), B_local,
+                                                         B_global, int(loss), step, _dptr(loss_out, "loss_out")))
 
     def check(self) -> None:
         L.check(self.lib.nfg_field_check(self.h))
+
+    def last_kernel_variant(self, which: int = 0) -> str:
+        """Template instantiation of the last fused train (0) / inference (1)
+        kernel launched by this thread (diagnostics; no reference equivalent)."""
+        return self.lib.nfg_last_kernel_variant(which).decode()
 
     def evaluate(self, X) -> np.ndarray:   # model.cpp:102-109
         X = self._check_x(X)
@@ -454,7 +510,8 @@ class FieldModel:
         return out
 
     def evaluate_device(self, X, B: int, out) -> None:
-        L.check(self.lib.nfg_field_evaluate_device(self.h, _dptr(X), B, _dptr(out)))
+        with _StreamOrder(self.ctx, X, out):
+            L.check(self.lib.nfg_field_evaluate_device(self.h, _dptr(X, "X"), B, _dptr(out, "out")))
 
     # ---- components -------------------------------------------------------------
     def encode_forward(self, X, want_cache: bool = False):   # grid.hpp:219-272
@@ -594,10 +651,12 @@ class DeviceRng:
         self.h = h
 
     def below(self, bound: int, n: int, out) -> None:   # next_below x n (pcg32.hpp:30-38)
-        L.check(self.lib.nfg_rng_below_device(self.h, bound, n, _dptr(out)))
+        with _StreamOrder(self.ctx, out):
+            L.check(self.lib.nfg_rng_below_device(self.h, bound, n, _dptr(out, "out", "int32")))
 
     def floats(self, n: int, out) -> None:   # next_float x n (pcg32.hpp:41-44)
-        L.check(self.lib.nfg_rng_floats_device(self.h, n, _dptr(out)))
+        with _StreamOrder(self.ctx, out):
+            L.check(self.lib.nfg_rng_floats_device(self.h, n, _dptr(out, "out")))
 
     def state(self):
         s, i = C.c_uint64(), C.c_uint64()

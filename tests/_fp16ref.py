@@ -40,8 +40,9 @@ def forward(W, b, shapes, Y, sigmoid):
     return out, acts, masks, mats
 
 
-def tile_scale(d, tile=128):
-    """The kernel's per-128-sample power-of-two scale: max|d| * s < 16."""
+def tile_scale(d, tile=64):
+    """The kernel's per-tile power-of-two scale: max|d| * s < 16 over each
+    64-sample k_train tile (TS = 16 x 4 warps, field_kernels.cuh)."""
     s = np.ones((d.shape[0], 1))
     for r in range(0, d.shape[0], tile):
         mx = np.abs(d[r:r + tile]).max()
@@ -51,12 +52,12 @@ def tile_scale(d, tile=128):
     return s
 
 
-def backward(W, b, shapes, Y, dOut, sigmoid):
+def backward(W, b, shapes, Y, dOut, sigmoid, tile=64):
     out, acts, masks, mats = forward(W, b, shapes, Y, sigmoid)
     dz = np.asarray(dOut, np.float64)
     if sigmoid:
         dz = dz * (out * (1 - out))
-    sc = tile_scale(dz)
+    sc = tile_scale(dz, tile)
     gW, gb = [None] * len(mats), [None] * len(mats)
     for k in range(len(mats) - 1, -1, -1):
         dzh = h(dz * sc) / sc

@@ -508,3 +508,46 @@ def test_wide_encodings_fall_back_to_staged_kernels(levels, hidden):   # L*F = 4
     Xq = rng.floats(500 * 3).reshape(-1, 3)
     a, b = m.evaluate(Xq), f.evaluate(Xq)
     assert np.abs(a - b).max() <= 5e-3 * np.abs(b).max() + 1e-5
+
+
+@pytest.mark.parametrize("bad", ["nan_target", "invalid_input"])
+def test_async_abort_is_sticky(bad):   # adam.hpp:86-90 / grid.hpp:226-229 under the asynchronous device API
+    """A device-pointer step that aborts must keep every LATER asynchronous step
+    from touching the state (the reference would have thrown at it): the
+    parameters, moments and step counter stay those of the last good step, and
+    check() reports the FIRST abort with its own reason."""
+    import torch
+    nf = _nf()
+    from paper_2201_05989_b200._lib import NfgInvalidArgument, NfgNonFinite
+    g = _grid(nf, dims=3, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=512)
+    m = _model(nf, g, hidden_layers=2, lr=1e-3)
+    B = 4096
+    X = torch.from_numpy(_points(B, 3, seed=4)).cuda()
+    T = torch.from_numpy(O.csg_sdf(_points(B, 3, seed=4)).reshape(B, 1)).cuda()
+    for s in (1, 2):
+        m.train_step_device(X, T, B, B, nf.LossKind.Mape, s)
+    m.check()
+    P2 = m.params
+    s2, M2, V2 = m.adam_state()
+    assert s2 == 2
+    Xb, Tb = X.clone(), T.clone()
+    if bad == "nan_target":
+        Tb[17, 0] = float("nan")
+    else:
+        Xb[17, 1] = 1.5
+    m.train_step_device(Xb, Tb, B, B, nf.LossKind.Mape, 3)   # aborts
+    for s in (4, 5):                                          # must stand down
+        m.train_step_device(X, T, B, B, nf.LossKind.Mape, s)
+    with pytest.raises(NfgNonFinite if bad == "nan_target" else NfgInvalidArgument,
+                       match="tables|mlp|non-finite" if bad == "nan_target" else "outside"):
+        m.check()
+    s_, M_, V_ = m.adam_state()
+    assert s_ == 2
+    assert np.array_equal(m.params, P2) and np.array_equal(M_, M2) and np.array_equal(V_, V2)
+    if bad == "invalid_input":
+        assert (m.grads == 0).all()       # the speculative step was undone
+        m.train_step_device(X, T, B, B, nf.LossKind.Mape, 3)
+        m.check()
+        assert m.step == 3 and not np.array_equal(m.params, P2)
+    else:
+        assert not np.isfinite(m.grads).all()   # the reference keeps the failing step's gradients
