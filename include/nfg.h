@@ -110,6 +110,14 @@ const char* nfg_last_error(void);
  * launched, e.g. "k_train ... table=f16 ... stage_alias=1". Lets parity tests
  * assert they exercised the exact variant bench.py measures. Thread-local. */
 const char* nfg_last_kernel_variant(int32_t which);
+/* Diagnostics (no reference equivalent): live L2-level throughput of this GPU
+ * for the hot path's access patterns, measured at full occupancy on a 32 MB +
+ * 64 MB L2-resident footprint (csrc/diag.cu). op 0: random 4 B L2 reads
+ * (sectors/s); 1: random 4 B cp.async (sectors/s); 2: random
+ * red.global.add.v2.f32 (sectors/s); 3: coalesced L2 streaming reads (bytes/s);
+ * 4: random 4 B ld.global.nc (sectors/s). The roofline denominators of
+ * bench.py. Synchronises the context stream. */
+nfg_status nfg_diag_l2_peak(nfg_ctx* ctx, int32_t op, double* rate);
 int nfg_abi_version(void);
 nfg_status nfg_ctx_create(int device, nfg_ctx** out);
 nfg_status nfg_ctx_destroy(nfg_ctx* ctx);

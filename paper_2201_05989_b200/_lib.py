@@ -85,6 +85,7 @@ SIGNATURES = {
     "nfg_last_error": (C.c_char_p, []),
     "nfg_abi_version": (C.c_int, []),
     "nfg_last_kernel_variant": (C.c_char_p, [C.c_int32]),
+    "nfg_diag_l2_peak": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_double)]),
     "nfg_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "nfg_ctx_destroy": (C.c_int, [_vp]),
     "nfg_ctx_synchronize": (C.c_int, [_vp]),

@@ -14,11 +14,11 @@ Tolerances and where they come from:
   * touched table entries: identical set (contract);
   * gradients are checked twice. (1) Against ``tests/_fp16ref.py``, an exact
     numpy emulation of the kernel's fp16 operand roundings (Y, activations,
-    weights, dz): <= 3e-3 in norm — this checks the kernel's math.
+    weights, dz): <= 1e-3 in norm — this checks the kernel's math.
     (2) Against the fp32 oracle: by the triangle inequality
     ||gpu - oracle|| <= ||gpu - emu|| + ||emu - oracle||, so the bound is
     the emulation's own distance from the oracle (the cost of fp16 operands,
-    measured on the same batch on the CPU, not asserted) + 3e-3. On a TRAINED
+    measured on the same batch on the CPU, not asserted) + 1e-3. On a TRAINED
     field that distance is < 1e-2 and the §8c contract (1e-2) is asserted
     directly. At init (tables ~1e-4, pre-activations near zero) fp16 rounding
     flips ReLU masks of near-zero units, and the emulation itself sits ~3%
@@ -39,7 +39,7 @@ CASES = {
     "config2": (CFG2, 1, False, 1, 1e-4, 1 << 18),
     "config1": (CFG1, 3, True, 0, 1e-2, 1 << 16),
 }
-MATH_TOL = 3e-3      # gpu vs the fp16-operand emulation (kernel math)
+MATH_TOL = 1e-3      # gpu vs the fp16-operand emulation (kernel math; measured <= 4.2e-4)
 CONTRACT = 1e-2      # SURVEY.md §8c table/MLP gradient contract (trained fields)
 
 
