@@ -31,12 +31,6 @@ WORKLOAD = "config2: 3D SDF hash L16 F2 T2^19 Nmin16 Nmax2048, MLP 32-64-64-1 Re
 
 # algorithmic work per unit
 ADAM_BYTES_PER_PARAM = 34          # r: p g m v; w: p m v g(=0) + fp16 shadow
-# L1 sector model of k_train (profiles/lsu_r1.md, profiles/ncu_r1.json, final round-1 build)
-L1_GATHER_SECTORS_PER_SAMPLE = 71.9
-L2_RED_REQUESTS_PER_SAMPLE = 68.8
-LSU_CYC_PER_GATHER_SECTOR = 1.04
-LSU_CYC_PER_RED = 1.58
-N_SMS = 148
 ENC_FWD_L2_BYTES_PER_SAMPLE = 2304  # 72 sectors x 32 B (3D, fp16 rows)
 ENC_BWD_L2_BYTES_PER_SAMPLE = 2560  # 80 sectors x 32 B (fp32 F=2 rows, RED)
 MLP_TRAIN_FLOP_PER_SAMPLE = 37248
@@ -52,7 +46,44 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--infer-b", type=int, default=B_INFER)
     ap.add_argument("--no-nerf", action="store_true")
+    ap.add_argument("--launcher-selftest", action="store_true",
+                    help="spawn/rendezvous check only (gloo, no GPU work): rank 0 prints the ranks it saw")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(args):
+    """``--gpus N`` (N > 1) outside torchrun: re-exec this script under
+    torch.distributed.run with N ranks on this node, so a plain
+    ``python bench.py --gpus 8`` cannot silently measure one GPU. Returns the
+    child's exit code, or None when this process already is a rank."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def launcher_selftest(rank, world):
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        seen = int(t.item())
+        dist.destroy_process_group()
+    else:
+        seen = 1
+    if rank == 0:
+        print(json.dumps({"launcher_selftest": True, "n_gpus": world, "ranks_seen": seen, "pid": os.getpid()}),
+              flush=True)
 
 
 def peaks():
@@ -341,15 +372,26 @@ def run_reference(args, rank, world):
 
 def main():
     args = parse()
+    if args.impl != "reference":
+        rc = launch_ranks(args)
+        if rc is not None:
+            sys.exit(rc)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but this job has WORLD_SIZE={world} ranks; refusing to report "
+                 "a number for a GPU count that is not the one measured")
+    if args.launcher_selftest:
+        return launcher_selftest(rank, world)
 
     import numpy as np
     import torch
     import torch.distributed as dist
+    if torch.cuda.device_count() < world:
+        sys.exit(f"bench.py: {world} ranks requested but only {torch.cuda.device_count()} GPUs are visible")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -360,6 +402,9 @@ def main():
         uid = [nf.Context.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.attach_comm(uid[0], rank, world)
+        comm_rank, comm_size = ctx.comm_info()
+        assert (comm_rank, comm_size) == (rank, world), (
+            f"NCCL communicator reports rank {comm_rank} of {comm_size}, expected {rank} of {world}")
     model = nf.FieldModel(ctx)
     model.hash_cfg = nf.HashEncodingConfig(**CFG2)
     model.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=1)
@@ -469,8 +514,27 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt.item())
     e2e_value = world * B_TRAIN * e2e_steps / t_e2e
+    # the same call on PAGEABLE host memory (a reference caller's Eigen::MatrixXf
+    # or a plain numpy array handed to the C ABI)
+    Xp = np.array(Xh.array, copy=True)
+    Tp = np.array(Th.array, copy=True)
     Xh.free()
     Th.free()
+    for i in range(2):
+        step += 1
+        model.train_step_host_ptr(Xp.ctypes.data, Tp.ctypes.data, B_TRAIN, nf.LossKind.Mape, step)
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        step += 1
+        loss = model.train_step_host_ptr(Xp.ctypes.data, Tp.ctypes.data, B_TRAIN, nf.LossKind.Mape, step)
+    t_pg = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([t_pg], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_pg = float(tt.item())
+    e2e_pageable = world * B_TRAIN * e2e_steps / t_pg
+    del Xp, Tp
 
     # ---- inference queries/s (config 5, queries sharded, no communication) ----
     Bq = args.infer_b
@@ -535,42 +599,62 @@ def main():
     clocks["train_region_samples"] = mark1 - mark0
 
     # ---- roofline of the dominant kernel --------------------------------------
+    # k_train and k_infer are L2-level bound (tables and gradients stay in the
+    # 126 MB L2: ncu DRAM traffic is ~6% of their algorithmic bytes), so their
+    # denominator is the L2-level rate of exactly their access kinds, measured
+    # live on this GPU (csrc/diag.cu): random 4 B cp.async sector gathers,
+    # random red.global.add.v2.f32 sector reductions, random 4 B ld.global.nc
+    # gathers. Adam streams p/m/v from HBM: its denominator is the HBM peak.
     hbm_peak, tflops_peak, peak_src = peaks()
+    l2 = {}
+    try:
+        for name, op in (("gather_cp_async", 1), ("red_v2_f32", 2), ("gather_ld_nc", 4), ("gather_ld_cg", 0),
+                         ("stream_read", 3)):
+            l2[name] = ctx.l2_peak(op)
+    except Exception as e:   # never lose the headline line
+        l2 = {"error": str(e)[:200]}
     train_ms, adam_ms = phase_ms[0], phase_ms[1]
     adam_gbs = n_params * ADAM_BYTES_PER_PARAM / (adam_ms / 1000.0) / 1e9 if adam_ms > 0 else None
     enc_bytes = B_TRAIN * (ENC_FWD_L2_BYTES_PER_SAMPLE + ENC_BWD_L2_BYTES_PER_SAMPLE)
     train_l2_gbs = enc_bytes / (train_ms / 1000.0) / 1e9 if train_ms > 0 else None
     train_tflops = B_TRAIN * MLP_TRAIN_FLOP_PER_SAMPLE / (train_ms / 1000.0) / 1e12 if train_ms > 0 else None
     ncu = ncu_traffic()
-    if train_ms >= adam_ms:
-        dominant = "k_train (fused encode+MLP+loss+backward)"
-        roof = {"bound": "hbm", "kernel": dominant, "achieved": train_l2_gbs, "peak": hbm_peak, "unit": "GB/s",
-                "frac": train_l2_gbs / hbm_peak if train_l2_gbs else None,
-                "traffic": ncu.get("k_train"), "peak_source": peak_src, "ncu": ncu.get("_src"),
-                "note": "achieved = algorithmic L2-level gather+RED bytes (2304+2560 B/sample x 2^18 samples) / "
-                        "CUDA-event kernel time; the kernel is L2-atomic/latency bound (tables+grads stay "
-                        "L2-resident: traffic = DRAM bytes per launch from ncu), so the HBM copy peak is only "
-                        "the nearest measured denominator"}
-        # The binding resource is the L1's per-sector cost of divergent accesses
-        # (profiles/lsu_r1.md): sectors per sample from ncu, SM cycles per sector
-        # from tools/lsu_bench.cu, converted at the measured SM clock.
-        mhz = clocks.get("sm_mhz") or 1965.0
-        model_us = ((L1_GATHER_SECTORS_PER_SAMPLE * LSU_CYC_PER_GATHER_SECTOR +
-                     L2_RED_REQUESTS_PER_SAMPLE * LSU_CYC_PER_RED) * B_TRAIN / N_SMS / mhz)
-        roof["l1_sector_model"] = {
-            "gather_sectors_per_sample": L1_GATHER_SECTORS_PER_SAMPLE, "red_requests_per_sample":
-            L2_RED_REQUESTS_PER_SAMPLE, "sm_cycles_per_gather_sector": LSU_CYC_PER_GATHER_SECTOR,
-            "sm_cycles_per_red": LSU_CYC_PER_RED, "bound_us": model_us, "kernel_us": train_ms * 1000.0,
-            "frac": model_us / (train_ms * 1000.0) if train_ms > 0 else None,
-            "source": "profiles/ncu_r1.json counts, profiles/lsu_r1.md per-sector costs"}
-    else:
-        dominant = "k_adam"
-        roof = {"bound": "hbm", "kernel": dominant, "achieved": adam_gbs, "peak": hbm_peak, "unit": "GB/s",
-                "frac": adam_gbs / hbm_peak if adam_gbs else None, "traffic": ncu.get("k_adam"),
-                "peak_source": peak_src, "ncu": ncu.get("_src")}
+    fwd_sec, bwd_sec = ENC_FWD_L2_BYTES_PER_SAMPLE / 32, ENC_BWD_L2_BYTES_PER_SAMPLE / 32
+    roof_train = roof_infer = None
+    if "error" not in l2 and train_ms > 0:
+        # time the kernel's sector mix needs at the measured per-kind rates
+        t_bound = B_TRAIN * (fwd_sec / l2["gather_cp_async"] + bwd_sec / l2["red_v2_f32"])
+        peak_mix = enc_bytes / t_bound / 1e9
+        dram = ncu.get("k_train")
+        roof_train = {
+            "bound": "l2", "kernel": "k_train (fused encode+MLP+loss+backward)", "achieved": train_l2_gbs,
+            "peak": peak_mix, "unit": "GB/s", "frac": train_l2_gbs / peak_mix, "traffic": dram,
+            "peak_source": "measured live (csrc/diag.cu: random 4 B cp.async gathers and red.global.add.v2.f32, "
+                           "L2-resident 96 MB footprint, full occupancy), weighted by the kernel's 72 gather + 80 "
+                           "reduction sectors per sample",
+            "algorithmic_bytes_per_launch": enc_bytes, "kernel_us": train_ms * 1000.0, "bound_us": t_bound * 1e6,
+            "mlp_tflops": train_tflops, "mlp_tensor_frac": train_tflops / tflops_peak if train_tflops else None,
+            "dram_gbs": dram / (train_ms / 1000.0) / 1e9 if dram else None,
+            "dram_frac_of_hbm": dram / (train_ms / 1000.0) / 1e9 / hbm_peak if dram else None,
+            "ncu": ncu.get("_src")}
+        if t_inf > 0:
+            inf_bytes = Bq * ENC_FWD_L2_BYTES_PER_SAMPLE
+            t_b = Bq * fwd_sec / l2["gather_ld_nc"]
+            ach = inf_bytes / (t_inf / 1000.0) / 1e9
+            roof_infer = {
+                "bound": "l2", "kernel": "k_infer (fused encode+MLP inference)", "achieved": ach,
+                "peak": inf_bytes / t_b / 1e9, "unit": "GB/s", "frac": t_b / (t_inf / 1000.0),
+                "traffic": ncu.get("k_infer"), "algorithmic_bytes_per_launch": inf_bytes,
+                "kernel_us": t_inf * 1000.0, "bound_us": t_b * 1e6,
+                "peak_source": "measured live (csrc/diag.cu: random 4 B ld.global.nc gathers), 72 sectors/query"}
+    # legacy view kept for comparison with round 1: L2-level bytes over the HBM peak
+    hbm_view = {"achieved": train_l2_gbs, "peak": hbm_peak, "frac": train_l2_gbs / hbm_peak if train_l2_gbs else None,
+                "peak_source": peak_src, "note": "L2-level bytes over the HBM copy peak (round-1 convention; not "
+                                                 "the binding resource)"}
     roof_adam = {"bound": "hbm", "kernel": "k_adam", "achieved": adam_gbs, "peak": hbm_peak, "unit": "GB/s",
                  "frac": adam_gbs / hbm_peak if adam_gbs else None, "traffic": ncu.get("k_adam"),
-                 "algorithmic_bytes": n_params * ADAM_BYTES_PER_PARAM}
+                 "algorithmic_bytes": n_params * ADAM_BYTES_PER_PARAM, "peak_source": peak_src}
+    roof = roof_train if (roof_train and train_ms >= adam_ms) else roof_adam
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -590,7 +674,10 @@ def main():
                            "l2": "not flushed: each step streams ~0.42 GB of Adam state (> 126 MB L2); "
                                  f"inputs cycle over {N_RESIDENT} resident batches"},
                 "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": B_TRAIN * 16,
-                        "d2h_bytes_per_step": 32, "steps": e2e_steps},
+                        "d2h_bytes_per_step": 32, "steps": e2e_steps, "host_memory": "pinned (cudaHostAlloc)"},
+                "e2e_pageable": {"value": e2e_pageable, "unit": "samples/s", "h2d_bytes_per_step": B_TRAIN * 16,
+                                 "d2h_bytes_per_step": 32, "steps": e2e_steps,
+                                 "host_memory": "pageable (numpy arrays through the C ABI train_step)"},
                 "inference": {"value": qps, "unit": "queries/s", "queries": Bq * world,
                               "ms_per_call": t_inf, "sweep_one_gpu": sweep},
                 "strong_scaling": strong,
@@ -599,7 +686,8 @@ def main():
                 "phases_ms_per_step": ({"train_kernel": phase_ms[0], "adam": phase_ms[1]} if world == 1 else
                                        {"train_kernel": phase_ms[0],
                                         "allreduce_pipelined_with_adam": phase_ms[2]}),
-                "roofline": roof, "roofline_adam": roof_adam,
+                "roofline": roof, "roofline_infer": roof_infer, "roofline_adam": roof_adam,
+                "roofline_train_hbm_view": hbm_view, "l2_peaks_measured": l2,
                 "secondary_rates": {"adam_gbs": adam_gbs, "train_l2_gbs": train_l2_gbs,
                                     "train_mlp_tflops": train_tflops},
                 "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,

@@ -138,6 +138,9 @@ nfg_status nfg_ctx_read_profile(nfg_ctx* ctx, double ms[4], int64_t* steps);
  * attached, train steps all-reduce the gradient slab before Adam. */
 nfg_status nfg_comm_unique_id(uint8_t id[128]);
 nfg_status nfg_ctx_attach_comm(nfg_ctx* ctx, const uint8_t id[128], int rank, int nranks);
+/* Rank and size as the attached NCCL communicator reports them (0 and 1
+ * without one): the bench asserts the job really runs on N ranks. */
+nfg_status nfg_ctx_comm_info(nfg_ctx* ctx, int* rank, int* nranks);
 
 /* ---- level table (grid.hpp:66-84), host only ---------------------------- */
 /* Writes min(cap, levels) specs; returns the level count or -1 on error. */
@@ -167,6 +170,11 @@ nfg_status nfg_field_get_config(const nfg_field* f, nfg_grid_config* grid, nfg_m
 nfg_status nfg_field_context(const nfg_field* f, nfg_ctx** ctx);
 nfg_status nfg_field_get_step(const nfg_field* f, uint64_t* step);
 nfg_status nfg_field_set_step(nfg_field* f, uint64_t step);
+/* Data parallelism: every rank takes root's parameters, Adam m/v and step
+ * (ncclBroadcast on the attached communicator; a no-op without one). The
+ * replicated Adam step of the ranks stays in lock-step only from identical
+ * state (no reference equivalent: the reference is single-process). */
+nfg_status nfg_field_broadcast(nfg_field* f, int root);
 
 /* FieldModel::train_step (model.cpp:111-138): encode -> MLP -> loss ->
  * backward -> Adam at lr_at(schedule, lr, step). Host pointers; returns the

@@ -95,6 +95,8 @@ SIGNATURES = {
     "nfg_ctx_read_profile": (C.c_int, [_vp, C.POINTER(C.c_double), _i64p]),
     "nfg_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "nfg_ctx_attach_comm": (C.c_int, [_vp, C.POINTER(C.c_uint8), C.c_int, C.c_int]),
+    "nfg_ctx_comm_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "nfg_field_broadcast": (C.c_int, [_vp, C.c_int]),
     "nfg_level_resolutions": (C.c_int32, [C.POINTER(nfg_grid_config), C.POINTER(nfg_level_spec), C.c_int32]),
     "nfg_growth_factor": (C.c_double, [C.POINTER(nfg_grid_config)]),
     "nfg_spatial_hash": (C.c_uint32, [_u32p, C.c_int32, C.c_uint32]),

@@ -51,6 +51,9 @@ struct NcclApi {
     decltype(&ncclCommDestroy) comm_destroy = nullptr;
     decltype(&ncclAllReduce) all_reduce = nullptr;
     decltype(&ncclGetErrorString) error_string = nullptr;
+    decltype(&ncclCommCount) comm_count = nullptr;
+    decltype(&ncclCommUserRank) comm_user_rank = nullptr;
+    decltype(&ncclBroadcast) broadcast = nullptr;
 };
 
 const NcclApi& nccl()
@@ -66,6 +69,9 @@ const NcclApi& nccl()
             api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
             api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
             api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+            api.comm_count = reinterpret_cast<decltype(api.comm_count)>(dlsym(h, "ncclCommCount"));
+            api.comm_user_rank = reinterpret_cast<decltype(api.comm_user_rank)>(dlsym(h, "ncclCommUserRank"));
+            api.broadcast = reinterpret_cast<decltype(api.broadcast)>(dlsym(h, "ncclBroadcast"));
         }
     }
     if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce)
@@ -856,6 +862,23 @@ nfg_status nfg_ctx_attach_comm(nfg_ctx* c, const uint8_t id[128], int rank, int 
     });
 }
 
+nfg_status nfg_ctx_comm_info(nfg_ctx* c, int* rank, int* nranks)
+{
+    return guard([&] {
+        int r = 0, n = 1;
+        if (c->comm) {   // ask NCCL itself, not the values attach_comm was given
+            const NcclApi& api = nccl();
+            require(api.comm_count && api.comm_user_rank, "comm_info: NCCL lacks ncclCommCount/ncclCommUserRank");
+            NFG_NCCL(api.comm_count(c->comm, &n));
+            NFG_NCCL(api.comm_user_rank(c->comm, &r));
+        }
+        if (rank)
+            *rank = r;
+        if (nranks)
+            *nranks = n;
+    });
+}
+
 int32_t nfg_level_resolutions(const nfg_grid_config* cfg, nfg_level_spec* out, int32_t cap)
 {
     int32_t n = -1;
@@ -1100,6 +1123,33 @@ nfg_status nfg_field_get_step(const nfg_field* f, uint64_t* step)
 nfg_status nfg_field_set_step(nfg_field* f, uint64_t step)
 {
     return guard([&] { f->step = step; });
+}
+
+nfg_status nfg_field_broadcast(nfg_field* f, int root)
+{
+    return guard([&] {
+        nfg_ctx* c = f->ctx;
+        if (!c->comm)
+            return;   // one rank: nothing to agree on
+        require(root >= 0 && root < c->nranks, "nfg_field_broadcast: bad root");
+        if (f->pending_steps)
+            settle_pending(f);
+        const NcclApi& n = nccl();
+        require(n.broadcast != nullptr, "nfg_field_broadcast: NCCL lacks ncclBroadcast");
+        // params, Adam m and v in the device layout, then the step counter:
+        // data-parallel ranks apply the same replicated Adam step, so they must
+        // start from bit-identical state
+        for (float* b : { f->d_p, f->d_m, f->d_v })
+            NFG_NCCL(n.broadcast(b, b, f->n_total_dev, ncclFloat32, root, c->comm, c->stream));
+        uint64_t* d_step = static_cast<uint64_t*>(c->s3.get(sizeof(uint64_t)));
+        NFG_CUDA(cudaMemcpyAsync(d_step, &f->step, sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+        NFG_NCCL(n.broadcast(d_step, d_step, 1, ncclUint64, root, c->comm, c->stream));
+        uint64_t s = 0;
+        NFG_CUDA(cudaMemcpyAsync(&s, d_step, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+        refresh_shadow(f);
+        NFG_CUDA(cudaStreamSynchronize(c->stream));
+        f->step = s;
+    });
 }
 
 nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* target, int64_t B, int32_t loss_kind,

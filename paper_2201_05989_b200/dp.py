@@ -53,6 +53,9 @@ class DataParallelTrainer:
     def __init__(self, model, rank: int, world: int):
         self.model, self.rank, self.world = model, rank, world
         attach(model.ctx, rank, world)
+        # the replicated Adam step keeps ranks in lock-step only from identical
+        # state: take rank 0's params, m, v and step (seeds or checkpoints may differ)
+        model.broadcast(0)
 
     def step_device(self, X_global, T_global, loss, step: int) -> None:
         """X_global/T_global: device tensors holding the full global batch on every rank

@@ -241,6 +241,20 @@ class Context:
         buf = (C.c_uint8 * 128)(*uid)
         L.check(self.lib.nfg_ctx_attach_comm(self.h, buf, rank, nranks))
 
+    def comm_info(self):
+        """(rank, nranks) as the attached NCCL communicator reports them."""
+        r, n = C.c_int(), C.c_int()
+        L.check(self.lib.nfg_ctx_comm_info(self.h, C.byref(r), C.byref(n)))
+        return r.value, n.value
+
+    def l2_peak(self, op: int) -> float:
+        """Measured L2-level rate of one access kind (diag.cu): 0 random 4 B
+        ld.cg, 1 random 4 B cp.async, 2 random red.v2.f32, 4 random 4 B
+        ld.nc — sectors/s; 3 streaming L2 reads — bytes/s."""
+        r = C.c_double()
+        L.check(self.lib.nfg_diag_l2_peak(self.h, op, C.byref(r)))
+        return r.value
+
 
 _DEFAULT_CTX: Optional[Context] = None
 
@@ -436,6 +450,10 @@ class FieldModel:
     @step.setter
     def step(self, s: int) -> None:
         L.check(self.lib.nfg_field_set_step(self.h, s))
+
+    def broadcast(self, root: int = 0) -> None:
+        """Data parallelism: take root's params, Adam m/v and step (no-op on one rank)."""
+        L.check(self.lib.nfg_field_broadcast(self.h, root))
 
     def adam_state(self):
         """(step, m, v) flat in param-group order (AdamState, adam.hpp:56-73)."""

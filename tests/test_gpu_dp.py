@@ -92,3 +92,28 @@ def test_dp_streamed_host_pointer_steps():
         for xh, th in bufs:
             xh.free()
             th.free()
+
+
+def test_broadcast_and_comm_info():
+    """nfg_field_broadcast on a 1-rank communicator keeps the state (root is
+    itself) and refreshes the fp16 shadow; comm_info reports NCCL's own view;
+    DataParallelTrainer broadcasts at construction."""
+    nf = _nf()
+    from paper_2201_05989_b200.dp import DataParallelTrainer
+    (a, b), (plain, dp) = _pair(nf, det=False)
+    assert plain.comm_info() == (0, 1) and dp.comm_info() == (0, 1)
+    rng = O.Pcg32(6, 6)
+    X = rng.floats(3 * 4096).reshape(-1, 3)
+    T = O.csg_sdf(X).reshape(-1, 1)
+    b.train_step(X, T, nf.LossKind.Mape, 1)
+    p0, (s0, m0, v0) = b.params, b.adam_state()
+    b.broadcast(0)
+    p1, (s1, m1, v1) = b.params, b.adam_state()
+    assert s0 == s1 == 1
+    for x, y in ((p0, p1), (m0, m1), (v0, v1)):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    out0 = b.evaluate(X[:256])
+    DataParallelTrainer(b, 0, 1)   # world 1: attach is a no-op, broadcast still runs
+    assert np.array_equal(b.evaluate(X[:256]), out0)
+    with pytest.raises(ValueError):
+        b.broadcast(1)   # root outside the communicator
