@@ -181,6 +181,15 @@ nfg_status nfg_field_broadcast(nfg_field* f, int root);
  * batch loss. X is dims x B, target n_out x B. */
 nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* target, int64_t B,
                                 int32_t loss_kind, int64_t step, float* loss);
+/* The same with an explicit global batch (SURVEY §8b's nfg_field_train_step
+ * signature): with data-parallel ranks holding ragged shards, every rank passes
+ * its own B_local and the common B_global; the loss gradient is normalised by
+ * B_global * n_out (losses.hpp:16) and the returned loss is this shard's share.
+ * nfg_field_train_step is this call with B_global = B * nranks. Pinned and
+ * pageable host buffers are both streamed under the fused kernel (pageable ones
+ * through pinned bounce buffers filled by host copy threads). */
+nfg_status nfg_field_train_step_global(nfg_field* f, const float* X, const float* target, int64_t B_local,
+                                       int64_t B_global, int32_t loss_kind, int64_t step, float* loss);
 /* Same on device pointers, asynchronous. B_global is the global batch across
  * data-parallel ranks (loss normalisation, losses.hpp:16). loss_dev (device
  * float, may be NULL) receives the global-batch loss of this rank's shard. */

@@ -115,6 +115,7 @@ SIGNATURES = {
     "nfg_field_get_step": (C.c_int, [_vp, _u64p]),
     "nfg_field_set_step": (C.c_int, [_vp, C.c_uint64]),
     "nfg_field_train_step": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int64, _fp]),
+    "nfg_field_train_step_global": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int64, C.c_int32, C.c_int64, _fp]),
     "nfg_field_train_step_device": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int64, C.c_int32, C.c_int64, _vp]),
     "nfg_field_gradients": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, _fp]),
     "nfg_field_check": (C.c_int, [_vp]),

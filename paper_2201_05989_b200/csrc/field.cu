@@ -7,11 +7,15 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/nfg.h"
@@ -113,6 +117,128 @@ void require(bool ok, const char* msg)
         throw std::invalid_argument(msg);
 }
 
+// Page-locked host staging (bounce) buffer for pageable callers.
+struct HostBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t n)
+    {
+        if (n > bytes) {
+            if (p)
+                cudaFreeHost(p);
+            p = nullptr;
+            bytes = 0;
+            if (cudaHostAlloc(&p, n, cudaHostAllocDefault) != cudaSuccess)
+                throw Fail{ NFG_ECUDA, "cudaHostAlloc bounce buffer failed" };
+            bytes = n;
+        }
+        return p;
+    }
+    ~HostBuf()
+    {
+        if (p)
+            cudaFreeHost(p);
+    }
+};
+
+// Pageable -> pinned copies of a streamed batch on the calling thread plus a
+// few persistent host threads. A job is a list of chunks; every participant
+// copies its 1/n slice of chunk 0, then of chunk 1, ... and bumps the chunk's
+// counter, so the caller puts chunk k on the copy engine as soon as all slices
+// of chunk k landed, while the others already copy chunk k+1 (and the fused
+// kernel runs). Workers spin for a while after a job (back-to-back steps
+// arrive well within that window) before they block, so a step does not pay
+// thread wake-ups.
+struct CopyPool {
+    struct Part {
+        const char* src;
+        char* dst;
+        size_t bytes;
+    };
+    std::vector<std::thread> threads;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::atomic<uint64_t> gen{ 0 };
+    std::atomic<bool> stop{ false };
+    std::atomic<int> sleepers{ 0 };
+    const std::vector<std::vector<Part>>* job = nullptr;   // job[k] = copies of chunk k
+    std::atomic<int> done[64];                              // >= NFG_MAX_CHUNKS
+    int n = 0;                                              // participants: workers + the caller
+
+    explicit CopyPool(int workers) : n(workers + 1)
+    {
+        for (auto& d : done)
+            d.store(0);
+        for (int i = 0; i < workers; ++i)
+            threads.emplace_back([this, i] { run(i + 1); });
+    }
+    ~CopyPool()
+    {
+        {
+            std::lock_guard<std::mutex> l(mu);
+            stop.store(true);
+        }
+        cv.notify_all();
+        for (auto& t : threads)
+            t.join();
+    }
+    void copy_slice(size_t k, int me)
+    {
+        for (const Part& p : (*job)[k]) {
+            const size_t lo = p.bytes * size_t(me) / size_t(n), hi = p.bytes * size_t(me + 1) / size_t(n);
+            std::memcpy(p.dst + lo, p.src + lo, hi - lo);
+        }
+        done[k].fetch_add(1, std::memory_order_acq_rel);
+    }
+    void run(int me)
+    {
+        uint64_t seen = 0;
+        for (;;) {
+            int spins = 0;
+            while (gen.load(std::memory_order_acquire) == seen && !stop.load(std::memory_order_relaxed)) {
+                if (++spins < 200000) {
+                    std::this_thread::yield();
+                    continue;
+                }
+                std::unique_lock<std::mutex> l(mu);
+                sleepers.fetch_add(1);
+                cv.wait(l, [&] { return stop.load() || gen.load() != seen; });
+                sleepers.fetch_sub(1);
+            }
+            if (stop.load())
+                return;
+            seen = gen.load(std::memory_order_acquire);
+            for (size_t k = 0; k < job->size(); ++k)
+                copy_slice(k, me);
+        }
+    }
+    void start(const std::vector<std::vector<Part>>& j)
+    {
+        for (size_t k = 0; k < j.size(); ++k)
+            done[k].store(0, std::memory_order_relaxed);
+        job = &j;
+        {
+            std::lock_guard<std::mutex> l(mu);
+            gen.fetch_add(1, std::memory_order_acq_rel);
+        }
+        if (sleepers.load() > 0)
+            cv.notify_all();
+    }
+    // the caller's share of chunk k, then wait for the workers' shares
+    void finish_chunk(size_t k)
+    {
+        copy_slice(k, 0);
+        while (done[k].load(std::memory_order_acquire) < n)
+            std::this_thread::yield();
+    }
+    void drain(size_t nchunks)
+    {
+        for (size_t k = 0; k < nchunks; ++k)
+            while (done[k].load(std::memory_order_acquire) < n)
+                std::this_thread::yield();
+    }
+};
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -150,6 +276,8 @@ struct nfg_ctx {
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1;
     DevBuf s0, s1, s2, s3;   // staging for host-pointer calls
+    HostBuf h0, h1;          // pinned bounce buffers for pageable streamed steps
+    CopyPool* copy_pool = nullptr;
     double* d_red = nullptr;
     // streamed inputs: H2D chunks on a copy stream, each followed by a
     // stream memory write of its ready flag (copy engine + front end only)
@@ -788,6 +916,7 @@ nfg_status nfg_ctx_destroy(nfg_ctx* c)
             cudaStreamDestroy(c->stream);
         if (c->copy_stream)
             cudaStreamDestroy(c->copy_stream);
+        delete c->copy_pool;
         if (c->ev_order)
             cudaEventDestroy(c->ev_order);
         if (c->comm_stream)
@@ -1152,95 +1281,159 @@ nfg_status nfg_field_broadcast(nfg_field* f, int root)
     });
 }
 
-nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* target, int64_t B, int32_t loss_kind,
-                                int64_t step, float* loss)
+// The reference's synchronous train_step on host pointers (model.cpp:111-138).
+static void host_train_step(nfg_field* f, const float* X, const float* target, int64_t B, int64_t B_global,
+                     int32_t loss_kind, int64_t step, float* loss)
 {
-    return guard([&] {
-        nfg_ctx* c = f->ctx;
-        if (f->pending_steps)
-            settle_pending(f);   // a deferred abort of earlier asynchronous steps surfaces here
-        const int d = f->gcfg.dims, no = f->mcfg.output_width;
-        const uint64_t before = f->step;
-        const bool was_clean = f->grads_clean;
-        if (f->stream_warm && f->grads_clean && f->opts.fused_train && !f->opts.deterministic && c->write_value32 &&
-            B >= (int64_t(1) << 15) && !launches_serialized() && is_pinned(X) && is_pinned(target)) {
-            // Overlap the H2D of the batch with the step: the fused kernel is
-            // launched first and waits per tile for its chunk's ready flag,
-            // which the copy stream writes (cuStreamWriteValue32) after each
-            // chunk lands, while the host enqueues the copies. Not used when
-            // launches may be serialised (a profiler or sanitizer injected,
-            // CUDA_LAUNCH_BLOCKING=1): a kernel waiting on another stream can
-            // then never finish, so those runs take the plain staged path.
-            // Pinned sources only: a pageable copy blocks the host and
-            // overlaps nothing.
-            float* dX = static_cast<float*>(c->s0.get(size_t(B) * d * 4));
-            float* dT = static_cast<float*>(c->s1.get(size_t(B) * no * 4));
-            // a first chunk covering the persistent kernel's first wave of tiles
-            // (2 CTAs x 64 samples per SM; NFG_STREAM_CHUNK0 overrides), then
-            // NFG_STREAM_CHUNKS - 1 equal chunks
-            static const int64_t chunk0_env = [] {
-                const char* e = getenv("NFG_STREAM_CHUNK0");
-                return e ? int64_t(atoll(e)) : int64_t(0);
+    nfg_ctx* c = f->ctx;
+    if (f->pending_steps)
+        settle_pending(f);   // a deferred abort of earlier asynchronous steps surfaces here
+    require(B >= 0 && B_global >= B, "train_step: B_global must cover the local batch");
+    const int d = f->gcfg.dims, no = f->mcfg.output_width;
+    const uint64_t before = f->step;
+    const bool was_clean = f->grads_clean;
+    const bool can_stream = f->stream_warm && f->grads_clean && f->opts.fused_train && !f->opts.deterministic &&
+                            c->write_value32 && B >= (int64_t(1) << 15) && !launches_serialized();
+    const bool pinned = can_stream && is_pinned(X) && is_pinned(target);
+    if (can_stream) {
+        // Overlap the H2D of the batch with the step: the fused kernel is
+        // launched first and waits per tile for its chunk's ready flag,
+        // which the copy stream writes (cuStreamWriteValue32) after each
+        // chunk lands, while the host enqueues the copies. Not used when
+        // launches may be serialised (a profiler or sanitizer injected,
+        // CUDA_LAUNCH_BLOCKING=1): a kernel waiting on another stream can
+        // then never finish, so those runs take the plain staged path.
+        // Pageable sources (a caller's Eigen::MatrixXf or numpy array) are
+        // first copied chunk by chunk into pinned bounce buffers by a few
+        // host threads, so the copy engine and the kernel start on chunk 0
+        // while the host still copies the rest.
+        float* dX = static_cast<float*>(c->s0.get(size_t(B) * d * 4));
+        float* dT = static_cast<float*>(c->s1.get(size_t(B) * no * 4));
+        // a first chunk covering the persistent kernel's first wave of tiles
+        // (2 CTAs x 64 samples per SM; NFG_STREAM_CHUNK0 overrides), then
+        // NFG_STREAM_CHUNKS - 1 equal chunks
+        static const int64_t chunk0_env = [] {
+            const char* e = getenv("NFG_STREAM_CHUNK0");
+            return e ? int64_t(atoll(e)) : int64_t(0);
+        }();
+        const int64_t chunk0 = std::min<int64_t>(B, chunk0_env > 0 ? chunk0_env : int64_t(c->num_sms) * 128);
+        const int64_t chunk = std::max<int64_t>(4096, (B - chunk0 + NFG_STREAM_CHUNKS - 2) / (NFG_STREAM_CHUNKS - 1));
+        const int64_t nchunks = 1 + (B - chunk0 + chunk - 1) / chunk;
+        const float* srcX = X;
+        const float* srcT = target;
+        std::vector<std::vector<CopyPool::Part>> job;
+        if (!pinned) {
+            float* hX = static_cast<float*>(c->h0.get(size_t(B) * d * 4));
+            float* hT = static_cast<float*>(c->h1.get(size_t(B) * no * 4));
+            // helper threads next to the caller (NFG_COPY_THREADS; 0 = the caller
+            // copies alone). Measured at config 2 on a 16-core host: pageable e2e
+            // 5.5e8 (caller alone), 6.6 / 6.8 / 6.9 / 7.0e8 samples/s with 1 / 2 /
+            // 3 / 5 helpers, pinned 7.15e8; the driver's own pageable staging 4.35e8.
+            static const int workers = [] {
+                const char* e = getenv("NFG_COPY_THREADS");
+                const int hw = int(std::thread::hardware_concurrency());
+                return e ? std::max(0, atoi(e)) : std::max(1, std::min(4, hw / 4));
             }();
-            const int64_t chunk0 = std::min<int64_t>(B, chunk0_env > 0 ? chunk0_env : int64_t(c->num_sms) * 128);
-            const int64_t chunk = std::max<int64_t>(4096, (B - chunk0 + NFG_STREAM_CHUNKS - 2) / (NFG_STREAM_CHUNKS - 1));
-            const int64_t nchunks = 1 + (B - chunk0 + chunk - 1) / chunk;
-            const unsigned int epoch = ++f->epoch;
-            NFG_CUDA(cudaEventRecord(c->ev_order, c->stream));        // staging buffers free
-            NFG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_order, 0));
-            int64_t k = 0;
-            auto enqueue_copies = [&] {
-                for (; k < nchunks; ++k) {
-                    const int64_t s0 = k == 0 ? 0 : chunk0 + (k - 1) * chunk;
-                    const int64_t n = std::min(k == 0 ? chunk0 : chunk, B - s0);
-                    NFG_CUDA(cudaMemcpyAsync(dX + s0 * d, X + s0 * d, size_t(n) * d * 4, cudaMemcpyHostToDevice,
-                                             c->copy_stream));
-                    NFG_CUDA(cudaMemcpyAsync(dT + s0 * no, target + s0 * no, size_t(n) * no * 4,
-                                             cudaMemcpyHostToDevice, c->copy_stream));
-                    if (c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0) != CUDA_SUCCESS)
-                        throw Fail{ NFG_ECUDA, "cuStreamWriteValue32 failed" };
-                }
-            };
-            const Streamed streamed{ f->d_ready, epoch, chunk0, chunk };
-            // the copies are enqueued right after the fused kernel's launch,
-            // ahead of the optimizer launches, so its first tiles wait less
-            auto copies = [&] {
-                try {
-                    enqueue_copies();
-                } catch (...) {
-                    for (; k < nchunks; ++k)   // never leave the kernel waiting
-                        c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0);
-                    throw;
-                }
-            };
+            if (!c->copy_pool && workers > 0)
+                c->copy_pool = new CopyPool(workers);
+            job.resize(size_t(nchunks));
+            for (int64_t k = 0; k < nchunks; ++k) {
+                const int64_t s0 = k == 0 ? 0 : chunk0 + (k - 1) * chunk;
+                const int64_t n = std::min(k == 0 ? chunk0 : chunk, B - s0);
+                job[size_t(k)] = { { reinterpret_cast<const char*>(X + s0 * d), reinterpret_cast<char*>(hX + s0 * d),
+                                     size_t(n) * d * 4 },
+                                   { reinterpret_cast<const char*>(target + s0 * no),
+                                     reinterpret_cast<char*>(hT + s0 * no), size_t(n) * no * 4 } };
+            }
+            // the previous step's DMA out of the bounce buffers finished:
+            // host-pointer steps are synchronous
+            if (c->copy_pool)
+                c->copy_pool->start(job);
+            srcX = hX;
+            srcT = hT;
+        }
+        const unsigned int epoch = ++f->epoch;
+        NFG_CUDA(cudaEventRecord(c->ev_order, c->stream));        // staging buffers free
+        NFG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_order, 0));
+        int64_t k = 0, caller_chunks = 0;
+        auto enqueue_copies = [&] {
+            for (; k < nchunks; ++k) {
+                const int64_t s0 = k == 0 ? 0 : chunk0 + (k - 1) * chunk;
+                const int64_t n = std::min(k == 0 ? chunk0 : chunk, B - s0);
+                if (!pinned && c->copy_pool) {
+                    c->copy_pool->finish_chunk(size_t(k));
+                    caller_chunks = k + 1;
+                } else if (!pinned)
+                    for (const CopyPool::Part& p : job[size_t(k)])
+                        std::memcpy(p.dst, p.src, p.bytes);
+                NFG_CUDA(cudaMemcpyAsync(dX + s0 * d, srcX + s0 * d, size_t(n) * d * 4, cudaMemcpyHostToDevice,
+                                         c->copy_stream));
+                NFG_CUDA(cudaMemcpyAsync(dT + s0 * no, srcT + s0 * no, size_t(n) * no * 4,
+                                         cudaMemcpyHostToDevice, c->copy_stream));
+                if (c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0) != CUDA_SUCCESS)
+                    throw Fail{ NFG_ECUDA, "cuStreamWriteValue32 failed" };
+            }
+        };
+        const Streamed streamed{ f->d_ready, epoch, chunk0, chunk };
+        // the copies are enqueued right after the fused kernel's launch,
+        // ahead of the optimizer launches, so its first tiles wait less
+        auto copies = [&] {
             try {
-                device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step, streamed, copies);
+                enqueue_copies();
             } catch (...) {
-                for (; k < nchunks; ++k)   // a failure before or after the copies: release every chunk
+                for (; k < nchunks; ++k)   // never leave the kernel waiting
                     c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0);
                 throw;
             }
-        } else {
-            const float* dX = stage(c->s0, X, size_t(B) * d, c->stream);
-            const float* dT = stage(c->s1, target, size_t(B) * no, c->stream);
-            device_train_step(f, dX, dT, B, B * c->nranks, loss_kind, step);
+        };
+        auto drain_pool = [&] {   // never return while workers still read the caller's arrays
+            if (!pinned && c->copy_pool) {
+                for (int64_t j = caller_chunks; j < nchunks; ++j)   // the caller's shares it never reached
+                    c->copy_pool->copy_slice(size_t(j), 0);
+                c->copy_pool->drain(size_t(nchunks));
+            }
+        };
+        try {
+            device_train_step(f, dX, dT, B, B_global, loss_kind, step, streamed, copies);
+        } catch (...) {
+            for (; k < nchunks; ++k)   // a failure before or after the copies: release every chunk
+                c->write_value32(c->copy_stream, CUdeviceptr(f->d_ready + k), epoch, 0);
+            drain_pool();
+            throw;
         }
-        fetch_result(f);
-        reset_scratch(f);   // for the next step, off its critical path (h_res holds this one)
-        f->scratch_ready = true;
-        if (f->h_res->flags[1]) {
-            f->step = before;   // the reference throws before incrementing (adam.hpp:86-92)
-            // invalid input on a clean slab was undone by re-zeroing; a
-            // non-finite gradient leaves the accumulated gradients in place
-            f->grads_clean = was_clean && (f->h_res->flags[3] & 3u) != 0;
-            raise_if_aborted(f);
-        }
-        f->grads_clean = true;   // Adam zeroed every gradient (adam.hpp:118-120)
-        f->stream_warm = true;   // every kernel of the step is loaded now
-        const double count = double(B) * c->nranks * no;
-        if (loss)
-            *loss = count > 0 ? float(f->h_res->loss_sum / count) : 0.0f;
-    });
+        drain_pool();
+    } else {
+        const float* dX = stage(c->s0, X, size_t(B) * d, c->stream);
+        const float* dT = stage(c->s1, target, size_t(B) * no, c->stream);
+        device_train_step(f, dX, dT, B, B_global, loss_kind, step);
+    }
+    fetch_result(f);
+    reset_scratch(f);   // for the next step, off its critical path (h_res holds this one)
+    f->scratch_ready = true;
+    if (f->h_res->flags[1]) {
+        f->step = before;   // the reference throws before incrementing (adam.hpp:86-92)
+        // invalid input on a clean slab was undone by re-zeroing; a
+        // non-finite gradient leaves the accumulated gradients in place
+        f->grads_clean = was_clean && (f->h_res->flags[3] & 3u) != 0;
+        raise_if_aborted(f);
+    }
+    f->grads_clean = true;   // Adam zeroed every gradient (adam.hpp:118-120)
+    f->stream_warm = true;   // every kernel of the step is loaded now
+    const double count = double(B_global) * no;
+    if (loss)
+        *loss = count > 0 ? float(f->h_res->loss_sum / count) : 0.0f;
+}
+
+nfg_status nfg_field_train_step(nfg_field* f, const float* X, const float* target, int64_t B, int32_t loss_kind,
+                                int64_t step, float* loss)
+{
+    return guard([&] { host_train_step(f, X, target, B, B * f->ctx->nranks, loss_kind, step, loss); });
+}
+
+nfg_status nfg_field_train_step_global(nfg_field* f, const float* X, const float* target, int64_t B_local,
+                                       int64_t B_global, int32_t loss_kind, int64_t step, float* loss)
+{
+    return guard([&] { host_train_step(f, X, target, B_local, B_global, loss_kind, step, loss); });
 }
 
 nfg_status nfg_field_gradients(nfg_field* f, const float* X, const float* target, int64_t B, int32_t loss_kind,

@@ -497,10 +497,17 @@ class FieldModel:
         L.check(self.lib.nfg_field_gradients(self.h, _ptr(X), _ptr(T), X.shape[0], int(loss), C.byref(out)))
         return float(out.value)
 
-    def train_step_host_ptr(self, x_ptr: int, t_ptr: int, B: int, loss: LossKind, step: int) -> float:
-        """train_step on caller-owned (e.g. pinned) host buffers, no validation copy."""
+    def train_step_host_ptr(self, x_ptr: int, t_ptr: int, B: int, loss: LossKind, step: int,
+                            B_global: Optional[int] = None) -> float:
+        """train_step on caller-owned host buffers (pinned or pageable), no
+        validation copy. ``B_global`` (data parallelism, ragged shards): the
+        global batch the loss is normalised by; default B x ranks."""
         out = C.c_float()
-        L.check(self.lib.nfg_field_train_step(self.h, x_ptr, t_ptr, B, int(loss), step, C.byref(out)))
+        if B_global is None:
+            L.check(self.lib.nfg_field_train_step(self.h, x_ptr, t_ptr, B, int(loss), step, C.byref(out)))
+        else:
+            L.check(self.lib.nfg_field_train_step_global(self.h, x_ptr, t_ptr, B, B_global, int(loss), step,
+                                                         C.byref(out)))
         return float(out.value)
 
     def train_step_device(self, X, target, B_local: int, B_global: int, loss: LossKind, step: int,

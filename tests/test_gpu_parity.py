@@ -551,3 +551,56 @@ def test_async_abort_is_sticky(bad):   # adam.hpp:86-90 / grid.hpp:226-229 under
         assert m.step == 3 and not np.array_equal(m.params, P2)
     else:
         assert not np.isfinite(m.grads).all()   # the reference keeps the failing step's gradients
+
+
+@pytest.mark.parametrize("B", [1 << 16, 40001])
+def test_pageable_streamed_steps_parity_and_invalid_last_chunk(B):
+    """Pageable host arrays (a reference caller's MatX / numpy) with B >= 2^15
+    are streamed through pinned bounce buffers filled by host copy threads:
+    losses match the oracle step by step, an inf in the LAST chunk leaves the
+    state untouched, and the caller's arrays are not read after the call."""
+    nf = _nf()
+    from paper_2201_05989_b200._lib import NfgInvalidArgument
+    g = _grid(nf, dims=3, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=512)
+    m = _model(nf, g, hidden_layers=2, table_fp32=True, lr=1e-3)
+    f = _oracle_field(m, lr=1e-3)
+    for step in range(1, 4):   # step 1 warms the field up (plain path), steps 2-3 stream
+        X = np.ascontiguousarray(_points(B, 3, seed=30 + step))
+        T = np.ascontiguousarray(O.csg_sdf(X).reshape(B, 1).astype(np.float32))
+        lg = m.train_step_host_ptr(X.ctypes.data, T.ctypes.data, B, nf.LossKind.Mape, step)
+        X[:] = 2.0   # scribbling over the arrays after the call must not matter
+        lo = f.train_step(_points(B, 3, seed=30 + step), T.copy(), O.LOSS_MAPE, step)
+        assert abs(lg - lo) <= 1e-3 * abs(lo), (step, lg, lo)
+    before = m.params
+    _, m0, v0 = m.adam_state()
+    X = np.ascontiguousarray(_points(B, 3, seed=40))
+    T = np.ascontiguousarray(O.csg_sdf(X).reshape(B, 1).astype(np.float32))
+    X[B - 3, 1] = np.inf
+    with pytest.raises(NfgInvalidArgument, match="non-finite"):
+        m.train_step_host_ptr(X.ctypes.data, T.ctypes.data, B, nf.LossKind.Mape, 4)
+    assert np.array_equal(m.params, before) and (m.grads == 0).all() and m.step == 3
+    _, m1, v1 = m.adam_state()
+    assert np.array_equal(m0, m1) and np.array_equal(v0, v1)
+    X[B - 3, 1] = 0.5
+    lg = m.train_step_host_ptr(X.ctypes.data, T.ctypes.data, B, nf.LossKind.Mape, 4)
+    lo = f.train_step(X.copy(), T.copy(), O.LOSS_MAPE, 4)
+    assert abs(lg - lo) <= 1e-3 * abs(lo), (lg, lo)
+
+
+def test_train_step_global_normalises_by_global_batch():
+    """nfg_field_train_step_global (SURVEY §8b signature): a shard of B samples
+    in a global batch of 3B contributes loss and gradients scaled by B / 3B
+    (losses.hpp:16 count = whole batch), identical to the oracle's gradient of
+    the same shard scaled by 1/3."""
+    nf = _nf()
+    g = _grid(nf, dims=3, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=512)
+    m = _model(nf, g, hidden_layers=2, table_fp32=True, lr=1e-3)
+    f = _oracle_field(m, lr=1e-3)
+    B = 5000
+    X = np.ascontiguousarray(_points(B, 3, seed=50))
+    T = np.ascontiguousarray(O.csg_sdf(X).reshape(B, 1).astype(np.float32))
+    lg = m.train_step_host_ptr(X.ctypes.data, T.ctypes.data, B, nf.LossKind.Mape, 1, B_global=3 * B)
+    lo = f.train_step(X.copy(), T.copy(), O.LOSS_MAPE, 1)
+    assert abs(3.0 * lg - lo) <= 1e-4 * abs(lo), (lg, lo)
+    with pytest.raises(ValueError):
+        m.train_step_host_ptr(X.ctypes.data, T.ctypes.data, B, nf.LossKind.Mape, 2, B_global=B - 1)
