@@ -102,7 +102,7 @@ public:
     MlpCfg mlp_cfg;
     Hyper hyper;
     Schedule schedule;
-    nfg_options options{ 0, 1, 0 };
+    nfg_options options{ 0, 1, 0, 0 };
 
     explicit FieldModelT(Context& ctx) : ctx_(ctx) {}
     ~FieldModelT()

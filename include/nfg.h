@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define NFG_ABI_VERSION 2
+#define NFG_ABI_VERSION 3
 
 typedef enum {
     NFG_OK = 0,
@@ -98,7 +98,13 @@ typedef struct {
     int32_t deterministic; /* 1: run-to-run bit-reproducible backward: table gradients accumulate per
                               row in the reference's order (grid.hpp:286-294; bit-identical to it for equal dY),
                               MLP gradients and the loss sum reduce per-CTA partials in a fixed order. Slower. */
+    int32_t mlp_engine;    /* tensor-core engine of the fused kernels' MLP (north star: "mma.sync or tcgen05,
+                              whichever is faster at width 64"): NFG_MMA_DEFAULT picks the measured-faster one per
+                              kernel, NFG_MMA_SYNC / NFG_MMA_TCGEN05 force one. Kernels or shapes
+                              without a tcgen05 build use mma.sync. */
 } nfg_options;
+
+enum { NFG_MMA_DEFAULT = 0, NFG_MMA_SYNC = 1, NFG_MMA_TCGEN05 = 2 };
 
 typedef struct nfg_ctx nfg_ctx;
 typedef struct nfg_field nfg_field;

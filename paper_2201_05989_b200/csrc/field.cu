@@ -350,7 +350,7 @@ struct nfg_field {
     nfg_grid_config gcfg{};
     nfg_mlp_config mcfg{};
     nfg_adam_hyper hyper{ 1e-2, 0.9, 0.99, 1e-15, 1e-6 };
-    nfg_options opts{ 0, 1, 0 };
+    nfg_options opts{ 0, 1, 0, 0 };
     std::vector<int64_t> milestones;
     double factor = 0.33;
     std::vector<nfg_level_spec> levels;
@@ -792,9 +792,11 @@ nfg::FieldShape make_shape(const nfg_grid_config& g, const nfg_mlp_config& m, co
     s.in_real = g.levels * g.features;
     s.in_steps = (s.in_real + 15) / 16;
     s.hidden_layers = m.hidden_layers;
+    s.hidden_width = m.hidden_width;
     s.n_out = m.output_width;
     s.sigmoid = m.output_activation == NFG_ACT_SIGMOID;
     s.table_fp32 = o.table_fp32;
+    s.mlp_engine = o.mlp_engine;
     for (size_t l = 0; l < lv.size() && l < NFG_MAX_LEVELS; ++l) {
         nfg::LevelDev& d = s.grid.lv[l];
         d.res = lv[l].resolution;
@@ -1050,8 +1052,10 @@ nfg_status nfg_field_create(nfg_ctx* ctx, const nfg_grid_config* grid, const nfg
             nfg::host::validate(f->gcfg);
             nfg::host::validate(f->mcfg);
             nfg::host::validate(f->hyper);
-            if (f->mcfg.hidden_width != 64)
-                throw Fail{ NFG_EUNSUPPORTED, "sm_100a MLP is built for hidden_width == 64 only" };
+            require(f->opts.mlp_engine >= NFG_MMA_DEFAULT && f->opts.mlp_engine <= NFG_MMA_TCGEN05,
+                    "nfg_options.mlp_engine must be NFG_MMA_DEFAULT, NFG_MMA_SYNC or NFG_MMA_TCGEN05");
+            if (f->mcfg.hidden_width > 64)
+                throw Fail{ NFG_EUNSUPPORTED, "sm_100a MLP is built for hidden_width <= 64" };
             if (f->mcfg.hidden_layers < 1 || f->mcfg.hidden_layers > 3)
                 throw Fail{ NFG_EUNSUPPORTED, "sm_100a MLP is built for 1..3 hidden layers" };
             if (f->mcfg.output_width > 16)

@@ -227,7 +227,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
 #endif
     if (a.scratch.flags[3] != 0u)
         return;   // invalid input (k_validate): the reference throws before any update
-    const MlpShape msh{ s.in_real, s.n_out, s.sigmoid };
+    const MlpShape msh{ s.in_real, s.n_out, s.sigmoid, s.hidden_width };
     load_weights<IN_STEPS, NH>(ws, bs, a.W, a.b, msh);
     if (SRC == SRC_ENCODE)
         for (int i = tid; i < s.grid.L; i += blockDim.x)
@@ -637,6 +637,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     NFG_PT_FLUSH();
     // ---- flush per-CTA dW / db (x 1/count) ----------------------------------
     const float ic = a.inv_count;
+    const int hw = s.hidden_width;
     auto flush = [&](const float (&cq)[2][4], int mt, int np, int out_k, int in_k, size_t woff) {
 #ifdef NFG_EXP_NO_FLUSH   // experiment builds only (tools/kbench.cu): upper bound of the dW flush cost
         return;
@@ -662,17 +663,17 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         for (int c = 0; c < C0; ++c) {
             const int p = warp + c * TW;
             if (p < P0)
-                flush(dw0[c], p / IN_STEPS, p % IN_STEPS, H, s.in_real, 0);
+                flush(dw0[c], p / IN_STEPS, p % IN_STEPS, hw, s.in_real, 0);
         }
 #pragma unroll
         for (int k = 1; k < NH; ++k)
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
                 const int p = warp + c * TW;
-                flush(dwh[k - 1][c], p / 4, p % 4, H, H, size_t(H) * s.in_real + size_t(k - 1) * H * H);
+                flush(dwh[k - 1][c], p / 4, p % 4, hw, hw, size_t(hw) * s.in_real + size_t(k - 1) * hw * hw);
             }
         if (warp < PO)
-            flush(dwo, 0, warp, s.n_out, H, size_t(H) * s.in_real + size_t(NH - 1) * H * H);
+            flush(dwo, 0, warp, s.n_out, hw, size_t(hw) * s.in_real + size_t(NH - 1) * hw * hw);
     }
     if (t == 0) {
         if (warp < 4)
@@ -680,12 +681,15 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             for (int k = 0; k < NH; ++k)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
+                    const int j = 16 * warp + g + 8 * h;
+                    if (j >= hw)
+                        continue;
                     const float v = dbh[k][h] * ic;
                     bad |= !sane(v);
                     if (a.part_wb)
-                        a.part_wb[blockIdx.x * a.n_wb + a.n_w + k * H + 16 * warp + g + 8 * h] = v;
+                        a.part_wb[blockIdx.x * a.n_wb + a.n_w + k * hw + j] = v;
                     else
-                        atomicAdd(a.gb + k * H + 16 * warp + g + 8 * h, v);
+                        atomicAdd(a.gb + k * hw + j, v);
                 }
         if (warp == TW - 1)
 #pragma unroll
@@ -694,9 +698,9 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                     const float v = dbo[h] * ic;
                     bad |= !sane(v);
                     if (a.part_wb)
-                        a.part_wb[blockIdx.x * a.n_wb + a.n_w + NH * H + g + 8 * h] = v;
+                        a.part_wb[blockIdx.x * a.n_wb + a.n_w + NH * hw + g + 8 * h] = v;
                     else
-                        atomicAdd(a.gb + NH * H + g + 8 * h, v);
+                        atomicAdd(a.gb + NH * hw + g + 8 * h, v);
                 }
     }
     if (GRAD == GRAD_LOSS && a.part_loss && lane == 0)
@@ -721,7 +725,7 @@ k_infer(const InferArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     float* bs = reinterpret_cast<float*>(sm + Lay::HALVES * 2);
     LevelDev* lvs = reinterpret_cast<LevelDev*>(sm + SM::LV_OFF);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-    const MlpShape msh{ s.in_real, s.n_out, s.sigmoid };
+    const MlpShape msh{ s.in_real, s.n_out, s.sigmoid, s.hidden_width };
     load_weights<IN_STEPS, NH>(ws, bs, a.W, a.b, msh);
     if (SRC == SRC_ENCODE)
         for (int i = tid; i < s.grid.L; i += blockDim.x)

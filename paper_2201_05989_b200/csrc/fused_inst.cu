@@ -1,12 +1,19 @@
 // fused_inst.cu — sm_100a instantiations of the fused encode+MLP kernels for
 // one input dimensionality (compiled twice: -DNFG_D=2 and -DNFG_D=3).
 #include "launch_impl.cuh"
+#include "../../include/nfg.h"
 
 #ifndef NFG_D
 #error "compile with -DNFG_D=2 or -DNFG_D=3"
 #endif
 #define NFG_CAT2(a, b) a##b
 #define NFG_CAT(a, b) NFG_CAT2(a, b)
+
+// Default engine of the fused inference kernel (nfg_options.mlp_engine ==
+// NFG_MMA_DEFAULT): the measured-faster one.
+#ifndef NFG_INFER_TC_DEFAULT
+#define NFG_INFER_TC_DEFAULT 0
+#endif
 
 namespace nfg {
 
@@ -70,9 +77,11 @@ cudaError_t NFG_CAT(launch_fused_infer_d, NFG_D)(const FieldShape& s, const Leve
                                                  int num_sms, cudaStream_t st)
 {
     const bool f32 = s.table_fp32 != 0;
+    const bool tc = s.mlp_engine == NFG_MMA_TCGEN05 || (s.mlp_engine == NFG_MMA_DEFAULT && NFG_INFER_TC_DEFAULT);
 #define X(F_, TT_, IS_, NH_)                                                                               \
     if (s.grid.F == F_ && f32 == (sizeof(TT_) == 4) && s.in_steps == IS_ && s.hidden_layers == NH_)         \
-        return run_infer<SRC_ENCODE, NFG_D, F_, TT_, IS_, NH_>(s, lv, a, num_sms, st);
+        return tc ? run_infer_tc<SRC_ENCODE, NFG_D, F_, TT_, IS_, NH_>(s, lv, a, num_sms, st)                 \
+                  : run_infer<SRC_ENCODE, NFG_D, F_, TT_, IS_, NH_>(s, lv, a, num_sms, st);
     NFG_FUSED_LIST(X)
 #undef X
     return cudaErrorNotSupported;

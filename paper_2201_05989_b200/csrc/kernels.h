@@ -14,9 +14,11 @@ struct FieldShape {
     int in_real;       // L*F
     int in_steps;      // ceil(in_real / 16)
     int hidden_layers;
+    int hidden_width;  // reference hidden_width (<= 64; the kernels pad to 64 with exact zeros)
     int n_out;
     int sigmoid;
     int table_fp32;
+    int mlp_engine;    // nfg_options.mlp_engine (NFG_MMA_*)
 };
 
 // Gradient-side device scratch of one training step.

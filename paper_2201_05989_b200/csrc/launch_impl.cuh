@@ -6,6 +6,7 @@
 #include <cstdlib>
 
 #include "field_kernels.cuh"
+#include "infer_tc.cuh"
 
 namespace nfg {
 
@@ -74,6 +75,33 @@ cudaError_t run_infer(const FieldShape& s, const LevelDev* lv, const InferArgs& 
     const int64_t want = (tiles + IW - 1) / IW;
     const int grid = int(std::min<int64_t>(want, int64_t(num_sms) * per_sm));
     k<<<grid, IW * 32, SM::BYTES, st>>>(a, s, lv);
+    return cudaGetLastError();
+}
+
+template <int SRC, int D, int F, typename TT, int IS, int NH>
+cudaError_t run_infer_tc(const FieldShape& s, const LevelDev* lv, const InferArgs& a, int num_sms, cudaStream_t st)
+{
+    using SM = InferTcSmem<IS, NH>;
+    auto k = k_infer_tc<SRC, D, F, TT, IS, NH>;
+    static bool ready = false;
+    if (!ready) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
+        if (e != cudaSuccess)
+            return e;
+        ready = true;
+    }
+    static char desc[160];
+    if (!desc[0])
+        snprintf(desc, sizeof(desc), "k_infer_tc src=%d d=%d F=%d table=%s in_steps=%d hidden=%d quads=%d mma=tcgen05",
+                 SRC, D, F, sizeof(TT) == 2 ? "f16" : "f32", IS, NH, IQ);
+    note_kernel_variant(1, desc);
+    const int64_t tiles = (a.B + 127) / 128;
+    if (tiles <= 0)
+        return cudaSuccess;
+    // one CTA per SM (it allocates the SM's TMEM columns for its quads); tiles
+    // are dealt round-robin over the SMs first
+    const int grid = int(std::min<int64_t>(tiles, num_sms));
+    k<<<grid, IQ * 128, SM::BYTES, st>>>(a, s, lv);
     return cudaGetLastError();
 }
 

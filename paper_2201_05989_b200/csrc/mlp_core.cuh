@@ -80,39 +80,42 @@ struct MlpShape {
     int in_real;     // L*F (reference input_width)
     int n_out;       // reference output_width (<= 16)
     int sigmoid;
+    int hw;          // reference hidden_width (<= 64): the 64-wide layers carry zero rows / columns
+                     // beyond it, which are exact no-ops (ReLU(0) = 0 and a zero dz) forward and backward
 };
 
 // Converts the fp32 master weights (reference layout: W_k out x in column-major,
-// then biases) into the padded fp16 [out][in] smem image. All threads.
+// then biases; hidden width sh.hw) into the padded fp16 [out][in] smem image
+// (64-wide, zero beyond sh.hw). All threads.
 template <int IN_STEPS, int NH>
 __device__ void load_weights(__half* ws, float* bs, const float* __restrict__ W, const float* __restrict__ b,
                              const MlpShape& sh)
 {
     using Lay = WLayout<IN_STEPS, NH>;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    // layer 0: 64 x in_real
+    const int tid = threadIdx.x, nt = blockDim.x, hw = sh.hw;
+    // layer 0: hw x in_real
     for (int i = tid; i < H * Lay::INS; i += nt) {
         const int o = i / Lay::INS, c = i % Lay::INS;
-        ws[i] = __float2half_rn(c < sh.in_real ? W[o + c * H] : 0.0f);
+        ws[i] = __float2half_rn(c < sh.in_real && o < hw ? W[o + c * hw] : 0.0f);
     }
-    size_t woff = size_t(H) * sh.in_real;
+    size_t woff = size_t(hw) * sh.in_real;
     for (int k = 0; k < NH - 1; ++k) {
         __half* dst = ws + Lay::W0_HALVES + k * Lay::WH_HALVES;
         for (int i = tid; i < H * HS; i += nt) {
             const int o = i / HS, c = i % HS;
-            dst[i] = __float2half_rn(c < H ? W[woff + o + c * H] : 0.0f);
+            dst[i] = __float2half_rn(c < hw && o < hw ? W[woff + o + c * hw] : 0.0f);
         }
-        woff += size_t(H) * H;
+        woff += size_t(hw) * hw;
     }
     __half* wo = ws + Lay::W0_HALVES + (NH - 1) * Lay::WH_HALVES;
     for (int i = tid; i < OUTP * HS; i += nt) {
         const int o = i / HS, c = i % HS;
-        wo[i] = __float2half_rn((c < H && o < sh.n_out) ? W[woff + o + c * sh.n_out] : 0.0f);
+        wo[i] = __float2half_rn((c < hw && o < sh.n_out) ? W[woff + o + c * sh.n_out] : 0.0f);
     }
     for (int i = tid; i < H * NH; i += nt)
-        bs[i] = b[i];
+        bs[i] = (i % H) < hw ? b[(i / H) * hw + (i % H)] : 0.0f;
     for (int i = tid; i < OUTP; i += nt)
-        bs[H * NH + i] = i < sh.n_out ? b[H * NH + i] : 0.0f;
+        bs[H * NH + i] = i < sh.n_out ? b[hw * NH + i] : 0.0f;
 }
 
 // acc[NT] = A (16 x 16*KS) * W^T where W is [8*NT rows][wstride] in smem.

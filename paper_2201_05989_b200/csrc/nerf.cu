@@ -762,7 +762,7 @@ nfg_status nfg_nerf_create(nfg_ctx* ctx, const nfg_nerf_config* cfg, uint64_t se
         if (g.levels * g.features != 32)
             throw Fail{ NFG_EUNSUPPORTED, "nerf: the density encoding must have levels * features == 32" };
         nfg_adam_hyper hy{ cfg->lr, 0.9, 0.99, 1e-15, 1e-6 };
-        nfg_options o{ 0, 1, 0 };
+        nfg_options o{ 0, 1, 0, 0 };
         // density MLP: 1 hidden layer of 64 -> 16 outputs, the first is log-density
         nfg_mlp_config md{ 0, 1, 64, 16, NFG_ACT_LINEAR };
         ok(nfg_field_create(ctx, &g, &md, &hy, &o, &n->density));

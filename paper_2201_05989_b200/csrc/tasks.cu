@@ -424,7 +424,7 @@ nfg_status nfg_fit_image(nfg_ctx* ctx, const nfg_image_task* task, const float* 
         m.output_width = 3;
         m.output_activation = NFG_ACT_SIGMOID;
         nfg_adam_hyper hy{ task->lr, 0.9, 0.99, 1e-15, 1e-6 };
-        nfg_options o = opts ? *opts : nfg_options{ 0, 1, 0 };
+        nfg_options o = opts ? *opts : nfg_options{ 0, 1, 0, 0 };
         nfg_field* f = nullptr;
         ok(nfg_field_create(ctx, &g, &m, &hy, &o, &f));
         std::unique_ptr<nfg_field, nfg_status (*)(nfg_field*)> model(f, nfg_field_destroy);
@@ -575,7 +575,7 @@ nfg_status nfg_fit_sdf_analytic(nfg_ctx* ctx, const nfg_sdf_task* task, uint64_t
         m.output_width = 1;
         m.output_activation = NFG_ACT_LINEAR;
         nfg_adam_hyper hy{ task->lr, 0.9, 0.99, 1e-15, 1e-6 };
-        nfg_options o = opts ? *opts : nfg_options{ 0, 1, 0 };
+        nfg_options o = opts ? *opts : nfg_options{ 0, 1, 0, 0 };
         nfg_field* f = nullptr;
         ok(nfg_field_create(ctx, &g, &m, &hy, &o, &f));
         std::unique_ptr<nfg_field, nfg_status (*)(nfg_field*)> model(f, nfg_field_destroy);

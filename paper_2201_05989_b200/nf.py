@@ -15,7 +15,7 @@ Names, argument meaning and error behaviour follow
 
 Errors: ``ValueError`` (std::invalid_argument), ``NfgNonFinite``
 (std::runtime_error from adam_step), ``NfgUnsupported`` (valid for the
-reference but not built for sm_100a, e.g. hidden_width != 64).
+reference but not built for sm_100a, e.g. hidden_width > 64).
 """
 from __future__ import annotations
 
@@ -194,9 +194,11 @@ class Options:
     table_fp32: bool = False    # gather fp32 master tables instead of the fp16 shadow
     fused_train: bool = True    # one fused kernel per step vs staged encode / MLP / encode-bwd kernels
     deterministic: bool = False  # bit-reproducible backward in the reference's accumulation order
+    mlp_engine: int = 0         # 0: measured-faster tensor-core engine per kernel, 1: mma.sync, 2: tcgen05
 
     def c(self) -> L.nfg_options:
-        return L.nfg_options(int(self.table_fp32), int(self.fused_train), int(self.deterministic))
+        return L.nfg_options(int(self.table_fp32), int(self.fused_train), int(self.deterministic),
+                             int(self.mlp_engine))
 
 
 class Context:

@@ -349,7 +349,7 @@ def test_invalid_and_unsupported():   # grid.hpp:224-229, NFG_EUNSUPPORTED
         m.evaluate(np.zeros((3, 3), np.float32))
     bad = nf.FieldModel()
     bad.hash_cfg = g
-    bad.mlp_cfg = nf.MlpConfig(hidden_width=32)
+    bad.mlp_cfg = nf.MlpConfig(hidden_width=128)
     with pytest.raises(NfgUnsupported):
         bad.init(1)
 
