@@ -458,6 +458,194 @@ void mlp_bwd(const MlpCfg& c, const S* W, const MlpCache<S>& cache, const S* dOu
 }
 
 // ---------------------------------------------------------------------------
+// Throughput stand-in for the reference's Eigen GEMMs (mlp.hpp:114,147-149),
+// used ONLY by the CPU-baseline timing (Field::fast_mlp; bench.py's
+// cpu_baseline / --impl reference legs). Same math, cache-blocked over
+// 8-sample panels with FMA contraction (the reference builds with
+// -O2 -march=native, proj/CMakeLists.txt:9, where Eigen issues FMAs); the
+// parity oracle above keeps its fixed summation order. fp32 only.
+// ---------------------------------------------------------------------------
+#pragma GCC push_options
+#pragma GCC optimize("O3", "fp-contract=fast")
+namespace fast {
+
+typedef float v8 __attribute__((vector_size(32)));
+
+inline v8 ld8(const float* p)
+{
+    v8 v;
+    std::memcpy(&v, p, sizeof(v));
+    return v;
+}
+inline void st8(float* p, v8 v) { std::memcpy(p, &v, sizeof(v)); }
+inline v8 bc8(float x) { return v8{ x, x, x, x, x, x, x, x }; }
+
+// C[m][n] (+)= sum_k A[m*lda + k] * Bm[k*ldb + n] for a 6 x 16 block (BLIS-style
+// register tile: 12 accumulators, two B vectors, one broadcast per row).
+inline void kernel_6x16(int K, const float* A, std::int64_t lda, const float* Bm, std::int64_t ldb, float* C,
+                        std::int64_t ldc, int mrows, bool accumulate)
+{
+    v8 c[6][2];
+    for (int r = 0; r < 6; ++r)
+        for (int v = 0; v < 2; ++v)
+            c[r][v] = (accumulate && r < mrows) ? ld8(C + r * ldc + 8 * v) : bc8(0.0f);
+    for (int k = 0; k < K; ++k) {
+        const v8 b0 = ld8(Bm + k * ldb), b1 = ld8(Bm + k * ldb + 8);
+        for (int r = 0; r < 6; ++r) {
+            const v8 a = bc8(r < mrows ? A[r * lda + k] : 0.0f);
+            c[r][0] += a * b0;
+            c[r][1] += a * b1;
+        }
+    }
+    for (int r = 0; r < mrows; ++r)
+        for (int v = 0; v < 2; ++v)
+            st8(C + r * ldc + 8 * v, c[r][v]);
+}
+
+// Z (B x out, sample-major) = A (B x in) W^T + b; Wt is W^T (in x out, out-contiguous
+// = the reference's column-major W itself).
+inline void dense(const float* W, const float* b, const float* A, std::int64_t B, int in, int out, float* Z)
+{
+    const int n16 = out / 16 * 16;
+#pragma omp parallel for schedule(static)
+    for (std::int64_t s0 = 0; s0 < B; s0 += 6) {
+        const int ms = int(std::min<std::int64_t>(6, B - s0));
+        for (int o0 = 0; o0 < n16; o0 += 16)
+            kernel_6x16(in, A + s0 * in, in, W + o0, out, Z + s0 * out + o0, out, ms, false);
+        for (int r = 0; r < ms; ++r) {
+            float* z = Z + (s0 + r) * out;
+            for (int o = n16; o < out; ++o) {
+                float acc = 0.0f;
+                for (int i = 0; i < in; ++i)
+                    acc += A[(s0 + r) * in + i] * W[std::size_t(i) * out + o];
+                z[o] = acc;
+            }
+            for (int o = 0; o < out; ++o)
+                z[o] += b[o];
+        }
+    }
+}
+
+inline void mlp_fwd(const MlpCfg& c, const float* W, const float* b, const float* Y, std::int64_t B, float* out,
+                    MlpCache<float>& cache)
+{
+    MlpLayout lay(c);
+    const int n = c.layers();
+    cache.acts.assign(1, std::vector<float>(Y, Y + B * c.in));
+    std::vector<float> z;
+    for (int k = 0; k < n; ++k) {
+        const int in = c.in_of(k), o = c.out_of(k);
+        z.resize(std::size_t(B) * o);
+        dense(W + lay.w_off[std::size_t(k)], b + lay.b_off[std::size_t(k)], cache.acts.back().data(), B, in, o,
+              z.data());
+        if (k + 1 < n) {
+            for (auto& v : z)
+                v = std::max(v, 0.0f);
+            cache.acts.push_back(z);
+        }
+    }
+    if (c.sigmoid)
+        for (auto& v : z)
+            v = 1.0f / (1.0f + std::exp(-v));
+    cache.acts.push_back(z);
+    std::copy(z.begin(), z.end(), out);
+}
+
+inline void mlp_bwd(const MlpCfg& c, const float* W, const MlpCache<float>& cache, const float* dOut,
+                    std::int64_t B, float* gW, float* gb, float* dY)
+{
+    MlpLayout lay(c);
+    const int n = c.layers();
+    const std::vector<float>& outp = cache.acts.back();
+    std::vector<float> dz(dOut, dOut + B * c.out);
+    if (c.sigmoid)
+        for (std::size_t i = 0; i < dz.size(); ++i)
+            dz[i] = dz[i] * (outp[i] * (1.0f - outp[i]));
+    for (int k = n - 1; k >= 0; --k) {
+        const int in = c.in_of(k), o = c.out_of(k);
+        const float* A = cache.acts[std::size_t(k)].data();
+        const float* w = W + lay.w_off[std::size_t(k)];
+        float* gw = gW + lay.w_off[std::size_t(k)];
+        float* gbk = gb + lay.b_off[std::size_t(k)];
+        // W^T copy (in-contiguous rows per output) for da = dz W
+        std::vector<float> wt(std::size_t(in) * o);
+        for (int i = 0; i < in; ++i)
+            for (int q = 0; q < o; ++q)
+                wt[std::size_t(q) * in + i] = w[q + std::size_t(i) * o];
+        std::vector<float> da(std::size_t(B) * in);
+        const int nt = omp_get_max_threads();
+        std::vector<float> part(std::size_t(nt) * (std::size_t(in) * o + o), 0.0f);
+        const bool wide = o % 16 == 0;
+#pragma omp parallel
+        {
+            const int tid = omp_get_thread_num();
+            float* pg = part.data() + std::size_t(tid) * (std::size_t(in) * o + o);
+            float* pb = pg + std::size_t(in) * o;
+            const std::int64_t chunk = (B + nt - 1) / nt, lo = std::min<std::int64_t>(B, tid * chunk),
+                               hi = std::min<std::int64_t>(B, lo + chunk);
+            // gW^T (in x o) += A^T dz over this thread's samples: M = in, N = o, K = samples
+            if (wide) {
+                std::vector<float> at(std::size_t(in) * 256);
+                for (std::int64_t s0 = lo; s0 < hi; s0 += 256) {
+                    const int ks = int(std::min<std::int64_t>(256, hi - s0));
+                    for (int r = 0; r < ks; ++r)   // transpose the panel: at[i][r]
+                        for (int i = 0; i < in; ++i)
+                            at[std::size_t(i) * 256 + r] = A[(s0 + r) * in + i];
+                    for (int i0 = 0; i0 < in; i0 += 6)
+                        for (int q0 = 0; q0 < o; q0 += 16)
+                            kernel_6x16(ks, at.data() + std::size_t(i0) * 256, 256, dz.data() + s0 * o + q0, o,
+                                        pg + std::size_t(i0) * o + q0, o, std::min(6, in - i0), true);
+                }
+            } else {
+                for (std::int64_t s = lo; s < hi; ++s)
+                    for (int i = 0; i < in; ++i) {
+                        const float a = A[s * in + i];
+                        for (int q = 0; q < o; ++q)
+                            pg[std::size_t(i) * o + q] += dz[std::size_t(s) * o + q] * a;
+                    }
+            }
+            for (std::int64_t s = lo; s < hi; ++s)
+                for (int q = 0; q < o; ++q)
+                    pb[q] += dz[std::size_t(s) * o + q];
+            // da (B x in) = dz (B x o) W (o x in): B-operand = wt (o x in, in-contiguous)
+            for (std::int64_t s0 = lo; s0 < hi; s0 += 6) {
+                const int ms = int(std::min<std::int64_t>(6, hi - s0));
+                if (in % 16 == 0) {
+                    for (int i0 = 0; i0 < in; i0 += 16)
+                        kernel_6x16(o, dz.data() + s0 * o, o, wt.data() + i0, in, da.data() + s0 * in + i0, in, ms,
+                                    false);
+                } else {
+                    for (int r = 0; r < ms; ++r)
+                        for (int i = 0; i < in; ++i) {
+                            float acc = 0.0f;
+                            for (int q = 0; q < o; ++q)
+                                acc += dz[std::size_t(s0 + r) * o + q] * wt[std::size_t(q) * in + i];
+                            da[std::size_t(s0 + r) * in + i] = acc;
+                        }
+                }
+            }
+        }
+        for (int t = 0; t < nt; ++t) {
+            const float* pg = part.data() + std::size_t(t) * (std::size_t(in) * o + o);
+            for (std::size_t e = 0; e < std::size_t(in) * o; ++e)
+                gw[e] += pg[e];
+            for (int q = 0; q < o; ++q)
+                gbk[q] += pg[std::size_t(in) * o + q];
+        }
+        if (k == 0) {
+            std::copy(da.begin(), da.end(), dY);
+        } else {
+            for (std::size_t i = 0; i < da.size(); ++i)
+                da[i] = A[i] > 0.0f ? da[i] : 0.0f;
+            dz.swap(da);
+        }
+    }
+}
+
+}   // namespace fast
+#pragma GCC pop_options
+
+// ---------------------------------------------------------------------------
 // Losses — losses.hpp:10-71. n = pred.size() (count over all outputs).
 // ---------------------------------------------------------------------------
 enum LossKind { L2 = 0, MAPE = 1, REL_L2 = 2 };
@@ -624,6 +812,7 @@ struct Field {
     std::vector<float> p, grad, mom, vel;
     std::uint64_t step = 0;
     PhaseTimes times;
+    bool fast_mlp = false;   // CPU-baseline timing only: the MLP through fast:: (Eigen stand-in)
 
     Field(const GridCfg& gc, const MlpCfg& mc) : g(gc), m(mc)
     {
@@ -658,7 +847,10 @@ struct Field {
         std::vector<float> Y(std::size_t(B) * g.L * g.F);
         encode_fwd<float>(g, lv, p.data(), X, B, Y.data(), nullptr, nullptr);
         MlpCache<float> cache;
-        mlp_fwd<float>(m, p.data() + n_tab, p.data() + n_tab + n_w, Y.data(), B, out, cache);
+        if (fast_mlp)
+            fast::mlp_fwd(m, p.data() + n_tab, p.data() + n_tab + n_w, Y.data(), B, out, cache);
+        else
+            mlp_fwd<float>(m, p.data() + n_tab, p.data() + n_tab + n_w, Y.data(), B, out, cache);
     }
 
     // model.cpp:111-138. Returns the loss; throws std::runtime_error from Adam.
@@ -680,13 +872,19 @@ struct Field {
         lap(times.encode_fwd);
         std::vector<float> pred(std::size_t(B) * m.out), dpred(pred.size()), dY(Y.size());
         MlpCache<float> cache;
-        mlp_fwd<float>(m, W(), b(), Y.data(), B, pred.data(), cache);
+        if (fast_mlp)
+            fast::mlp_fwd(m, W(), b(), Y.data(), B, pred.data(), cache);
+        else
+            mlp_fwd<float>(m, W(), b(), Y.data(), B, pred.data(), cache);
         lap(times.mlp_fwd);
         const float loss = loss_with_grad<float>(loss_kind, pred.data(), target,
                                                  std::int64_t(pred.size()), dpred.data());
         lap(times.loss);
-        mlp_bwd<float>(m, W(), cache, dpred.data(), B, grad.data() + n_tab,
-                       grad.data() + n_tab + n_w, dY.data());
+        if (fast_mlp)
+            fast::mlp_bwd(m, W(), cache, dpred.data(), B, grad.data() + n_tab, grad.data() + n_tab + n_w, dY.data());
+        else
+            mlp_bwd<float>(m, W(), cache, dpred.data(), B, grad.data() + n_tab, grad.data() + n_tab + n_w,
+                           dY.data());
         lap(times.mlp_bwd);
         encode_bwd<float>(g, lv, rows.data(), wts.data(), B, dY.data(), grad.data());
         lap(times.encode_bwd);

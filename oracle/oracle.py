@@ -101,6 +101,7 @@ def _declare(L: C.CDLL) -> None:
     d("orc_field_evaluate", C.c_int, _vp, _f32p, C.c_int64, _f32p)
     d("orc_field_times", None, _vp, _f64p)
     d("orc_field_reset_times", None, _vp)
+    d("orc_field_set_fast_mlp", None, _vp, C.c_int)
     d("orc_rng_create", _vp, C.c_uint64, C.c_uint64)
     d("orc_rng_destroy", None, _vp)
     d("orc_rng_u32", C.c_uint32, _vp)
@@ -508,6 +509,11 @@ class Field:
 
     def reset_times(self) -> None:
         self._lib.orc_field_reset_times(self.h)
+
+    def set_fast_mlp(self, on: bool = True) -> None:
+        """CPU-baseline timing only: the MLP through cache-blocked FMA GEMMs
+        standing in for the reference's Eigen GEMMs (nf_oracle.hpp fast::)."""
+        self._lib.orc_field_set_fast_mlp(self.h, int(on))
 
 
 # --------------------------------------------------------------------------

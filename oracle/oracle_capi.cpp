@@ -341,6 +341,8 @@ void orc_field_times(void* h, double* out6)
     out6[5] = t.adam;
 }
 void orc_field_reset_times(void* h) { static_cast<FieldHandle*>(h)->f.times = orc::PhaseTimes{}; }
+// CPU-baseline timing only: route the MLP through the blocked FMA GEMMs (fast::).
+void orc_field_set_fast_mlp(void* h, int on) { static_cast<FieldHandle*>(h)->f.fast_mlp = on != 0; }
 
 // ---- rng / fixtures -----------------------------------------------------
 void* orc_rng_create(std::uint64_t seed, std::uint64_t seq) { return new RngHandle{ orc::Pcg(seed, seq) }; }

@@ -351,6 +351,7 @@ struct nfg_field {
     nfg_mlp_config mcfg{};
     nfg_adam_hyper hyper{ 1e-2, 0.9, 0.99, 1e-15, 1e-6 };
     nfg_options opts{ 0, 1, 0, 0 };
+    int train_grid = 0;   // CTAs of the last fused train launch (the persistent kernel's first wave)
     std::vector<int64_t> milestones;
     double factor = 0.33;
     std::vector<nfg_level_spec> levels;
@@ -686,7 +687,7 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
         Span span(c, 0);
         if (fused) {
             NFG_CUDA(nfg::launch_train(f->shape, f->d_levels, nfg::SRC_ENCODE, nfg::GRAD_LOSS, nfg::SINK_SCATTER, a,
-                                       c->num_sms, c->stream, nullptr));
+                                       c->num_sms, c->stream, &f->train_grid));
             c->launches++;
         } else if (f->opts.deterministic) {
             const size_t LF = size_t(f->shape.in_real);
@@ -1314,13 +1315,16 @@ static void host_train_step(nfg_field* f, const float* X, const float* target, i
         float* dX = static_cast<float*>(c->s0.get(size_t(B) * d * 4));
         float* dT = static_cast<float*>(c->s1.get(size_t(B) * no * 4));
         // a first chunk covering the persistent kernel's first wave of tiles
-        // (2 CTAs x 64 samples per SM; NFG_STREAM_CHUNK0 overrides), then
-        // NFG_STREAM_CHUNKS - 1 equal chunks
+        // (its CTAs x 64 samples, known from the plain step that precedes
+        // streaming; NFG_STREAM_CHUNK0 overrides), then NFG_STREAM_CHUNKS - 1
+        // equal chunks
         static const int64_t chunk0_env = [] {
             const char* e = getenv("NFG_STREAM_CHUNK0");
             return e ? int64_t(atoll(e)) : int64_t(0);
         }();
-        const int64_t chunk0 = std::min<int64_t>(B, chunk0_env > 0 ? chunk0_env : int64_t(c->num_sms) * 128);
+        const int64_t wave = f->train_grid > 0 ? int64_t(f->train_grid) * nfg::train_warps_per_cta() * 16
+                                               : int64_t(c->num_sms) * 128;
+        const int64_t chunk0 = std::min<int64_t>(B, chunk0_env > 0 ? chunk0_env : wave);
         const int64_t chunk = std::max<int64_t>(4096, (B - chunk0 + NFG_STREAM_CHUNKS - 2) / (NFG_STREAM_CHUNKS - 1));
         const int64_t nchunks = 1 + (B - chunk0 + chunk - 1) / chunk;
         const float* srcX = X;

@@ -21,9 +21,12 @@
 // MLP -> output activation (model.cpp:102-109).
 #pragma once
 
+#include <type_traits>
+
 #include "encode.cuh"
 #include "kernels.h"
 #include "mlp_core.cuh"
+#include "tc_core.cuh"
 
 namespace nfg {
 
@@ -103,6 +106,98 @@ struct StageAlias {
     static constexpr bool ON = !PREFETCH && SRC == SRC_ENCODE && NH >= 2 && SG::SB == 4 && 32 * SG::SB <= 2 * H &&
                                ELEMS <= 4 * ROWS;
 #endif
+};
+
+// ---- tcgen05 dW (k_train<..., TCW = true>) -----------------------------------
+// The per-warp forward / backward chains stay on mma.sync with activations in
+// registers (they feed straight from the encode and into the scatter); the
+// CTA-wide dW / db reductions over the tile's TS samples run on tcgen05 with the
+// accumulators in TMEM across all tiles of the CTA (instead of 62 registers per
+// thread). The tile's activations and dz are kept in shared memory in the
+// canonical MN-major operand layout with the samples as K:
+//   element (feature f, sample s) at (f / 8) * KC_SBO + (s / 8) * 128 + (s % 8) * 16 + (f % 8) * 2
+// (core matrices of 8 samples x 8 features; LBO = 128 B between sample blocks,
+// SBO = KC_SBO between feature blocks). Layer k's dW^T | db accumulates as
+// D_k[unit][in | 1] += dz_k^T act_k (M = 64; the activation buffers carry a
+// block whose first feature is 1, so the bias gradient is column `in`); the
+// output layer accumulates transposed, D[hidden][out] += act^T dz_out (M = 64,
+// N = 16). M = 64 accumulators occupy TMEM lanes 0-15 (or 16-31, "interleaved")
+// of each 32-lane subpartition: slot k uses lane half k & 1, columns 72 (k >> 1).
+// Validated on the hardware by tools/tc_probe.cu.
+constexpr int KC_SBO = TS / 8 * 128;
+
+__device__ __forceinline__ int kc_off(int f, int smp)
+{
+    return (f >> 3) * KC_SBO + (smp >> 3) * 128 + (smp & 7) * 16 + (f & 7) * 2;
+}
+
+// Stores an A-fragment block (samples row0 .. row0+15, 16*KS features) into a
+// canonical MN-major buffer (conflict-free: 32 lanes -> 32 banks).
+template <int KS>
+__device__ __forceinline__ void store_a_kc(const uint32_t (&a)[KS][4], unsigned char* buf, int row0, int lane)
+{
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+        const int f = 16 * s + 2 * t;
+        *reinterpret_cast<uint32_t*>(buf + kc_off(f, row0 + g)) = a[s][0];
+        *reinterpret_cast<uint32_t*>(buf + kc_off(f, row0 + g + 8)) = a[s][1];
+        *reinterpret_cast<uint32_t*>(buf + kc_off(f + 8, row0 + g)) = a[s][2];
+        *reinterpret_cast<uint32_t*>(buf + kc_off(f + 8, row0 + g + 8)) = a[s][3];
+    }
+}
+
+template <int NH>
+struct TcSlots {
+    static constexpr int COLS = H + 8;   // columns per TMEM region (a hidden layer's 64 inputs + the db column block)
+    __host__ __device__ static constexpr int ncols(int k0)
+    {
+        int n = 0;
+        for (int k = 0; k <= NH; ++k) {
+            const int w = k < NH ? (k == 0 ? k0 : H) + 8 : OUTP;
+            const int e = (k >> 1) * COLS + w;
+            n = e > n ? e : n;
+        }
+        return n;
+    }
+};
+
+template <int IN_STEPS, int NH, int STAGE_BYTES = 0, bool ALIAS = false>
+struct TrainSmemTc {
+    using Lay = WLayout<IN_STEPS, NH>;
+    static constexpr int K0 = 16 * IN_STEPS;
+    static constexpr int LV_OFF = align16(Lay::BYTES);
+    static constexpr int ACT0_OFF = (LV_OFF + int(sizeof(LevelDev)) * NFG_MAX_LEVELS + 127) & ~127;
+    static constexpr int ACT0_BYTES = (K0 / 8 + 1) * KC_SBO;   // + the ones block
+    static constexpr int ACTH_OFF = ACT0_OFF + ACT0_BYTES;
+    static constexpr int ACTH_BYTES = (H / 8 + 1) * KC_SBO;    // + the ones block
+    static constexpr int DZH_OFF = ACTH_OFF + NH * ACTH_BYTES;
+    static constexpr int DZH_BYTES = H / 8 * KC_SBO;
+    static constexpr int DZO_OFF = DZH_OFF + NH * DZH_BYTES;
+    static constexpr int DZO_BYTES = OUTP / 8 * KC_SBO;
+    static constexpr int RED_OFF = DZO_OFF + DZO_BYTES;
+    static constexpr int DBO_OFF = RED_OFF + 4 * TW * 4;                 // per-warp output-bias partials
+    static constexpr int MBAR_OFF = align16(DBO_OFF + TW * OUTP * 4);
+    static constexpr int TSLOT_OFF = MBAR_OFF + 8;
+    static constexpr int STAGE_OFF = align16(TSLOT_OFF + 8);
+    static constexpr int BYTES = STAGE_OFF + (ALIAS ? 0 : STAGE_BYTES);
+    static constexpr int INS = Lay::INS, OS = OUTP + 8, DB_OFF = RED_OFF;   // (mma.sync-path names; unused)
+    static constexpr int NCOLS = TcSlots<NH>::ncols(K0);
+    static constexpr uint32_t TMEM_COLS = tc::alloc_cols(NCOLS);
+};
+
+// Aliased gather staging in the canonical buffers: slot k of this lane lives in
+// buffer k / 16 (acth[0], acth[1], dz[0], dz[1]), feature block (k % 16) / 2,
+// sample block 2 warp + (k % 2) — the warp's own samples, below the ones block.
+template <class SMT>
+struct SlotsKC {
+    unsigned char* base;   // sm + warp * 256 + lane * SB
+    __device__ __forceinline__ unsigned char* ptr(int k) const
+    {
+        const int b = k >> 4, r = k & 15;
+        const int off = b < 2 ? SMT::ACTH_OFF + b * SMT::ACTH_BYTES : SMT::DZH_OFF + (b - 2) * SMT::DZH_BYTES;
+        return base + off + (r >> 1) * KC_SBO + (r & 1) * 128;
+    }
 };
 
 template <int IN_STEPS, int NH>
@@ -199,14 +294,20 @@ __device__ __forceinline__ void load_x(float* x, const float* __restrict__ X, in
 #ifndef NFG_TRAIN_MIN_BLOCKS
 #define NFG_TRAIN_MIN_BLOCKS 2
 #endif
-template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IN_STEPS, int NH>
-__global__ void __launch_bounds__(TW * 32, NFG_TRAIN_MIN_BLOCKS)
+// With the dW accumulators in TMEM (TCW) the kernel fits 3 CTAs per SM.
+#ifndef NFG_TRAIN_MIN_BLOCKS_TC
+#define NFG_TRAIN_MIN_BLOCKS_TC 3
+#endif
+template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IN_STEPS, int NH, bool TCW = false>
+__global__ void __launch_bounds__(TW * 32, TCW ? NFG_TRAIN_MIN_BLOCKS_TC : NFG_TRAIN_MIN_BLOCKS)
 k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ levels)
 {
     using Lay = WLayout<IN_STEPS, NH>;
     using SG = StageGeo<SRC, D, F, TT, IN_STEPS>;
     using SA = StageAlias<SRC, D, F, TT, IN_STEPS, NH>;
-    using SM = TrainSmem<IN_STEPS, NH, SG::BYTES, SA::ON>;
+    static_assert(!(TCW && SA::PREFETCH), "gather-ahead is an mma.sync-path experiment");
+    using SM = std::conditional_t<TCW, TrainSmemTc<IN_STEPS, NH, SG::BYTES, SA::ON>,
+                                  TrainSmem<IN_STEPS, NH, SG::BYTES, SA::ON>>;
     extern __shared__ __align__(16) unsigned char sm[];
     __half* ws = reinterpret_cast<__half*>(sm);
     float* bs = reinterpret_cast<float*>(sm + Lay::HALVES * 2);
@@ -232,8 +333,30 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     if (SRC == SRC_ENCODE)
         for (int i = tid; i < s.grid.L; i += blockDim.x)
             lvs[i] = levels[i];
+    uint32_t tbase = 0, mbar = 0;
+    if constexpr (TCW) {
+        // ones blocks of the activation buffers (db = dz^T 1), TMEM, mbarrier
+        for (int i = tid; i < TS * 8; i += blockDim.x) {
+            const int smp = i >> 3, c = i & 7;
+            const __half v = __float2half_rn(c == 0 ? 1.0f : 0.0f);
+            *reinterpret_cast<__half*>(sm + SM::ACT0_OFF + kc_off(16 * IN_STEPS + c, smp)) = v;
+#pragma unroll
+            for (int k = 0; k < NH; ++k)
+                *reinterpret_cast<__half*>(sm + SM::ACTH_OFF + k * SM::ACTH_BYTES + kc_off(H + c, smp)) = v;
+        }
+        mbar = tc::smem_u32(sm + SM::MBAR_OFF);
+        if (tid == 0)
+            tc::mbar_init(mbar, 1);
+        if (warp == 0)
+            tc::tmem_alloc(reinterpret_cast<uint32_t*>(sm + SM::TSLOT_OFF), SM::TMEM_COLS);
+        tc::fence_smem_async();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        tbase = *reinterpret_cast<const uint32_t*>(sm + SM::TSLOT_OFF);
+    }
     // padding columns of the activation buffers: a 1 then zeros (db_tile)
-    for (int r = tid; r < TS; r += blockDim.x) {
+    for (int r = tid; !TCW && r < TS; r += blockDim.x) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             act0[r * SM::INS + 16 * IN_STEPS + c] = __float2half_rn(c == 0 ? 1.0f : 0.0f);
@@ -275,6 +398,13 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     bool bad = false;
     unsigned int invalid = 0u;
     double loss_acc = 0.0;   // deterministic mode (lane 0 of each warp)
+    // TCW: dz scale of the TMEM accumulators (power of two; the running minimum
+    // of the tiles' own scales — a smaller one rescales the accumulators), the
+    // pending dW commit, the output bias gradient (lanes g == 0)
+    float kscale = 0.0f;
+    bool pending = false, first_mma = true;
+    uint32_t mphase = 0;
+    float dbo4[2][2] = { { 0.0f, 0.0f }, { 0.0f, 0.0f } };
     NFG_PT_DECL
     const int64_t ntiles = (a.B + TS - 1) / TS;
     const int r0 = 16 * warp;
@@ -365,6 +495,12 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     }
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         NFG_PT_START();
+        if (TCW && pending) {   // the previous tile's dW MMAs read the activation / dz / staging buffers
+            tc::mbar_wait(mbar, mphase);
+            mphase ^= 1u;
+            pending = false;
+            tc::fence_after();
+        }
         const int64_t sg = tile * TS + r0 + g, sg8 = sg + 8;
         const bool vg = sg < a.B, vg8 = sg8 < a.B;
         if (!SA::PREFETCH && a.ready) {   // streamed inputs: wait for this tile's chunk to land
@@ -402,6 +538,10 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 if (LPG)
                     __syncwarp();
                 blend_pass(0, lin_slots, xg, xg8, vg, vg8, afr);
+            } else if constexpr (SA::ON && TCW) {
+                const SlotsKC<SM> slots{ sm + warp * 256 + lane * SG::SB };
+                encode_all(slots);
+                __syncwarp();   // every lane's staged rows consumed before the warp writes them
             } else if constexpr (SA::ON) {
                 SlotsChunked<SA::ROWS, HS * 2, 4> slots;
                 slots.chunk[0] = reinterpret_cast<unsigned char*>(acth + r0 * HS);
@@ -417,7 +557,10 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         } else {
             input_frags<SRC, D, F, TT, IN_STEPS>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
         }
-        store_a<IN_STEPS>(afr, act0, SM::INS, r0, lane);
+        if constexpr (TCW)
+            store_a_kc<IN_STEPS>(afr, sm + SM::ACT0_OFF, r0, lane);
+        else
+            store_a<IN_STEPS>(afr, act0, SM::INS, r0, lane);
         NFG_PT(0);
 
         // ---- MLP forward --------------------------------------------------
@@ -427,13 +570,19 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         layer_fwd<IN_STEPS, HT>(afr, W0s, SM::INS, acc, lane);
         mask[0] = bias_relu<HT>(acc, bs, lane);
         c_to_a<4, false>(acc, ah);
-        store_a<4>(ah, acth, HS, r0, lane);
+        if constexpr (TCW)
+            store_a_kc<4>(ah, sm + SM::ACTH_OFF, r0, lane);
+        else
+            store_a<4>(ah, acth, HS, r0, lane);
 #pragma unroll
         for (int k = 1; k < NH; ++k) {
             layer_fwd<4, HT>(ah, Whs + (k - 1) * Lay::WH_HALVES, HS, acc, lane);
             mask[k] = bias_relu<HT>(acc, bs + H * k, lane);
             c_to_a<4, false>(acc, ah);
-            store_a<4>(ah, acth + k * TS * HS, HS, r0, lane);
+            if constexpr (TCW)
+                store_a_kc<4>(ah, sm + SM::ACTH_OFF + k * SM::ACTH_BYTES, r0, lane);
+            else
+                store_a<4>(ah, acth + k * TS * HS, HS, r0, lane);
         }
         float ao[2][4];
         layer_fwd<4, 2>(ah, Wos, HS, ao, lane);
@@ -503,6 +652,36 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             sc = ldexpf(1.0f, k);
             isc = ldexpf(1.0f, -k);
         }
+        if constexpr (TCW) {
+            // one scale per CTA accumulator: the running minimum of the tile
+            // scales (scaled maxima stay < 16); a smaller tile scale rescales
+            // the TMEM accumulators by the exact power-of-two ratio
+            if (kscale == 0.0f) {
+                kscale = sc;
+            } else if (sc < kscale) {
+                if (pending) {
+                    tc::mbar_wait(mbar, mphase);
+                    mphase ^= 1u;
+                    pending = false;
+                    tc::fence_after();
+                }
+                const float ratio = sc / kscale;
+#pragma unroll
+                for (int c8 = 0; c8 < (SM::NCOLS + 7) / 8; ++c8) {
+                    float v[8];
+                    const uint32_t ta = tbase + (uint32_t(32 * warp) << 16) + 8u * c8;
+                    tc::ld8(ta, v);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        v[i] *= ratio;
+                    tc::st8(ta, v);
+                }
+                tc::wait_st();
+                kscale = sc;
+            }
+            sc = kscale;
+            isc = 1.0f / kscale;
+        }
 
         // ---- MLP backward ---------------------------------------------------
 #pragma unroll
@@ -512,18 +691,41 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 ao[j][e] *= sc;
         uint32_t azo[1][4];
         c_to_a<1, true>(ao, azo);
-        store_a<1>(azo, dzo, SM::OS, r0, lane);
+        if constexpr (TCW) {
+            store_a_kc<1>(azo, sm + SM::DZO_OFF, r0, lane);
+            // output bias gradient from the same fp16 dz the MMAs see
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const float2 top = unpack_half2(azo[0][2 * j]), bot = unpack_half2(azo[0][2 * j + 1]);
+                float sx = top.x + bot.x, sy = top.y + bot.y;
+#pragma unroll
+                for (int m = 4; m < 32; m <<= 1) {
+                    sx += __shfl_xor_sync(0xffffffffu, sx, m);
+                    sy += __shfl_xor_sync(0xffffffffu, sy, m);
+                }
+                dbo4[j][0] = fmaf(sx, isc, dbo4[j][0]);
+                dbo4[j][1] = fmaf(sy, isc, dbo4[j][1]);
+            }
+        } else {
+            store_a<1>(azo, dzo, SM::OS, r0, lane);
+        }
         layer_bwd<1, HT>(azo, Wos, HS, acc, lane);
         apply_mask<HT>(acc, mask[NH - 1]);
 #pragma unroll
         for (int k = NH - 1; k >= 1; --k) {
             c_to_a<4, true>(acc, ah);
-            store_a<4>(ah, dzh + k * TS * HS, HS, r0, lane);
+            if constexpr (TCW)
+                store_a_kc<4>(ah, sm + SM::DZH_OFF + k * SM::DZH_BYTES, r0, lane);
+            else
+                store_a<4>(ah, dzh + k * TS * HS, HS, r0, lane);
             layer_bwd<4, HT>(ah, Whs + (k - 1) * Lay::WH_HALVES, HS, acc, lane);
             apply_mask<HT>(acc, mask[k - 1]);
         }
         c_to_a<4, true>(acc, ah);
-        store_a<4>(ah, dzh, HS, r0, lane);
+        if constexpr (TCW)
+            store_a_kc<4>(ah, sm + SM::DZH_OFF, r0, lane);
+        else
+            store_a<4>(ah, dzh, HS, r0, lane);
         float ay[2 * IN_STEPS][4];
         layer_bwd<4, 2 * IN_STEPS>(ah, W0s, SM::INS, ay, lane);
 
@@ -571,6 +773,41 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             }
         }
         NFG_PT(4);
+        if constexpr (TCW) {
+            // ---- dW / db += dz^T [act | 1] on tcgen05, accumulated in TMEM ----------
+            tc::fence_smem_async();   // this tile's activation / dz stores -> tensor core
+            tc::fence_before();
+            __syncthreads();
+            NFG_PT(5);
+            if (tid == 0) {
+                tc::fence_after();
+                constexpr int K0 = 16 * IN_STEPS;
+                constexpr uint32_t ID0 = tc::idesc_f16_mn(64, K0 + 8), IDH = tc::idesc_f16_mn(64, H + 8),
+                                   IDO = tc::idesc_f16_mn(64, OUTP);
+                const uint32_t s0 = tc::smem_u32(sm);
+                auto slot = [&](int k) {
+                    return tbase + ((k & 1) ? (16u << 16) : 0u) + uint32_t((k >> 1) * TcSlots<NH>::COLS);
+                };
+#pragma unroll
+                for (int ks = 0; ks < TS / 16; ++ks) {
+                    const uint32_t acc_on = (ks > 0 || !first_mma) ? 1u : 0u;
+                    auto dsc = [&](int off) { return tc::desc(s0 + off + 256u * ks, 128u, uint32_t(KC_SBO)); };
+                    tc::mma_f16(slot(0), dsc(SM::DZH_OFF), dsc(SM::ACT0_OFF), ID0, acc_on);
+#pragma unroll
+                    for (int k = 1; k < NH; ++k)
+                        tc::mma_f16(slot(k), dsc(SM::DZH_OFF + k * SM::DZH_BYTES),
+                                    dsc(SM::ACTH_OFF + (k - 1) * SM::ACTH_BYTES), IDH, acc_on);
+                    tc::mma_f16(slot(NH), dsc(SM::ACTH_OFF + (NH - 1) * SM::ACTH_BYTES), dsc(SM::DZO_OFF), IDO,
+                                acc_on);
+                }
+                tc::commit(mbar);
+            }
+            first_mma = false;
+            pending = true;
+            NFG_PT(6);
+            NFG_PT(7);
+            continue;
+        }
         __syncthreads();
         NFG_PT(5);
 
@@ -638,6 +875,78 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     // ---- flush per-CTA dW / db (x 1/count) ----------------------------------
     const float ic = a.inv_count;
     const int hw = s.hidden_width;
+    if constexpr (TCW) {
+        if (pending) {
+            tc::mbar_wait(mbar, mphase);
+            tc::fence_after();
+        }
+        if (!first_mma) {
+            // warp w, lane L < 16 (L >= 16): TMEM lane 32 w + L = row 16 w + (L % 16) of
+            // the lane-half-0 (half-1) accumulator slots
+            const float fs = ic / kscale;
+            const int half = lane >> 4, m = 16 * warp + (lane & 15);
+            const size_t wo_off = size_t(hw) * s.in_real + size_t(NH - 1) * hw * hw;
+#pragma unroll
+            for (int c8 = 0; c8 < (SM::NCOLS + 7) / 8; ++c8) {
+                float v[8];
+                tc::ld8(tbase + (uint32_t(32 * warp) << 16) + 8u * c8, v);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int col = 8 * c8 + i, region = col / TcSlots<NH>::COLS;
+                    const int lc = col - region * TcSlots<NH>::COLS, k = 2 * region + half;
+                    if (m >= hw || k > NH)
+                        continue;
+                    size_t idx;
+                    bool is_b = false;
+                    if (k < NH) {
+                        const int nin = k == 0 ? 16 * IN_STEPS : H, in_k = k == 0 ? s.in_real : hw;
+                        if (lc < in_k)
+                            idx = (k == 0 ? 0 : size_t(hw) * s.in_real + size_t(k - 1) * hw * hw) + m + size_t(lc) * hw;
+                        else if (lc == nin) {
+                            idx = size_t(k) * hw + m;
+                            is_b = true;
+                        } else
+                            continue;
+                    } else {
+                        if (lc >= s.n_out)
+                            continue;
+                        idx = wo_off + lc + size_t(m) * s.n_out;
+                    }
+                    const float val = v[i] * fs;
+                    bad |= !sane(val);
+                    if (a.part_wb)
+                        a.part_wb[blockIdx.x * a.n_wb + (is_b ? a.n_w : 0) + idx] = val;
+                    else
+                        atomicAdd((is_b ? a.gb : a.gW) + idx, val);
+                }
+            }
+        }
+        // output bias: per-warp partials (lanes g == 0), summed over the warps in order
+        float* dbo_s = reinterpret_cast<float*>(sm + SM::DBO_OFF);
+        if (g == 0)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int b = 0; b < 2; ++b)
+                    dbo_s[warp * OUTP + 8 * j + 2 * t + b] = dbo4[j][b];
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (tid < s.n_out) {
+            float v = 0.0f;
+#pragma unroll
+            for (int w = 0; w < TW; ++w)
+                v += dbo_s[w * OUTP + tid];
+            v *= ic;
+            bad |= !sane(v);
+            if (a.part_wb)
+                a.part_wb[blockIdx.x * a.n_wb + a.n_w + NH * hw + tid] = v;
+            else
+                atomicAdd(a.gb + NH * hw + tid, v);
+        }
+        if (warp == 0)
+            tc::tmem_dealloc(tbase, SM::TMEM_COLS);
+    } else {
     auto flush = [&](const float (&cq)[2][4], int mt, int np, int out_k, int in_k, size_t woff) {
 #ifdef NFG_EXP_NO_FLUSH   // experiment builds only (tools/kbench.cu): upper bound of the dW flush cost
         return;
@@ -703,6 +1012,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                         atomicAdd(a.gb + NH * hw + g + 8 * h, v);
                 }
     }
+    }   // mma.sync dW path
     if (GRAD == GRAD_LOSS && a.part_loss && lane == 0)
         a.part_loss[blockIdx.x * TW + warp] = loss_acc;
     if (__any_sync(0xffffffffu, bad) && lane == 0)

@@ -10,9 +10,9 @@
 #define NFG_CAT(a, b) NFG_CAT2(a, b)
 
 // Default engine of the fused inference kernel (nfg_options.mlp_engine ==
-// NFG_MMA_DEFAULT): the measured-faster one.
-#ifndef NFG_INFER_TC_DEFAULT
-#define NFG_INFER_TC_DEFAULT 0
+// NFG_MMA_DEFAULT): the measured-faster one per batch size.
+#ifndef NFG_INFER_TC_BELOW
+#define NFG_INFER_TC_BELOW (int64_t(1) << 18)
 #endif
 
 namespace nfg {
@@ -77,7 +77,12 @@ cudaError_t NFG_CAT(launch_fused_infer_d, NFG_D)(const FieldShape& s, const Leve
                                                  int num_sms, cudaStream_t st)
 {
     const bool f32 = s.table_fp32 != 0;
-    const bool tc = s.mlp_engine == NFG_MMA_TCGEN05 || (s.mlp_engine == NFG_MMA_DEFAULT && NFG_INFER_TC_DEFAULT);
+    // default engine: tcgen05 below 2^18 queries (its 128-sample tiles dealt over all SMs beat the
+    // mma.sync kernel's 1.15 waves of 16-sample warp tiles at 2^16 by 1.27x), mma.sync above (1.10x faster
+    // from 2^22: the L1 is the binding unit and the tcgen05 epilogues' shared-memory round trips compete
+    // with the gathers for it); profiles/tc_infer_r2.md
+    const bool tc = s.mlp_engine == NFG_MMA_TCGEN05 ||
+                    (s.mlp_engine == NFG_MMA_DEFAULT && a.B < NFG_INFER_TC_BELOW);
 #define X(F_, TT_, IS_, NH_)                                                                               \
     if (s.grid.F == F_ && f32 == (sizeof(TT_) == 4) && s.in_steps == IS_ && s.hidden_layers == NH_)         \
         return tc ? run_infer_tc<SRC_ENCODE, NFG_D, F_, TT_, IS_, NH_>(s, lv, a, num_sms, st)                 \

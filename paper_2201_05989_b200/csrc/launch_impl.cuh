@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -10,12 +11,14 @@
 
 namespace nfg {
 
-template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IS, int NH>
+template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IS, int NH, bool TCW>
 cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& a, int num_sms, cudaStream_t st,
                       int* grid_used)
 {
-    using SM = TrainSmem<IS, NH, StageGeo<SRC, D, F, TT, IS>::BYTES, StageAlias<SRC, D, F, TT, IS, NH>::ON>;
-    auto k = k_train<SRC, GRAD, SINK, D, F, TT, IS, NH>;
+    using SG = StageGeo<SRC, D, F, TT, IS>;
+    constexpr bool ALIAS = StageAlias<SRC, D, F, TT, IS, NH>::ON;
+    using SM = std::conditional_t<TCW, TrainSmemTc<IS, NH, SG::BYTES, ALIAS>, TrainSmem<IS, NH, SG::BYTES, ALIAS>>;
+    auto k = k_train<SRC, GRAD, SINK, D, F, TT, IS, NH, TCW>;
     static int per_sm = -1;   // resolved once per instantiation
     if (per_sm < 0) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
@@ -30,13 +33,42 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, TW * 32, SM::BYTES);
         if (e != cudaSuccess)
             return e;
+        const int n_occ = n;
+        if constexpr (TCW) {
+            // The occupancy API reports 1 CTA per SM for this kernel, but 3 are
+            // co-resident on a B200 (measured: k_train 416 us at a 1-CTA grid,
+            // 270 us at 3; profiles/tc_train_r2.md). Size the persistent grid
+            // from the actual per-SM limits: registers, shared memory, threads,
+            // and the 512 TMEM columns the resident CTAs share.
+            cudaFuncAttributes fa{};
+            int dev = 0, smem_sm = 0, smem_resv = 0;
+            if ((e = cudaFuncGetAttributes(&fa, k)) != cudaSuccess || (e = cudaGetDevice(&dev)) != cudaSuccess ||
+                (e = cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev)) !=
+                    cudaSuccess ||
+                (e = cudaDeviceGetAttribute(&smem_resv, cudaDevAttrReservedSharedMemoryPerBlock, dev)) != cudaSuccess)
+                return e;
+            const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+            const int by_regs = 65536 / (regs_warp * TW);
+            const int by_smem = smem_sm / (SM::BYTES + int(fa.sharedSizeBytes) + smem_resv);
+            const int by_tmem = int(512 / TrainSmemTc<IS, NH>::TMEM_COLS);
+            n = std::max(1, std::min({ by_regs, by_smem, by_tmem, 2048 / (TW * 32) }));
+        }
         per_sm = std::max(n, 1);
+        if (const char* o = getenv("NFG_TRAIN_CTAS_PER_SM"))   // experiment hook (grid sizing only)
+            per_sm = std::max(1, atoi(o));
+        if (getenv("NFG_DEBUG_OCC")) {
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, k);
+            fprintf(stderr, "[nfg] k_train tcw=%d smem_dyn=%d occ=%d per_sm=%d regs=%d local=%zu static_smem=%zu "
+                    "max_dyn=%d\n", int(TCW), SM::BYTES, n_occ, per_sm, fa.numRegs, fa.localSizeBytes,
+                    fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes);
+        }
     }
-    static char desc[160];
+    static char desc[192];
     if (!desc[0])
         snprintf(desc, sizeof(desc), "k_train src=%d grad=%d sink=%d d=%d F=%d table=%s in_steps=%d hidden=%d "
-                 "stage_alias=%d ctas_per_sm=%d", SRC, GRAD, SINK, D, F, sizeof(TT) == 2 ? "f16" : "f32", IS, NH,
-                 int(StageAlias<SRC, D, F, TT, IS, NH>::ON), per_sm);
+                 "stage_alias=%d ctas_per_sm=%d dw=%s", SRC, GRAD, SINK, D, F, sizeof(TT) == 2 ? "f16" : "f32", IS,
+                 NH, int(ALIAS), per_sm, TCW ? "tcgen05" : "mma.sync");
     note_kernel_variant(0, desc);
     const int64_t ntiles = (a.B + TS - 1) / TS;
     if (ntiles <= 0)
@@ -46,6 +78,23 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
         *grid_used = grid;
     k<<<grid, TW * 32, SM::BYTES, st>>>(a, s, lv);
     return cudaGetLastError();
+}
+
+// Engine of the fused training kernel's dW reduction (nfg_options.mlp_engine).
+#ifndef NFG_TRAIN_TC_DEFAULT
+#define NFG_TRAIN_TC_DEFAULT 1
+#endif
+inline bool train_tcw(const FieldShape& s)
+{
+    return s.mlp_engine == 2 || (s.mlp_engine == 0 && NFG_TRAIN_TC_DEFAULT);
+}
+
+template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IS, int NH>
+cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& a, int num_sms, cudaStream_t st,
+                      int* grid_used)
+{
+    return train_tcw(s) ? run_train<SRC, GRAD, SINK, D, F, TT, IS, NH, true>(s, lv, a, num_sms, st, grid_used)
+                        : run_train<SRC, GRAD, SINK, D, F, TT, IS, NH, false>(s, lv, a, num_sms, st, grid_used);
 }
 
 template <int SRC, int D, int F, typename TT, int IS, int NH>

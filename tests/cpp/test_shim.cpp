@@ -7,6 +7,7 @@
 // and run by tests/test_gpu_shim.py on a B200.
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <set>
 
 #include "../../include/nf/gpu_field_model.hpp"
@@ -40,6 +41,7 @@ struct ImageTask {   // tasks.hpp:16-31 member names
     double lr = 1e-2, lr_decay = 0.33;
 };
 using FieldModel = nf::gpu::FieldModelT<HashEncodingConfig, MlpConfig, AdamHyper, LrSchedule>;
+enum class LossKind { L2, Mape, RelativeL2 };   // model.hpp:17
 using nf::gpu::Mat;
 
 static int failures = 0;
@@ -186,6 +188,78 @@ int main()
             threw = true;
         }
         CHECK(threw);
+    }
+
+    // criterion 4, transcribed from acceptance.cpp:323-369 with the reference's
+    // own shape (hidden width 8): public members, the free encode_forward on a
+    // copy of the tables, the EncodeCache layout, LossKind-typed train_step
+    {
+        FieldModel model(ctx);
+        model.auto_mirror = true;
+        model.hash_cfg.dims = 2;
+        model.hash_cfg.levels = 2;
+        model.hash_cfg.table_size = 1u << 10;
+        model.hash_cfg.n_min = 8;
+        model.hash_cfg.n_max = 16;
+        model.mlp_cfg.hidden_layers = 1;
+        model.mlp_cfg.hidden_width = 8;
+        model.mlp_cfg.output_width = 1;
+        model.init(3);
+        const nf::gpu::FeatureTables<Mat> before = model.tables;
+
+        Mat X(2, 4), target(1, 4, 0.3f);
+        const float xs[4] = { 0.1f, 0.11f, 0.12f, 0.13f };
+        for (int i = 0; i < 4; ++i)
+            X(0, i) = X(1, i) = xs[i];
+        model.train_step(X, target, LossKind::L2, 1);
+
+        std::size_t touched = 0, moved_elsewhere = 0;
+        nf::gpu::EncodeCache cache;
+        Mat Y;
+        nf::gpu::encode_forward(before, X, Y, cache);   // identical rows as the step used
+        std::set<std::pair<int, std::uint32_t>> rows;
+        for (int l = 0; l < cache.levels; ++l)
+            for (int p = 0; p < cache.batch; ++p)
+                for (int c = 0; c < cache.corners; ++c)
+                    rows.emplace(l, cache.rows[cache.offset(l, p) + c]);
+        for (std::size_t l = 0; l < before.values.size(); ++l)
+            for (long col = 0; col < before.values[l].cols(); ++col) {
+                const bool was_touched = rows.count({ int(l), std::uint32_t(col) }) != 0;
+                float maxd = 0.0f;
+                for (long f = 0; f < before.values[l].rows(); ++f)
+                    maxd = std::max(maxd, std::fabs(model.tables.values[l](f, col) - before.values[l](f, col)));
+                const bool changed = maxd > 0;
+                if (was_touched)
+                    touched += changed ? 1 : 0;
+                else if (changed)
+                    ++moved_elsewhere;
+            }
+        CHECK(moved_elsewhere == 0);   // untouched table entries are bit-identical
+        CHECK(touched > 0);            // touched table entries actually move
+        // group flags: L2 on weights only, skip-zero on tables only (acceptance.cpp:381-388)
+        const auto groups = model.param_groups();
+        CHECK(groups.size() == 3 && !groups[0].flags.apply_l2 && groups[0].flags.skip_zero_grad &&
+              groups[1].flags.apply_l2 && !groups[1].flags.skip_zero_grad && !groups[2].flags.apply_l2 &&
+              !groups[2].flags.skip_zero_grad);
+        const nf::gpu::AdamState st = model.adam_state();
+        CHECK(st.step == 1 && st.m.size() == 3 && st.m[0].size() == before.parameter_count());
+        // member writes reach the device (test_tasks.cpp:31-33): zero weights, constant output bias
+        for (auto& w : model.mlp.weights)
+            std::fill(w.data(), w.data() + w.rows() * w.cols(), 0.0f);
+        std::fill(model.mlp.biases.back().data(), model.mlp.biases.back().data() + 1, 0.25f);
+        const Mat out = model.evaluate(X);
+        CHECK(out(0, 0) == 0.25f && out(0, 3) == 0.25f);
+        // encode_backward accumulates into tables.grads (grid.hpp:277-295)
+        nf::gpu::FeatureTables<Mat> t2 = before;
+        t2.zero_grads();
+        Mat dY(Y.rows(), Y.cols(), 1.0f);
+        nf::gpu::encode_backward(t2, cache, dY);
+        double gsum = 0.0;
+        for (const auto& g : t2.grads)
+            for (long i = 0; i < g.rows() * g.cols(); ++i)
+                gsum += g.data()[i];
+        // every (point, level) spreads weight 1 over its corners, for each of the 2 features
+        CHECK(std::fabs(gsum - 4.0 * 2 * 2) < 1e-4);
     }
 
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);

@@ -106,3 +106,55 @@ def test_tc_engine_empty_batch():
     ms, mt = _pair(nf, g, train_steps=0)
     out = mt.evaluate(np.zeros((0, 3), np.float32))
     assert out.shape[0] == 0
+
+
+@pytest.mark.parametrize("det", [False, True])
+@pytest.mark.parametrize("case", ["config2", "config1"])
+def test_train_dw_engines_agree(case, det):   # model.cpp:111-138, dW on tcgen05 vs mma.sync
+    """The fused step's dW / db reductions on tcgen05 (TMEM accumulators over
+    all tiles of a CTA, a running power-of-two dz scale) against the mma.sync
+    reductions (register accumulators, per-tile scale): same fp16 operands, fp32
+    accumulation in a different order; the bias gradients of the output layer
+    come from the same fp16 dz in both."""
+    from paper_2201_05989_b200 import nf
+    if case == "config2":
+        g = _grid(nf, dims=3, levels=16, table_size=1 << 19, features=2, n_min=16, n_max=2048)
+        n_out, sig, kind = 1, False, nf.LossKind.Mape
+    else:
+        g = _grid(nf, dims=2, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=1024)
+        n_out, sig, kind = 3, True, nf.LossKind.L2
+    ms = []
+    for eng in (SYNC, TC):
+        m = nf.FieldModel(options=nf.Options(mlp_engine=eng, deterministic=det))
+        m.hash_cfg = g
+        m.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=n_out,
+                                 output_activation=nf.OutputActivation.Sigmoid if sig else nf.OutputActivation.Linear)
+        m.hyper = nf.AdamHyper(lr=1e-3)
+        m.init(1337)
+        ms.append(m)
+    rng = O.Pcg32(5, 5)
+    d = g.dims
+    for step in range(1, 4):   # move off the init with the tcgen05 model, then share its parameters
+        X = rng.floats(16384 * d).reshape(-1, d)
+        T = np.tile(O.csg_sdf(X if d == 3 else np.c_[X, X[:, :1]]).reshape(-1, 1), (1, n_out))
+        if sig:
+            T = np.clip(T + 0.5, 0, 1)
+        ms[1].train_step(X, T.astype(np.float32), kind, step)
+    ms[0].write(nf.BUF_PARAMS, ms[1].params)
+    B = 3 * 65536 + 77   # several tiles per CTA (running scale) and a ragged tail
+    X = rng.floats(B * d).reshape(-1, d)
+    T = np.tile(O.csg_sdf(X if d == 3 else np.c_[X, X[:, :1]]).reshape(-1, 1), (1, n_out)).astype(np.float32)
+    if sig:
+        T = np.clip(T + 0.5, 0, 1)
+    out = []
+    for m, eng in zip(ms, ("mma.sync", "tcgen05")):
+        loss = m.gradients(X, T, kind)
+        assert f"dw={eng}" in m.last_kernel_variant(0), m.last_kernel_variant(0)
+        out.append((loss, m.grads))
+    (l0, g0), (l1, g1) = out
+    t, w, b = ms[0].sizes
+    assert abs(l0 - l1) <= 1e-6 * abs(l0)
+    assert np.array_equal(g0[:t] != 0, g1[:t] != 0)
+    assert np.linalg.norm(g0[:t] - g1[:t]) <= 1e-4 * np.linalg.norm(g0[:t])   # dY identical up to fp32 order
+    for a_, r_ in ((g1[t:t + w], g0[t:t + w]), (g1[t + w:], g0[t + w:])):
+        assert np.linalg.norm(a_ - r_) <= 1e-3 * np.linalg.norm(r_)
