@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define NFG_ABI_VERSION 3
+#define NFG_ABI_VERSION 4
 
 typedef enum {
     NFG_OK = 0,
@@ -102,9 +102,17 @@ typedef struct {
                               whichever is faster at width 64"): NFG_MMA_DEFAULT picks the measured-faster one per
                               kernel, NFG_MMA_SYNC / NFG_MMA_TCGEN05 force one. Kernels or shapes
                               without a tcgen05 build use mma.sync. */
+    int32_t dp_exchange;   /* data-parallel gradient exchange (an NCCL communicator attached).
+                              NFG_DP_ALLREDUCE (= NFG_DP_DEFAULT): one fused kernel, then the gradient slab all-reduced
+                              in chunks on a comm stream, Adam updating each chunk as soon as it is reduced.
+                              NFG_DP_LEVELS: the fused kernel stores dY instead of scattering; the table gradients are
+                              then scattered level group by level group (finest first) and each group's all-reduce and
+                              Adam start while later groups scatter. Hides the exchange behind the scatter but the
+                              unfused scatter costs more than it hides (measured). */
 } nfg_options;
 
 enum { NFG_MMA_DEFAULT = 0, NFG_MMA_SYNC = 1, NFG_MMA_TCGEN05 = 2 };
+enum { NFG_DP_DEFAULT = 0, NFG_DP_ALLREDUCE = 1, NFG_DP_LEVELS = 2 };
 
 typedef struct nfg_ctx nfg_ctx;
 typedef struct nfg_field nfg_field;

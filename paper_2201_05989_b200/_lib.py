@@ -37,7 +37,7 @@ class nfg_adam_hyper(C.Structure):
 
 class nfg_options(C.Structure):
     _fields_ = [("table_fp32", C.c_int32), ("fused_train", C.c_int32), ("deterministic", C.c_int32),
-                ("mlp_engine", C.c_int32)]
+                ("mlp_engine", C.c_int32), ("dp_exchange", C.c_int32)]
 
 
 class nfg_image_task(C.Structure):

@@ -55,7 +55,7 @@ k_encode_fwd(const FieldShape s, const LevelDev* __restrict__ levels, const floa
 template <int D, int F>
 __global__ void __launch_bounds__(256)
 k_encode_bwd(const FieldShape s, const LevelDev* __restrict__ levels, const float* __restrict__ X, int64_t B,
-             const float* __restrict__ dY, float* __restrict__ grads, const unsigned int* flags)
+             const float* __restrict__ dY, float* __restrict__ grads, const unsigned int* flags, int l0, int l1)
 {
     if (flags && flags[3] != 0u)
         return;   // invalid input of this step (k_validate)
@@ -71,7 +71,7 @@ k_encode_bwd(const FieldShape s, const LevelDev* __restrict__ levels, const floa
     for (int i = 0; i < D; ++i)
         x[i] = X[p * D + i];
     const int LF = s.grid.L * F;
-    for (int l = 0; l < s.grid.L; ++l) {
+    for (int l = l0; l < l1; ++l) {
         const LevelDev lv = lvs[l];
         const CornerSet<D> cs = corners_of<D>(s.grid, lv, x);
         float* base = grads + size_t(lv.row_off) * F;
@@ -107,10 +107,10 @@ static cudaError_t enc_fwd(const FieldShape& s, const LevelDev* lv, const float*
 
 template <int D, int F>
 static cudaError_t enc_bwd(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B, const float* dY,
-                           float* grads, const unsigned int* flags, cudaStream_t st)
+                           float* grads, const unsigned int* flags, cudaStream_t st, int l0, int l1)
 {
     const int64_t blocks = (B + 255) / 256;
-    k_encode_bwd<D, F><<<unsigned(blocks), 256, 0, st>>>(s, lv, X, B, dY, grads, flags);
+    k_encode_bwd<D, F><<<unsigned(blocks), 256, 0, st>>>(s, lv, X, B, dY, grads, flags, l0, l1);
     return cudaGetLastError();
 }
 
@@ -130,13 +130,16 @@ cudaError_t launch_encode_fwd_lv(const FieldShape& s, const LevelDev* lv, const 
 }
 
 cudaError_t launch_encode_bwd_lv(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
-                                 const float* dY, float* grads, cudaStream_t st, const unsigned int* flags)
+                                 const float* dY, float* grads, cudaStream_t st, const unsigned int* flags, int l0,
+                                 int l1)
 {
-    if (B <= 0)
+    if (l1 < 0)
+        l1 = s.grid.L;
+    if (B <= 0 || l0 >= l1)
         return cudaSuccess;
 #define NFG_ENC_B(D_, F_)                                                                                   \
     if (s.grid.d == D_ && s.grid.F == F_)                                                                    \
-        return enc_bwd<D_, F_>(s, lv, X, B, dY, grads, flags, st);
+        return enc_bwd<D_, F_>(s, lv, X, B, dY, grads, flags, st, l0, l1);
     NFG_ENC_B(2, 1) NFG_ENC_B(2, 2) NFG_ENC_B(2, 4) NFG_ENC_B(2, 8)
     NFG_ENC_B(3, 1) NFG_ENC_B(3, 2) NFG_ENC_B(3, 4) NFG_ENC_B(3, 8)
 #undef NFG_ENC_B

@@ -288,6 +288,8 @@ struct nfg_ctx {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_grads = nullptr;
     cudaEvent_t ev_chunk[8] = {};
+    // level-pipelined exchange: per level group, scatter done (main) / reduced (comm)
+    cudaEvent_t ev_scat[8] = {}, ev_red[8] = {}, ev_scr = nullptr;
     CUresult (*write_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
     // phase timing (nfg_ctx_set_profiling)
     bool profile = false;
@@ -642,7 +644,7 @@ void reduce_scratch(nfg_field* f, cudaStream_t st)
 
 void device_backward(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
                      int loss_kind, const Streamed& sm = Streamed(), bool allow_speculative = true,
-                     bool reduce_grads = true)
+                     bool reduce_grads = true, float* store_dy = nullptr)
 {
     require(loss_kind >= 0 && loss_kind <= 2, "train_step: unknown loss");
     require(B_local >= 0 && B_global >= B_local, "train_step: invalid batch size");
@@ -685,7 +687,12 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
         c->prof_steps++;
     if (B_local > 0) {
         Span span(c, 0);
-        if (fused) {
+        if (fused && store_dy) {   // level-pipelined data parallelism: dY out, scattered per level group
+            a.dY = store_dy;
+            NFG_CUDA(nfg::launch_train(f->shape, f->d_levels, nfg::SRC_ENCODE, nfg::GRAD_LOSS, nfg::SINK_STORE, a,
+                                       c->num_sms, c->stream, &f->train_grid));
+            c->launches++;
+        } else if (fused) {
             NFG_CUDA(nfg::launch_train(f->shape, f->d_levels, nfg::SRC_ENCODE, nfg::GRAD_LOSS, nfg::SINK_SCATTER, a,
                                        c->num_sms, c->stream, &f->train_grid));
             c->launches++;
@@ -729,12 +736,106 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
     }
 }
 
+// Whether a data-parallel step takes the level-pipelined exchange (NFG_DP_LEVELS).
+bool dp_levels(const nfg_field* f)
+{
+    return f->ctx->comm && f->opts.dp_exchange == NFG_DP_LEVELS && f->opts.fused_train &&
+           !f->opts.deterministic && f->gcfg.features == 2 && f->shape.in_steps <= 2 && nfg::fused_supported(f->shape);
+}
+
+// Level groups of the level-pipelined exchange, finest first: contiguous level
+// ranges [l0, l1) whose gradient slices reach ~4 MB (one NCCL call each,
+// enough to run near bus bandwidth); the coarsest group also carries the MLP
+// parameters. At config 2 (11 hashed levels of 4 MB) this is 8 groups.
+struct LevelGroup {
+    int l0, l1;
+    uint64_t lo, hi;   // slab range
+};
+std::vector<LevelGroup> level_groups(const nfg_field* f, int max_groups)
+{
+    const int L = f->gcfg.levels, F = f->gcfg.features;
+    auto start = [&](int l) { return l >= L ? f->n_tab_dev : f->dev_row_off[size_t(l)] * uint64_t(F); };
+    std::vector<LevelGroup> g;
+    int l1 = L;
+    while (l1 > 0) {
+        int l0 = l1 - 1;
+        while (l0 > 0 && (start(l1) - start(l0)) * 4 < (uint64_t(4) << 20))
+            --l0;
+        g.push_back({ l0, l1, start(l0), start(l1) });
+        l1 = l0;
+    }
+    // merge the coarsest groups until the count fits the event slots
+    while (int(g.size()) > max_groups) {
+        LevelGroup& a = g[g.size() - 2];
+        const LevelGroup b = g.back();
+        a.l0 = b.l0;
+        a.lo = b.lo;
+        g.pop_back();
+    }
+    return g;   // g.back() is the coarsest group, l0 = 0, lo = 0
+}
+
 template <class AfterBackward>
 void device_train_step(nfg_field* f, const float* X, const float* target, int64_t B_local, int64_t B_global,
                        int loss_kind, int64_t step, const Streamed& sm, AfterBackward&& after_backward)
 {
     nfg_ctx* c = f->ctx;
     const bool dp = c->comm != nullptr;
+    if (dp && dp_levels(f)) {
+        // Level-pipelined exchange: the fused kernel stores dY (no table
+        // scatter); the loss / flags scratch is reduced at once; then each level
+        // group, finest first, is scattered on the main stream and all-reduced
+        // on the comm stream as soon as its scatter is done, and Adam updates
+        // each reduced group while later groups are still scattering / reducing.
+        // Only the coarsest (smallest) group's reduction follows the last scatter.
+        const size_t LF = size_t(f->shape.in_real);
+        float* dY = static_cast<float*>(c->s3.get(size_t(std::max<int64_t>(B_local, 1)) * LF * 4));
+        device_backward(f, X, target, B_local, B_global, loss_kind, sm, true, /*reduce_grads=*/false, dY);
+        after_backward();
+        const float lr_now = float(nfg::host::lr_at(f->milestones, f->factor, f->hyper.lr, step));
+        Span span(c, 2);
+        NFG_CUDA(cudaEventRecord(c->ev_grads, c->stream));
+        NFG_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_grads, 0));
+        reduce_scratch(f, c->comm_stream);
+        NFG_CUDA(cudaEventRecord(c->ev_scr, c->comm_stream));
+        const int ng_max = int(sizeof(c->ev_scat) / sizeof(c->ev_scat[0]));
+        const std::vector<LevelGroup> groups = level_groups(f, ng_max);
+        for (size_t k = 0; k < groups.size(); ++k) {
+            const LevelGroup& gk = groups[k];
+            const bool last = k + 1 == groups.size();
+            NFG_CUDA(nfg::launch_encode_bwd_lv(f->shape, f->d_levels, X, B_local, dY, f->d_g, c->stream,
+                                               f->d_res->flags, gk.l0, gk.l1));
+            c->launches++;
+            NFG_CUDA(cudaEventRecord(c->ev_scat[k], c->stream));
+            NFG_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_scat[k], 0));
+            NFG_NCCL(nccl().all_reduce(f->d_g + gk.lo, f->d_g + gk.lo, gk.hi - gk.lo, ncclFloat32, ncclSum, c->comm,
+                                       c->comm_stream));
+            if (last)   // the MLP W, b (final since the fused kernel) travel with the coarsest group
+                NFG_NCCL(nccl().all_reduce(f->d_g + f->n_tab_dev, f->d_g + f->n_tab_dev, f->n_total_dev - f->n_tab_dev,
+                                           ncclFloat32, ncclSum, c->comm, c->comm_stream));
+            NFG_CUDA(cudaEventRecord(c->ev_red[k], c->comm_stream));
+        }
+        nfg::AdamArgs a = adam_args(f, lr_now);
+        NFG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_scr, 0));
+        for (size_t k = 0; k < groups.size(); ++k) {
+            const bool last = k + 1 == groups.size();
+            NFG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_red[k], 0));
+            a.lo = groups[k].lo;
+            a.hi = groups[k].hi;
+            NFG_CUDA(nfg::launch_adam_range(a, c->num_sms, c->stream));
+            if (last) {   // the MLP parameters
+                a.lo = f->n_tab_dev;
+                a.hi = f->n_total_dev;
+                NFG_CUDA(nfg::launch_adam_range(a, c->num_sms, c->stream));
+                c->launches++;
+            }
+            c->launches++;
+        }
+        NFG_CUDA(nfg::launch_adam_fallback(a, c->num_sms, c->stream));
+        c->launches += 2;
+        f->step += 1;
+        return;
+    }
     device_backward(f, X, target, B_local, B_global, loss_kind, sm, true, /*reduce_grads=*/!dp);
     after_backward();   // streamed steps: enqueue the batch copies before the optimizer launches
     const float lr_now = float(nfg::host::lr_at(f->milestones, f->factor, f->hyper.lr, step));
@@ -990,6 +1091,11 @@ nfg_status nfg_ctx_attach_comm(nfg_ctx* c, const uint8_t id[128], int rank, int 
             NFG_CUDA(cudaEventCreateWithFlags(&c->ev_grads, cudaEventDisableTiming));
             for (auto& e : c->ev_chunk)
                 NFG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            for (auto& e : c->ev_scat)
+                NFG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            for (auto& e : c->ev_red)
+                NFG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            NFG_CUDA(cudaEventCreateWithFlags(&c->ev_scr, cudaEventDisableTiming));
         }
     });
 }
@@ -1055,6 +1161,8 @@ nfg_status nfg_field_create(nfg_ctx* ctx, const nfg_grid_config* grid, const nfg
             nfg::host::validate(f->hyper);
             require(f->opts.mlp_engine >= NFG_MMA_DEFAULT && f->opts.mlp_engine <= NFG_MMA_TCGEN05,
                     "nfg_options.mlp_engine must be NFG_MMA_DEFAULT, NFG_MMA_SYNC or NFG_MMA_TCGEN05");
+            require(f->opts.dp_exchange >= NFG_DP_DEFAULT && f->opts.dp_exchange <= NFG_DP_LEVELS,
+                    "nfg_options.dp_exchange must be NFG_DP_DEFAULT, NFG_DP_ALLREDUCE or NFG_DP_LEVELS");
             if (f->mcfg.hidden_width > 64)
                 throw Fail{ NFG_EUNSUPPORTED, "sm_100a MLP is built for hidden_width <= 64" };
             if (f->mcfg.hidden_layers < 1 || f->mcfg.hidden_layers > 3)

@@ -73,6 +73,24 @@ cudaError_t NFG_CAT(launch_fused_dout_d, NFG_D)(const FieldShape& s, const Level
     return cudaErrorNotSupported;
 }
 
+// Fused encode + MLP forward / loss / MLP backward with dY stored instead of
+// scattered (the data-parallel level-pipelined exchange: the table-gradient
+// scatter then runs per level group so each group's all-reduce starts early).
+cudaError_t NFG_CAT(launch_fused_store_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
+                                                 int num_sms, cudaStream_t st, int* grid_used)
+{
+    const bool f32 = s.table_fp32 != 0;
+#define X(F_, TT_, IS_, NH_)                                                                               \
+    if (s.grid.F == F_ && f32 == (sizeof(TT_) == 4) && s.in_steps == IS_ && s.hidden_layers == NH_)         \
+        return run_train<SRC_ENCODE, GRAD_LOSS, SINK_STORE, NFG_D, F_, TT_, IS_, NH_>(s, lv, a, num_sms, st,   \
+                                                                                       grid_used);
+    X(2, __half, 1, 1) X(2, __half, 1, 2) X(2, __half, 1, 3) X(2, __half, 2, 1) X(2, __half, 2, 2)
+    X(2, __half, 2, 3) X(2, float, 1, 1) X(2, float, 1, 2) X(2, float, 1, 3) X(2, float, 2, 1)
+    X(2, float, 2, 2) X(2, float, 2, 3)
+#undef X
+    return cudaErrorNotSupported;
+}
+
 cudaError_t NFG_CAT(launch_fused_infer_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const InferArgs& a,
                                                  int num_sms, cudaStream_t st)
 {

@@ -94,8 +94,10 @@ cudaError_t launch_infer(const FieldShape& s, const LevelDev* lv, int src, const
                          cudaStream_t st);
 cudaError_t launch_encode_fwd_lv(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
                                  const void* table, float* Y, uint32_t* rows, float* weights, cudaStream_t st);
+// Levels [l0, l1) only (l1 < 0: all): the data-parallel exchange scatters level groups separately.
 cudaError_t launch_encode_bwd_lv(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
-                                 const float* dY, float* grads, cudaStream_t st, const unsigned int* flags = nullptr);
+                                 const float* dY, float* grads, cudaStream_t st, const unsigned int* flags = nullptr,
+                                 int l0 = 0, int l1 = -1);
 
 struct AdamArgs {
     float* p;

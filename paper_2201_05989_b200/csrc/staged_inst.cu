@@ -36,6 +36,8 @@ cudaError_t launch_fused_train_d2(const FieldShape&, const LevelDev*, const Trai
 cudaError_t launch_fused_train_d3(const FieldShape&, const LevelDev*, const TrainArgs&, int, cudaStream_t, int*);
 cudaError_t launch_fused_dout_d2(const FieldShape&, const LevelDev*, const TrainArgs&, int, cudaStream_t, int*);
 cudaError_t launch_fused_dout_d3(const FieldShape&, const LevelDev*, const TrainArgs&, int, cudaStream_t, int*);
+cudaError_t launch_fused_store_d2(const FieldShape&, const LevelDev*, const TrainArgs&, int, cudaStream_t, int*);
+cudaError_t launch_fused_store_d3(const FieldShape&, const LevelDev*, const TrainArgs&, int, cudaStream_t, int*);
 cudaError_t launch_fused_infer_d2(const FieldShape&, const LevelDev*, const InferArgs&, int, cudaStream_t);
 cudaError_t launch_fused_infer_d3(const FieldShape&, const LevelDev*, const InferArgs&, int, cudaStream_t);
 
@@ -43,8 +45,10 @@ cudaError_t launch_train(const FieldShape& s, const LevelDev* lv, int src, int g
                          int num_sms, cudaStream_t st, int* grid_used)
 {
     if (src == SRC_ENCODE) {
-        if (sink != SINK_SCATTER)
-            return cudaErrorNotSupported;
+        if (sink == SINK_STORE)
+            return grad != GRAD_LOSS ? cudaErrorNotSupported
+                   : s.grid.d == 2   ? launch_fused_store_d2(s, lv, a, num_sms, st, grid_used)
+                                     : launch_fused_store_d3(s, lv, a, num_sms, st, grid_used);
         if (grad == GRAD_DOUT)
             return s.grid.d == 2 ? launch_fused_dout_d2(s, lv, a, num_sms, st, grid_used)
                                  : launch_fused_dout_d3(s, lv, a, num_sms, st, grid_used);

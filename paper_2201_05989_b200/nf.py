@@ -195,10 +195,11 @@ class Options:
     fused_train: bool = True    # one fused kernel per step vs staged encode / MLP / encode-bwd kernels
     deterministic: bool = False  # bit-reproducible backward in the reference's accumulation order
     mlp_engine: int = 0         # 0: measured-faster tensor-core engine per kernel, 1: mma.sync, 2: tcgen05
+    dp_exchange: int = 0        # 0/1: chunked all-reduce pipelined with Adam, 2: level-pipelined scatter + exchange
 
     def c(self) -> L.nfg_options:
         return L.nfg_options(int(self.table_fp32), int(self.fused_train), int(self.deterministic),
-                             int(self.mlp_engine))
+                             int(self.mlp_engine), int(self.dp_exchange))
 
 
 class Context:

@@ -30,7 +30,7 @@ def test_exports_every_declared_symbol(lib):
     for n in names:
         assert hasattr(lib, n), n
     assert set(names) == set(_lib.SIGNATURES), set(names) ^ set(_lib.SIGNATURES)
-    assert lib.nfg_abi_version() == 3
+    assert lib.nfg_abi_version() == 4
 
 
 def test_library_is_sm100a():

@@ -11,14 +11,14 @@ from test_gpu_parity import _nf
 pytestmark = pytest.mark.gpu
 
 
-def _pair(nf, det):
+def _pair(nf, det, exchange=0, table_fp32=False):
     import torch  # noqa: F401  (loads torch's libnccl for the communicator)
     plain = nf.Context(0)
     dp = nf.Context(0)
     dp.attach_comm(nf.Context.unique_id(), 0, 1)
     models = []
     for ctx in (plain, dp):
-        m = nf.FieldModel(ctx, options=nf.Options(deterministic=det))
+        m = nf.FieldModel(ctx, options=nf.Options(deterministic=det, dp_exchange=exchange, table_fp32=table_fp32))
         m.hash_cfg = nf.HashEncodingConfig(dims=3, levels=16, table_size=1 << 19, features=2, n_min=16, n_max=2048)
         m.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=1)
         m.hyper = nf.AdamHyper(lr=1e-3)
@@ -117,3 +117,59 @@ def test_broadcast_and_comm_info():
     assert np.array_equal(b.evaluate(X[:256]), out0)
     with pytest.raises(ValueError):
         b.broadcast(1)   # root outside the communicator
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("exchange", [1, 2])   # NFG_DP_ALLREDUCE, NFG_DP_LEVELS
+def test_dp_exchanges_track_single_process(exchange, fp32):
+    """Both data-parallel exchanges on a 1-rank communicator against the
+    single-process fused step. NFG_DP_LEVELS runs the fused kernel with dY
+    stored, scatters the table gradients level group by level group (finest
+    first) and all-reduces / updates each group separately: every gradient
+    range must be reduced and updated exactly once (all gradients zero after
+    Adam, every level moves), and the steps track the fused single-process path
+    (same loss to fp32 summation order; scatter order differs)."""
+    nf = _nf()
+    (a, b), ctxs = _pair(nf, det=False, exchange=exchange, table_fp32=fp32)
+    rng = O.Pcg32(7, 7)
+    P0 = b.params
+    for step in range(1, 4):
+        X = rng.floats(3 * 50000).reshape(-1, 3)
+        T = O.csg_sdf(X).reshape(-1, 1)
+        la = a.train_step(X, T, nf.LossKind.Mape, step)
+        lb = b.train_step(X, T, nf.LossKind.Mape, step)
+        assert abs(la - lb) <= 1e-5 * abs(la), (step, la, lb)
+        assert not b.grads.any()
+        if exchange == 2:
+            assert "sink=1" in b.last_kernel_variant(0), b.last_kernel_variant(0)   # dY stored, not scattered
+        else:
+            assert "sink=0" in b.last_kernel_variant(0), b.last_kernel_variant(0)
+    assert a.step == b.step == 3
+    d = np.abs(a.params - b.params)
+    assert np.mean(d > 1e-5) < 0.02
+    # every level group (and the MLP) was updated
+    moved = b.params != P0
+    t = b.sizes[0]
+    g = O.GridCfg(levels=16, table_size=1 << 19, features=2, n_min=16, n_max=2048, dims=3)
+    for sp in O.level_resolutions(g):
+        lo, hi = 2 * sp.row_offset, 2 * (sp.row_offset + sp.table_len)
+        assert moved[lo:hi].any(), sp
+    assert moved[t:].mean() > 0.9
+
+
+def test_dp_levels_nonfinite_stands_down():   # adam.hpp:86-90 through the level-pipelined exchange
+    nf = _nf()
+    from paper_2201_05989_b200._lib import NfgNonFinite
+    (a, b), ctxs = _pair(nf, det=False, exchange=2)
+    rng = O.Pcg32(8, 8)
+    X = rng.floats(3 * 40000).reshape(-1, 3)
+    T = O.csg_sdf(X).reshape(-1, 1)
+    b.train_step(X, T, nf.LossKind.Mape, 1)
+    before = b.params
+    T2 = T.copy()
+    T2[123, 0] = np.nan
+    with pytest.raises(NfgNonFinite):
+        b.train_step(X, T2, nf.LossKind.L2, 2)
+    assert np.array_equal(b.params.view(np.uint32), before.view(np.uint32))
+    assert b.step == 1
+    assert np.isfinite(b.train_step(X, T, nf.LossKind.Mape, 2))
