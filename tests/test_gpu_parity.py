@@ -389,8 +389,24 @@ def test_train_step_parity(case, kind, n_out, sig, fused):   # model.cpp:111-138
     O.encode_backward(og, cache, dY, gt)
     assert abs(lg - lo) <= 1e-4 * abs(lo)
     assert np.array_equal(G[:t] != 0, gt != 0)           # same touched-entry set
-    for a, r in ((G[:t], gt), (G[t:t + w], gW), (G[t + w:], gb)):
-        assert np.linalg.norm(a - r) <= 6e-2 * np.linalg.norm(r)
+    # Gradient bound, derived rather than asserted (as test_gpu_headline): the
+    # kernel vs the exact fp16-operand emulation of the same step <= 1e-3
+    # (its math), and by the triangle inequality the kernel vs the fp32 oracle
+    # <= the emulation's own distance from the oracle (the cost of fp16
+    # operands on this batch, computed here) + 1e-3.
+    import _fp16ref as R
+    shapes = [(64, mc.input_width)] + [(64, 64)] * (mc.hidden_layers - 1) + [(n_out, 64)]
+    out_e, _, _, _ = R.forward(P[t:t + w], P[t + w:], shapes, Y, sig)
+    _, dpe = O.loss_with_grad(kind, out_e.astype(np.float32), T)
+    _, eW, eb, eY = R.backward(P[t:t + w], P[t + w:], shapes, Y, dpe, sig, tile=64)
+    ge = np.zeros(t, np.float32)
+    O.encode_backward(og, cache, eY.astype(np.float32), ge)
+
+    def rel(a, r):
+        return np.linalg.norm(np.asarray(a, np.float64) - r) / max(np.linalg.norm(np.asarray(r, np.float64)), 1e-30)
+    for a, r, e in ((G[:t], gt, ge), (G[t:t + w], gW, eW), (G[t + w:], gb, eb)):
+        assert rel(a, e) <= 1e-3, (rel(a, e), rel(e, r))
+        assert rel(a, r) <= rel(e, r) + 1e-3, (rel(a, r), rel(e, r))
         big = np.abs(r) > 1e-2 * np.abs(r).max()
         assert np.mean(np.sign(a[big]) == np.sign(r[big])) > 0.99
     m.write(1, np.zeros_like(G))
@@ -455,11 +471,15 @@ def test_evaluate_parity(fp32, levels):   # model.cpp:102-109 (fused encode + ML
     for step in range(1, 6):
         X = rng.floats(30000).reshape(-1, 3)
         m.train_step(X, O.csg_sdf(X).reshape(-1, 1), nf.LossKind.Mape, step)
-    f.params[:] = m.params
+    P = m.params
+    if not fp32:   # the kernel gathers the fp16 shadow: the oracle reads the same rounded tables
+        t = m.sizes[0]
+        P[:t] = P[:t].astype(np.float16).astype(np.float32)
+    f.params[:] = P
     X = _points(1 << 16, 3, seed=77)
     out = m.evaluate(X)
     ref = f.evaluate(X)
-    assert np.abs(out - ref).max() <= 1e-2 * np.abs(ref).max() + 1e-4
+    assert np.abs(out - ref).max() <= 2e-3 * np.abs(ref).max() + 1e-5   # §8c MLP-output contract (fp16 MMA)
 
 
 def test_image_loss_curve_parity():   # loss curves, config-1 shape, 128^2 image, 300 steps

@@ -34,8 +34,11 @@ METRICS = [
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
-                         check=True).stdout
+    if rep.endswith(".csv"):   # exported on the GPU box (large reports are not copied back)
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     res = {}
@@ -60,14 +63,17 @@ def launches(path):
 
 def main():
     tag = sys.argv[1]
-    out = {"round": 1, "tag": tag,
+    out = {"round": 2 if tag.startswith("r2") else 1, "tag": tag,
            "source": "ncu --set full --clock-control none --import-source on (one launch each, bench.py config-2 "
                      "workload); launch list: ncu --metrics gpu__time_duration.sum --clock-control none",
            "kernels": {}}
     for k in ("k_train", "k_adam", "k_infer"):
         rep = os.path.join(ROOT, "gpurun_out", f"prof_{k}_{tag}.ncu-rep")
+        csv_ = os.path.join(ROOT, "gpurun_out", f"prof_{k}_{tag}_raw.csv")
         if os.path.exists(rep):
             out["kernels"][k] = raw(rep)
+        elif os.path.exists(csv_):
+            out["kernels"][k] = raw(csv_)
     lp = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
     if os.path.exists(lp):
         out["launch_list_us"] = launches(lp)
