@@ -283,6 +283,10 @@ struct nfg_ctx {
     // stream memory write of its ready flag (copy engine + front end only)
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_order = nullptr;
+    // early step result (host-pointer steps): the loss / flags are read back on
+    // res_stream as soon as the backward is final, while Adam still runs
+    cudaStream_t res_stream = nullptr;
+    cudaEvent_t ev_res = nullptr, ev_res_done = nullptr;
     // data parallelism: NCCL runs the gradient all-reduce in chunks on its own
     // stream while Adam updates the chunks already reduced
     cudaStream_t comm_stream = nullptr;
@@ -354,6 +358,7 @@ struct nfg_field {
     nfg_adam_hyper hyper{ 1e-2, 0.9, 0.99, 1e-15, 1e-6 };
     nfg_options opts{ 0, 1, 0, 0 };
     int train_grid = 0;   // CTAs of the last fused train launch (the persistent kernel's first wave)
+    bool early_result = false;   // host_train_step: read the step result before Adam finishes
     std::vector<int64_t> milestones;
     double factor = 0.33;
     std::vector<nfg_level_spec> levels;
@@ -591,10 +596,13 @@ void det_prepare(nfg_field* f, nfg::TrainArgs& a, int64_t B, bool with_loss)
 {
     nfg_ctx* c = f->ctx;
     const int64_t ntiles = (B + 15) / 16;   // >= tiles of any train instantiation
-    const int64_t max_grid = std::min<int64_t>(ntiles, int64_t(c->num_sms) * 16);
+    // tile workers: CTAs, or groups of CTAs (k_train TCW), plus a group's rounding slack
+    const int64_t max_grid = std::min<int64_t>(ntiles, int64_t(c->num_sms) * 16) + 8;
     a.n_w = int64_t(f->n_w);
     a.n_wb = int64_t(f->n_w + f->n_b);
     a.part_wb = static_cast<float*>(f->det_part.get(size_t(std::max<int64_t>(max_grid, 1)) * size_t(a.n_wb) * 4));
+    // idle workers (no tile) write no dW partials: start from zeros
+    NFG_CUDA(cudaMemsetAsync(a.part_wb, 0, size_t(max_grid) * size_t(a.n_wb) * 4, c->stream));
     a.part_loss = with_loss ? static_cast<double*>(f->det_loss.get(
                                   size_t(std::max<int64_t>(max_grid, 1)) * nfg::train_warps_per_cta() * 8))
                             : nullptr;
@@ -839,6 +847,16 @@ void device_train_step(nfg_field* f, const float* X, const float* target, int64_
     device_backward(f, X, target, B_local, B_global, loss_kind, sm, true, /*reduce_grads=*/!dp);
     after_backward();   // streamed steps: enqueue the batch copies before the optimizer launches
     const float lr_now = float(nfg::host::lr_at(f->milestones, f->factor, f->hyper.lr, step));
+    if (!dp && f->early_result) {
+        // the loss sum and the producers' flags are final here: read them back
+        // on a side stream while Adam runs (host_train_step returns without
+        // waiting for Adam when no flag is set: Adam then cannot abort)
+        NFG_CUDA(cudaEventRecord(c->ev_res, c->stream));
+        NFG_CUDA(cudaStreamWaitEvent(c->res_stream, c->ev_res, 0));
+        NFG_CUDA(cudaMemcpyAsync(f->h_res, f->d_res, sizeof(StepResult) + 4 * sizeof(unsigned int),
+                                 cudaMemcpyDeviceToHost, c->res_stream));
+        NFG_CUDA(cudaEventRecord(c->ev_res_done, c->res_stream));
+    }
     if (!dp) {
         Span span(c, 1);
         run_adam(f, lr_now, false);
@@ -982,6 +1000,9 @@ nfg_status nfg_ctx_create(int device, nfg_ctx** out)
             NFG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
             NFG_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
             NFG_CUDA(cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming));
+            NFG_CUDA(cudaStreamCreateWithFlags(&c->res_stream, cudaStreamNonBlocking));
+            NFG_CUDA(cudaEventCreateWithFlags(&c->ev_res, cudaEventDisableTiming));
+            NFG_CUDA(cudaEventCreateWithFlags(&c->ev_res_done, cudaEventDisableTiming));
             void* fn = nullptr;
             cudaDriverEntryPointQueryResult q;
             if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
@@ -1405,6 +1426,7 @@ static void host_train_step(nfg_field* f, const float* X, const float* target, i
     const int d = f->gcfg.dims, no = f->mcfg.output_width;
     const uint64_t before = f->step;
     const bool was_clean = f->grads_clean;
+    f->early_result = c->comm == nullptr;   // single process: read the result while Adam runs
     const bool can_stream = f->stream_warm && f->grads_clean && f->opts.fused_train && !f->opts.deterministic &&
                             c->write_value32 && B >= (int64_t(1) << 15) && !launches_serialized();
     const bool pinned = can_stream && is_pinned(X) && is_pinned(target);
@@ -1523,7 +1545,19 @@ static void host_train_step(nfg_field* f, const float* X, const float* target, i
         const float* dT = stage(c->s1, target, size_t(B) * no, c->stream);
         device_train_step(f, dX, dT, B, B_global, loss_kind, step);
     }
-    fetch_result(f);
+    bool settled = false;
+    if (f->early_result) {
+        f->early_result = false;
+        NFG_CUDA(cudaEventSynchronize(c->ev_res_done));
+        const unsigned int* fl = f->h_res->flags;
+        // no producer flag and no abort: Adam cannot abort (its exact scan only
+        // runs when a producer flagged a possibly non-finite gradient), so the
+        // step's outcome is known and the host returns while Adam runs; every
+        // later use of the field is stream-ordered after it
+        settled = fl[0] == 0u && fl[1] == 0u && fl[3] == 0u && sticky_host(f)[0] == 0u;
+    }
+    if (!settled)
+        fetch_result(f);
     reset_scratch(f);   // for the next step, off its critical path (h_res holds this one)
     f->scratch_ready = true;
     if (f->h_res->flags[1]) {

@@ -74,6 +74,7 @@ struct TrainSmem {
     static constexpr int RED_OFF = DB_OFF + (NH + 1) * H * 4;
     static constexpr int STAGE_OFF = align16(RED_OFF + 4 * TW * 4);
     static constexpr int BYTES = STAGE_OFF + (ALIAS ? 0 : STAGE_BYTES);
+    static constexpr int GROUP_BYTES = 0;   // one group per CTA
 };
 
 // Per-warp aliasing of the gather staging (fp16 tables, F = 2, >= 2 hidden
@@ -162,7 +163,11 @@ struct TcSlots {
     }
 };
 
-template <int IN_STEPS, int NH, int STAGE_BYTES = 0, bool ALIAS = false>
+// NG groups of TW warps per CTA (TCW): the weights, biases and level table
+// are shared (one copy per SM), everything from ACT0_OFF on is per group
+// (GROUP_BYTES apart); each group runs its own tiles like a CTA of its own,
+// synchronising with a named barrier.
+template <int IN_STEPS, int NH, int STAGE_BYTES = 0, bool ALIAS = false, int NG = 1>
 struct TrainSmemTc {
     using Lay = WLayout<IN_STEPS, NH>;
     static constexpr int K0 = 16 * IN_STEPS;
@@ -180,11 +185,17 @@ struct TrainSmemTc {
     static constexpr int MBAR_OFF = align16(DBO_OFF + TW * OUTP * 4);
     static constexpr int TSLOT_OFF = MBAR_OFF + 8;
     static constexpr int STAGE_OFF = align16(TSLOT_OFF + 8);
-    static constexpr int BYTES = STAGE_OFF + (ALIAS ? 0 : STAGE_BYTES);
+    static constexpr int GROUP_BYTES = ((STAGE_OFF + (ALIAS ? 0 : STAGE_BYTES) - ACT0_OFF) + 127) & ~127;
+    static constexpr int BYTES = ACT0_OFF + NG * GROUP_BYTES;
     static constexpr int INS = Lay::INS, OS = OUTP + 8, DB_OFF = RED_OFF;   // (mma.sync-path names; unused)
     static constexpr int NCOLS = TcSlots<NH>::ncols(K0);
-    static constexpr uint32_t TMEM_COLS = tc::alloc_cols(NCOLS);
+    static constexpr uint32_t GROUP_COLS = tc::alloc_cols(NCOLS);       // TMEM columns per group
+    static constexpr uint32_t TMEM_COLS = tc::alloc_cols(int(GROUP_COLS) * NG);
 };
+
+#ifndef NFG_TRAIN_GROUPS
+#define NFG_TRAIN_GROUPS 1   // TCW: groups of TW warps per CTA; 3 (one weight copy per SM) measured slower: 290 vs 271 us
+#endif
 
 // Aliased gather staging in the canonical buffers: slot k of this lane lives in
 // buffer k / 16 (acth[0], acth[1], dz[0], dz[1]), feature block (k % 16) / 2,
@@ -298,28 +309,46 @@ __device__ __forceinline__ void load_x(float* x, const float* __restrict__ X, in
 #ifndef NFG_TRAIN_MIN_BLOCKS_TC
 #define NFG_TRAIN_MIN_BLOCKS_TC 3
 #endif
+template <bool TCW>
+struct TrainGroups {
+    static constexpr int NG = TCW ? NFG_TRAIN_GROUPS : 1;   // groups of TW warps per CTA
+    static constexpr int MIN_BLOCKS = TCW ? (NFG_TRAIN_MIN_BLOCKS_TC + NG - 1) / NG : NFG_TRAIN_MIN_BLOCKS;
+};
+
 template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IN_STEPS, int NH, bool TCW = false>
-__global__ void __launch_bounds__(TW * 32, TCW ? NFG_TRAIN_MIN_BLOCKS_TC : NFG_TRAIN_MIN_BLOCKS)
+__global__ void __launch_bounds__(TW * 32 * TrainGroups<TCW>::NG, TrainGroups<TCW>::MIN_BLOCKS)
 k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ levels)
 {
     using Lay = WLayout<IN_STEPS, NH>;
     using SG = StageGeo<SRC, D, F, TT, IN_STEPS>;
     using SA = StageAlias<SRC, D, F, TT, IN_STEPS, NH>;
     static_assert(!(TCW && SA::PREFETCH), "gather-ahead is an mma.sync-path experiment");
-    using SM = std::conditional_t<TCW, TrainSmemTc<IN_STEPS, NH, SG::BYTES, SA::ON>,
+    constexpr int NG = TrainGroups<TCW>::NG;
+    using SM = std::conditional_t<TCW, TrainSmemTc<IN_STEPS, NH, SG::BYTES, SA::ON, NG>,
                                   TrainSmem<IN_STEPS, NH, SG::BYTES, SA::ON>>;
     extern __shared__ __align__(16) unsigned char sm[];
+    // TCW: NG groups of TW warps; a group works like a CTA of its own (its
+    // tiles, buffers, barrier, TMEM columns); tid / warp are group-local
+    const int ctid = threadIdx.x, gi = (ctid >> 5) / TW;
+    const int64_t vblk = int64_t(blockIdx.x) * NG + gi, vgrid = int64_t(gridDim.x) * NG;
+    unsigned char* const smg = sm + (TCW ? gi * SM::GROUP_BYTES : 0);   // this group's buffers
+    auto gsync = [&] {
+        if constexpr (NG == 1)
+            __syncthreads();
+        else
+            tc::bar_sync(1 + gi, TW * 32);
+    };
     __half* ws = reinterpret_cast<__half*>(sm);
     float* bs = reinterpret_cast<float*>(sm + Lay::HALVES * 2);
     LevelDev* lvs = reinterpret_cast<LevelDev*>(sm + SM::LV_OFF);
-    __half* act0 = reinterpret_cast<__half*>(sm + SM::ACT0_OFF);
-    __half* acth = reinterpret_cast<__half*>(sm + SM::ACTH_OFF);
-    __half* dzh = reinterpret_cast<__half*>(sm + SM::DZH_OFF);
-    __half* dzo = reinterpret_cast<__half*>(sm + SM::DZO_OFF);
-    float* db = reinterpret_cast<float*>(sm + SM::DB_OFF);
-    float* red = reinterpret_cast<float*>(sm + SM::RED_OFF);
+    __half* act0 = reinterpret_cast<__half*>(smg + SM::ACT0_OFF);
+    __half* acth = reinterpret_cast<__half*>(smg + SM::ACTH_OFF);
+    __half* dzh = reinterpret_cast<__half*>(smg + SM::DZH_OFF);
+    __half* dzo = reinterpret_cast<__half*>(smg + SM::DZO_OFF);
+    float* db = reinterpret_cast<float*>(smg + SM::DB_OFF);
+    float* red = reinterpret_cast<float*>(smg + SM::RED_OFF);
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    const int tid = ctid % (TW * 32), lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
     // lane-pair gathers / reductions (encode.cuh): one level per lane (F == 2)
 #ifdef NFG_NO_LANE_PAIRS
     constexpr bool LPG = false, LPS = false;
@@ -331,29 +360,29 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     const MlpShape msh{ s.in_real, s.n_out, s.sigmoid, s.hidden_width };
     load_weights<IN_STEPS, NH>(ws, bs, a.W, a.b, msh);
     if (SRC == SRC_ENCODE)
-        for (int i = tid; i < s.grid.L; i += blockDim.x)
+        for (int i = ctid; i < s.grid.L; i += blockDim.x)
             lvs[i] = levels[i];
     uint32_t tbase = 0, mbar = 0;
     if constexpr (TCW) {
         // ones blocks of the activation buffers (db = dz^T 1), TMEM, mbarrier
-        for (int i = tid; i < TS * 8; i += blockDim.x) {
+        for (int i = tid; i < TS * 8; i += TW * 32) {
             const int smp = i >> 3, c = i & 7;
             const __half v = __float2half_rn(c == 0 ? 1.0f : 0.0f);
-            *reinterpret_cast<__half*>(sm + SM::ACT0_OFF + kc_off(16 * IN_STEPS + c, smp)) = v;
+            *reinterpret_cast<__half*>(smg + SM::ACT0_OFF + kc_off(16 * IN_STEPS + c, smp)) = v;
 #pragma unroll
             for (int k = 0; k < NH; ++k)
-                *reinterpret_cast<__half*>(sm + SM::ACTH_OFF + k * SM::ACTH_BYTES + kc_off(H + c, smp)) = v;
+                *reinterpret_cast<__half*>(smg + SM::ACTH_OFF + k * SM::ACTH_BYTES + kc_off(H + c, smp)) = v;
         }
-        mbar = tc::smem_u32(sm + SM::MBAR_OFF);
+        mbar = tc::smem_u32(smg + SM::MBAR_OFF);
         if (tid == 0)
             tc::mbar_init(mbar, 1);
-        if (warp == 0)
+        if (ctid < 32)   // one allocation for the CTA; group gi uses columns [gi, gi + 1) * GROUP_COLS
             tc::tmem_alloc(reinterpret_cast<uint32_t*>(sm + SM::TSLOT_OFF), SM::TMEM_COLS);
         tc::fence_smem_async();
         tc::fence_before();
         __syncthreads();
         tc::fence_after();
-        tbase = *reinterpret_cast<const uint32_t*>(sm + SM::TSLOT_OFF);
+        tbase = *reinterpret_cast<const uint32_t*>(sm + SM::TSLOT_OFF) + uint32_t(gi) * SM::GROUP_COLS;
     }
     // padding columns of the activation buffers: a 1 then zeros (db_tile)
     for (int r = tid; !TCW && r < TS; r += blockDim.x) {
@@ -483,17 +512,17 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 fr[s0 + sl][2 * h + 1] = pack_half2(e8.x, e8.y);
             }
     };
-    const SlotsLinear lin_slots{ sm + SM::STAGE_OFF + tid * SG::SB, TW * 32 * SG::SB };
+    const SlotsLinear lin_slots{ smg + SM::STAGE_OFF + tid * SG::SB, TW * 32 * SG::SB };
     float xn[D], xn8[D];   // gather-ahead: inputs of the next tile
-    if (SA::PREFETCH && int64_t(blockIdx.x) < ntiles) {
-        wait_ready(blockIdx.x);
+    if (SA::PREFETCH && vblk < ntiles) {
+        wait_ready(vblk);
         if (a.ready)
-            __syncthreads();
-        load_inputs(blockIdx.x, xn, xn8);
-        const int64_t s0_ = int64_t(blockIdx.x) * TS + r0 + g;
+            gsync();
+        load_inputs(vblk, xn, xn8);
+        const int64_t s0_ = vblk * TS + r0 + g;
         issue_pass(0, lin_slots, xn, xn8, s0_ < a.B, s0_ + 8 < a.B);
     }
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int64_t tile = vblk; tile < ntiles; tile += vgrid) {
         NFG_PT_START();
         if (TCW && pending) {   // the previous tile's dW MMAs read the activation / dz / staging buffers
             tc::mbar_wait(mbar, mphase);
@@ -505,7 +534,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         const bool vg = sg < a.B, vg8 = sg8 < a.B;
         if (!SA::PREFETCH && a.ready) {   // streamed inputs: wait for this tile's chunk to land
             wait_ready(tile);
-            __syncthreads();
+            gsync();
         }
         float xg[D], xg8[D];
         if (SA::PREFETCH) {
@@ -539,7 +568,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                     __syncwarp();
                 blend_pass(0, lin_slots, xg, xg8, vg, vg8, afr);
             } else if constexpr (SA::ON && TCW) {
-                const SlotsKC<SM> slots{ sm + warp * 256 + lane * SG::SB };
+                const SlotsKC<SM> slots{ smg + warp * 256 + lane * SG::SB };
                 encode_all(slots);
                 __syncwarp();   // every lane's staged rows consumed before the warp writes them
             } else if constexpr (SA::ON) {
@@ -558,7 +587,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             input_frags<SRC, D, F, TT, IN_STEPS>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
         }
         if constexpr (TCW)
-            store_a_kc<IN_STEPS>(afr, sm + SM::ACT0_OFF, r0, lane);
+            store_a_kc<IN_STEPS>(afr, smg + SM::ACT0_OFF, r0, lane);
         else
             store_a<IN_STEPS>(afr, act0, SM::INS, r0, lane);
         NFG_PT(0);
@@ -571,7 +600,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         mask[0] = bias_relu<HT>(acc, bs, lane);
         c_to_a<4, false>(acc, ah);
         if constexpr (TCW)
-            store_a_kc<4>(ah, sm + SM::ACTH_OFF, r0, lane);
+            store_a_kc<4>(ah, smg + SM::ACTH_OFF, r0, lane);
         else
             store_a<4>(ah, acth, HS, r0, lane);
 #pragma unroll
@@ -580,7 +609,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             mask[k] = bias_relu<HT>(acc, bs + H * k, lane);
             c_to_a<4, false>(acc, ah);
             if constexpr (TCW)
-                store_a_kc<4>(ah, sm + SM::ACTH_OFF + k * SM::ACTH_BYTES, r0, lane);
+                store_a_kc<4>(ah, smg + SM::ACTH_OFF + k * SM::ACTH_BYTES, r0, lane);
             else
                 store_a<4>(ah, acth + k * TS * HS, HS, r0, lane);
         }
@@ -629,10 +658,10 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                     atomicAdd(a.scratch.loss_sum, double(term));
             }
         }
-        const int64_t next_tile = tile + gridDim.x;
+        const int64_t next_tile = tile + vgrid;
         if (SA::PREFETCH && next_tile < ntiles)
             wait_ready(next_tile);   // published to the CTA by the barrier below
-        __syncthreads();
+        gsync();
         NFG_PT(2);
         if (SA::PREFETCH && next_tile < ntiles) {
             // every warp has blended this tile (barrier above): its slots are free
@@ -692,7 +721,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         uint32_t azo[1][4];
         c_to_a<1, true>(ao, azo);
         if constexpr (TCW) {
-            store_a_kc<1>(azo, sm + SM::DZO_OFF, r0, lane);
+            store_a_kc<1>(azo, smg + SM::DZO_OFF, r0, lane);
             // output bias gradient from the same fp16 dz the MMAs see
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
@@ -715,7 +744,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         for (int k = NH - 1; k >= 1; --k) {
             c_to_a<4, true>(acc, ah);
             if constexpr (TCW)
-                store_a_kc<4>(ah, sm + SM::DZH_OFF + k * SM::DZH_BYTES, r0, lane);
+                store_a_kc<4>(ah, smg + SM::DZH_OFF + k * SM::DZH_BYTES, r0, lane);
             else
                 store_a<4>(ah, dzh + k * TS * HS, HS, r0, lane);
             layer_bwd<4, HT>(ah, Whs + (k - 1) * Lay::WH_HALVES, HS, acc, lane);
@@ -723,7 +752,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         }
         c_to_a<4, true>(acc, ah);
         if constexpr (TCW)
-            store_a_kc<4>(ah, sm + SM::DZH_OFF, r0, lane);
+            store_a_kc<4>(ah, smg + SM::DZH_OFF, r0, lane);
         else
             store_a<4>(ah, dzh, HS, r0, lane);
         float ay[2 * IN_STEPS][4];
@@ -777,14 +806,14 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             // ---- dW / db += dz^T [act | 1] on tcgen05, accumulated in TMEM ----------
             tc::fence_smem_async();   // this tile's activation / dz stores -> tensor core
             tc::fence_before();
-            __syncthreads();
+            gsync();
             NFG_PT(5);
             if (tid == 0) {
                 tc::fence_after();
                 constexpr int K0 = 16 * IN_STEPS;
                 constexpr uint32_t ID0 = tc::idesc_f16_mn(64, K0 + 8), IDH = tc::idesc_f16_mn(64, H + 8),
                                    IDO = tc::idesc_f16_mn(64, OUTP);
-                const uint32_t s0 = tc::smem_u32(sm);
+                const uint32_t s0 = tc::smem_u32(smg);
                 auto slot = [&](int k) {
                     return tbase + ((k & 1) ? (16u << 16) : 0u) + uint32_t((k >> 1) * TcSlots<NH>::COLS);
                 };
@@ -915,14 +944,14 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                     const float val = v[i] * fs;
                     bad |= !sane(val);
                     if (a.part_wb)
-                        a.part_wb[blockIdx.x * a.n_wb + (is_b ? a.n_w : 0) + idx] = val;
+                        a.part_wb[vblk * a.n_wb + (is_b ? a.n_w : 0) + idx] = val;
                     else
                         atomicAdd((is_b ? a.gb : a.gW) + idx, val);
                 }
             }
         }
         // output bias: per-warp partials (lanes g == 0), summed over the warps in order
-        float* dbo_s = reinterpret_cast<float*>(sm + SM::DBO_OFF);
+        float* dbo_s = reinterpret_cast<float*>(smg + SM::DBO_OFF);
         if (g == 0)
 #pragma unroll
             for (int j = 0; j < 2; ++j)
@@ -930,7 +959,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 for (int b = 0; b < 2; ++b)
                     dbo_s[warp * OUTP + 8 * j + 2 * t + b] = dbo4[j][b];
         tc::fence_before();
-        __syncthreads();
+        gsync();
         tc::fence_after();
         if (tid < s.n_out) {
             float v = 0.0f;
@@ -940,12 +969,14 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             v *= ic;
             bad |= !sane(v);
             if (a.part_wb)
-                a.part_wb[blockIdx.x * a.n_wb + a.n_w + NH * hw + tid] = v;
+                a.part_wb[vblk * a.n_wb + a.n_w + NH * hw + tid] = v;
             else
                 atomicAdd(a.gb + NH * hw + tid, v);
         }
-        if (warp == 0)
-            tc::tmem_dealloc(tbase, SM::TMEM_COLS);
+        if constexpr (NG > 1)
+            __syncthreads();   // every group has read its TMEM columns (before the dbo barrier)
+        if (ctid < 32)
+            tc::tmem_dealloc(*reinterpret_cast<const uint32_t*>(sm + SM::TSLOT_OFF), SM::TMEM_COLS);
     } else {
     auto flush = [&](const float (&cq)[2][4], int mt, int np, int out_k, int in_k, size_t woff) {
 #ifdef NFG_EXP_NO_FLUSH   // experiment builds only (tools/kbench.cu): upper bound of the dW flush cost
@@ -1014,7 +1045,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     }
     }   // mma.sync dW path
     if (GRAD == GRAD_LOSS && a.part_loss && lane == 0)
-        a.part_loss[blockIdx.x * TW + warp] = loss_acc;
+        a.part_loss[vblk * TW + warp] = loss_acc;
     if (__any_sync(0xffffffffu, bad) && lane == 0)
         atomicOr(a.scratch.flags, 1u);
     invalid = __reduce_or_sync(0xffffffffu, invalid);

@@ -17,8 +17,10 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
 {
     using SG = StageGeo<SRC, D, F, TT, IS>;
     constexpr bool ALIAS = StageAlias<SRC, D, F, TT, IS, NH>::ON;
-    using SM = std::conditional_t<TCW, TrainSmemTc<IS, NH, SG::BYTES, ALIAS>, TrainSmem<IS, NH, SG::BYTES, ALIAS>>;
+    constexpr int NG = TrainGroups<TCW>::NG;
+    using SM = std::conditional_t<TCW, TrainSmemTc<IS, NH, SG::BYTES, ALIAS, NG>, TrainSmem<IS, NH, SG::BYTES, ALIAS>>;
     auto k = k_train<SRC, GRAD, SINK, D, F, TT, IS, NH, TCW>;
+    constexpr int threads = TW * 32 * NG;
     static int per_sm = -1;   // resolved once per instantiation
     if (per_sm < 0) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
@@ -30,7 +32,7 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
                 return e;
         }
         int n = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, TW * 32, SM::BYTES);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, threads, SM::BYTES);
         if (e != cudaSuccess)
             return e;
         const int n_occ = n;
@@ -48,10 +50,10 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
                 (e = cudaDeviceGetAttribute(&smem_resv, cudaDevAttrReservedSharedMemoryPerBlock, dev)) != cudaSuccess)
                 return e;
             const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
-            const int by_regs = 65536 / (regs_warp * TW);
+            const int by_regs = 65536 / (regs_warp * TW * NG);
             const int by_smem = smem_sm / (SM::BYTES + int(fa.sharedSizeBytes) + smem_resv);
-            const int by_tmem = int(512 / TrainSmemTc<IS, NH>::TMEM_COLS);
-            n = std::max(1, std::min({ by_regs, by_smem, by_tmem, 2048 / (TW * 32) }));
+            const int by_tmem = int(512 / SM::TMEM_COLS);
+            n = std::max(1, std::min({ by_regs, by_smem, by_tmem, 2048 / threads }));
         }
         per_sm = std::max(n, 1);
         if (const char* o = getenv("NFG_TRAIN_CTAS_PER_SM"))   // experiment hook (grid sizing only)
@@ -67,16 +69,17 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
     static char desc[192];
     if (!desc[0])
         snprintf(desc, sizeof(desc), "k_train src=%d grad=%d sink=%d d=%d F=%d table=%s in_steps=%d hidden=%d "
-                 "stage_alias=%d ctas_per_sm=%d dw=%s", SRC, GRAD, SINK, D, F, sizeof(TT) == 2 ? "f16" : "f32", IS,
-                 NH, int(ALIAS), per_sm, TCW ? "tcgen05" : "mma.sync");
+                 "stage_alias=%d ctas_per_sm=%d groups=%d dw=%s", SRC, GRAD, SINK, D, F, sizeof(TT) == 2 ? "f16" : "f32",
+                 IS, NH, int(ALIAS), per_sm, NG, TCW ? "tcgen05" : "mma.sync");
     note_kernel_variant(0, desc);
     const int64_t ntiles = (a.B + TS - 1) / TS;
     if (ntiles <= 0)
         return cudaSuccess;
-    const int grid = int(std::min<int64_t>(ntiles, int64_t(num_sms) * per_sm));
+    // grid_used counts tile workers (groups): the deterministic partials are per group
+    const int grid = int(std::min<int64_t>((ntiles + NG - 1) / NG, int64_t(num_sms) * per_sm));
     if (grid_used)
-        *grid_used = grid;
-    k<<<grid, TW * 32, SM::BYTES, st>>>(a, s, lv);
+        *grid_used = grid * NG;
+    k<<<grid, threads, SM::BYTES, st>>>(a, s, lv);
     return cudaGetLastError();
 }
 
