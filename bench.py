@@ -510,11 +510,12 @@ def main():
         step += 1
         model.train_step_host_ptr(Xh.ptr, Th.ptr, B_TRAIN, nf.LossKind.Mape, step)
     barrier()
-    e2e_steps = max(5, args.steps // 2)
+    e2e_steps = max(10, args.steps)
     t0 = time.perf_counter()
     for i in range(e2e_steps):
         step += 1
         loss = model.train_step_host_ptr(Xh.ptr, Th.ptr, B_TRAIN, nf.LossKind.Mape, step)
+    ctx.synchronize()   # train_step returns once its loss is known; the last Adam belongs in the region
     t_e2e = time.perf_counter() - t0
     if world > 1:
         tt = torch.tensor([t_e2e], device="cuda")
@@ -535,6 +536,7 @@ def main():
     for i in range(e2e_steps):
         step += 1
         loss = model.train_step_host_ptr(Xp.ctypes.data, Tp.ctypes.data, B_TRAIN, nf.LossKind.Mape, step)
+    ctx.synchronize()
     t_pg = time.perf_counter() - t0
     if world > 1:
         tt = torch.tensor([t_pg], device="cuda")

@@ -287,6 +287,9 @@ struct nfg_ctx {
     // res_stream as soon as the backward is final, while Adam still runs
     cudaStream_t res_stream = nullptr;
     cudaEvent_t ev_res = nullptr, ev_res_done = nullptr;
+    // the last host call was a train step that returned once its fused kernel
+    // had finished: nothing queued on the main stream reads the staging buffers
+    bool staging_idle = false;
     // data parallelism: NCCL runs the gradient all-reduce in chunks on its own
     // stream while Adam updates the chunks already reduced
     cudaStream_t comm_stream = nullptr;
@@ -1426,6 +1429,8 @@ static void host_train_step(nfg_field* f, const float* X, const float* target, i
     const int d = f->gcfg.dims, no = f->mcfg.output_width;
     const uint64_t before = f->step;
     const bool was_clean = f->grads_clean;
+    const bool staging_idle = c->staging_idle;
+    c->staging_idle = false;
     f->early_result = c->comm == nullptr;   // single process: read the result while Adam runs
     const bool can_stream = f->stream_warm && f->grads_clean && f->opts.fused_train && !f->opts.deterministic &&
                             c->write_value32 && B >= (int64_t(1) << 15) && !launches_serialized();
@@ -1491,8 +1496,10 @@ static void host_train_step(nfg_field* f, const float* X, const float* target, i
             srcT = hT;
         }
         const unsigned int epoch = ++f->epoch;
-        NFG_CUDA(cudaEventRecord(c->ev_order, c->stream));        // staging buffers free
-        NFG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_order, 0));
+        if (!staging_idle) {   // else the previous step's Adam may still run: the copies start under it
+            NFG_CUDA(cudaEventRecord(c->ev_order, c->stream));   // staging buffers free
+            NFG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_order, 0));
+        }
         int64_t k = 0, caller_chunks = 0;
         auto enqueue_copies = [&] {
             for (; k < nchunks; ++k) {
@@ -1558,6 +1565,9 @@ static void host_train_step(nfg_field* f, const float* X, const float* target, i
     }
     if (!settled)
         fetch_result(f);
+    // host-pointer calls are synchronous: every kernel that read this step's
+    // staged inputs has finished (the fused kernel, or the whole step)
+    c->staging_idle = true;
     reset_scratch(f);   // for the next step, off its critical path (h_res holds this one)
     f->scratch_ready = true;
     if (f->h_res->flags[1]) {
