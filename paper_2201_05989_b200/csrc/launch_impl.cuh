@@ -9,6 +9,10 @@
 #include "field_kernels.cuh"
 #include "infer_tc.cuh"
 
+#ifndef NFG_MAX_DEVICES
+#define NFG_MAX_DEVICES 64
+#endif
+
 namespace nfg {
 
 template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IS, int NH, bool TCW>
@@ -21,8 +25,12 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
     using SM = std::conditional_t<TCW, TrainSmemTc<IS, NH, SG::BYTES, ALIAS, NG>, TrainSmem<IS, NH, SG::BYTES, ALIAS>>;
     auto k = k_train<SRC, GRAD, SINK, D, F, TT, IS, NH, TCW>;
     constexpr int threads = TW * 32 * NG;
-    static int per_sm = -1;   // resolved once per instantiation
-    if (per_sm < 0) {
+    static int per_sm_dev[NFG_MAX_DEVICES];   // resolved once per instantiation and device
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= NFG_MAX_DEVICES)
+        return cudaErrorInvalidDevice;
+    int& per_sm = per_sm_dev[dev];
+    if (per_sm <= 0) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
         if (e != cudaSuccess)
             return e;
@@ -43,8 +51,8 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
             // from the actual per-SM limits: registers, shared memory, threads,
             // and the 512 TMEM columns the resident CTAs share.
             cudaFuncAttributes fa{};
-            int dev = 0, smem_sm = 0, smem_resv = 0;
-            if ((e = cudaFuncGetAttributes(&fa, k)) != cudaSuccess || (e = cudaGetDevice(&dev)) != cudaSuccess ||
+            int smem_sm = 0, smem_resv = 0;
+            if ((e = cudaFuncGetAttributes(&fa, k)) != cudaSuccess ||
                 (e = cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev)) !=
                     cudaSuccess ||
                 (e = cudaDeviceGetAttribute(&smem_resv, cudaDevAttrReservedSharedMemoryPerBlock, dev)) != cudaSuccess)
@@ -105,8 +113,12 @@ cudaError_t run_infer(const FieldShape& s, const LevelDev* lv, const InferArgs& 
 {
     using SM = InferSmem<IS, NH>;
     auto k = k_infer<SRC, D, F, TT, IS, NH>;
-    static int per_sm = -1;
-    if (per_sm < 0) {
+    static int per_sm_dev[NFG_MAX_DEVICES];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= NFG_MAX_DEVICES)
+        return cudaErrorInvalidDevice;
+    int& per_sm = per_sm_dev[dev];
+    if (per_sm <= 0) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
         if (e != cudaSuccess)
             return e;
@@ -135,12 +147,15 @@ cudaError_t run_infer_tc(const FieldShape& s, const LevelDev* lv, const InferArg
 {
     using SM = InferTcSmem<IS, NH>;
     auto k = k_infer_tc<SRC, D, F, TT, IS, NH>;
-    static bool ready = false;
-    if (!ready) {
+    static bool ready_dev[NFG_MAX_DEVICES];   // the attribute is per device context
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= NFG_MAX_DEVICES)
+        return cudaErrorInvalidDevice;
+    if (!ready_dev[dev]) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
         if (e != cudaSuccess)
             return e;
-        ready = true;
+        ready_dev[dev] = true;
     }
     static char desc[160];
     if (!desc[0])

@@ -35,12 +35,6 @@ using nfg::hc::grid_for;
 using nfg::hc::ok;
 using nfg::hc::run;
 
-
-
-
-
-
-
 struct Ray {
     double dir[3];
     double t, t_exit;

@@ -158,3 +158,33 @@ def test_train_dw_engines_agree(case, det):   # model.cpp:111-138, dW on tcgen05
     assert np.linalg.norm(g0[:t] - g1[:t]) <= 1e-4 * np.linalg.norm(g0[:t])   # dY identical up to fp32 order
     for a_, r_ in ((g1[t:t + w], g0[t:t + w]), (g1[t + w:], g0[t + w:])):
         assert np.linalg.norm(a_ - r_) <= 1e-3 * np.linalg.norm(r_)
+
+
+def test_train_dw_running_scale_rescales():   # the TMEM accumulators' dz scale decreasing tile by tile
+    """Targets that grow along the sample order make every later tile of a
+    CTA need a smaller power-of-two dz scale than the one its accumulators
+    hold, so the tcgen05 path rescales TMEM on (almost) every tile; the
+    result must still match the mma.sync path's per-tile-scaled reduction."""
+    from paper_2201_05989_b200 import nf
+    g = _grid(nf, dims=3, levels=16, table_size=1 << 16, features=2, n_min=16, n_max=512)
+    ms = []
+    for eng in (SYNC, TC):
+        m = nf.FieldModel(options=nf.Options(mlp_engine=eng, deterministic=True))
+        m.hash_cfg = g
+        m.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=1)
+        m.init(5)
+        ms.append(m)
+    B = 1 << 17
+    X = _points(B, 3, seed=11)
+    ramp = np.exp2(np.linspace(-12.0, 12.0, B)).astype(np.float32).reshape(-1, 1)   # |d| spans 2^24
+    T = (O.csg_sdf(X).reshape(-1, 1) * ramp).astype(np.float32)
+    out = []
+    for m in ms:
+        loss = m.gradients(X, T, nf.LossKind.L2)
+        out.append((loss, m.grads))
+    (l0, g0), (l1, g1) = out
+    t, w, b = ms[0].sizes
+    assert abs(l0 - l1) <= 1e-6 * abs(l0)
+    assert np.linalg.norm(g0[:t] - g1[:t]) <= 1e-4 * np.linalg.norm(g0[:t])
+    for a_, r_ in ((g1[t:t + w], g0[t:t + w]), (g1[t + w:], g0[t + w:])):
+        assert np.linalg.norm(a_ - r_) <= 1e-3 * np.linalg.norm(r_)
