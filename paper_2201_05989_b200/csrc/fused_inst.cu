@@ -6,6 +6,9 @@
 #ifndef NFG_D
 #error "compile with -DNFG_D=2 or -DNFG_D=3"
 #endif
+#ifndef NFG_PART
+#error "compile with -DNFG_PART=0..3"
+#endif
 #define NFG_CAT2(a, b) a##b
 #define NFG_CAT(a, b) NFG_CAT2(a, b)
 
@@ -28,19 +31,42 @@ namespace nfg {
     X(1, __half, 2, 2) X(4, __half, 2, 2) X(8, __half, 2, 2)                  \
     X(1, float, 2, 2) X(4, float, 2, 2) X(8, float, 2, 2)
 
+// The instantiations are split over four translation units per dimension
+// (NFG_PART 0..3, Makefile) so a parallel build compiles them side by side.
+cudaError_t NFG_CAT(launch_fused_train_f32_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
+                                                     int num_sms, cudaStream_t st, int* grid_used);
+
+#if NFG_PART == 0
 cudaError_t NFG_CAT(launch_fused_train_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
                                                  int num_sms, cudaStream_t st, int* grid_used)
 {
-    const bool f32 = s.table_fp32 != 0;
+    if (s.table_fp32 != 0)
+        return NFG_CAT(launch_fused_train_f32_d, NFG_D)(s, lv, a, num_sms, st, grid_used);
 #define X(F_, TT_, IS_, NH_)                                                                               \
-    if (s.grid.F == F_ && f32 == (sizeof(TT_) == 4) && s.in_steps == IS_ && s.hidden_layers == NH_)         \
-        return run_train<SRC_ENCODE, GRAD_LOSS, SINK_SCATTER, NFG_D, F_, TT_, IS_, NH_>(s, lv, a, num_sms, st, \
-                                                                                         grid_used);
+    if (sizeof(TT_) == 2 && s.grid.F == F_ && s.in_steps == IS_ && s.hidden_layers == NH_)                 \
+        return run_train<SRC_ENCODE, GRAD_LOSS, SINK_SCATTER, NFG_D, F_, __half, IS_, NH_>(s, lv, a, num_sms,  \
+                                                                                            st, grid_used);
     NFG_FUSED_LIST(X)
 #undef X
     return cudaErrorNotSupported;
 }
+#endif
 
+#if NFG_PART == 1
+cudaError_t NFG_CAT(launch_fused_train_f32_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
+                                                     int num_sms, cudaStream_t st, int* grid_used)
+{
+#define X(F_, TT_, IS_, NH_)                                                                               \
+    if (sizeof(TT_) == 4 && s.grid.F == F_ && s.in_steps == IS_ && s.hidden_layers == NH_)                 \
+        return run_train<SRC_ENCODE, GRAD_LOSS, SINK_SCATTER, NFG_D, F_, float, IS_, NH_>(s, lv, a, num_sms,   \
+                                                                                           st, grid_used);
+    NFG_FUSED_LIST(X)
+#undef X
+    return cudaErrorNotSupported;
+}
+#endif
+
+#if NFG_PART == 3
 // Whether a fused instantiation exists for this shape (the field falls back to
 // the staged kernels otherwise).
 bool NFG_CAT(fused_supported_d, NFG_D)(const FieldShape& s)
@@ -54,6 +80,9 @@ bool NFG_CAT(fused_supported_d, NFG_D)(const FieldShape& s)
     return false;
 }
 
+#endif
+
+#if NFG_PART == 2
 // Fused backward with an external dLoss/dOutput (nfg_field_backward_device:
 // the NeRF density network, 3D, L*F = 32, 1 or 2 hidden layers).
 cudaError_t NFG_CAT(launch_fused_dout_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
@@ -91,6 +120,9 @@ cudaError_t NFG_CAT(launch_fused_store_d, NFG_D)(const FieldShape& s, const Leve
     return cudaErrorNotSupported;
 }
 
+#endif
+
+#if NFG_PART == 3
 cudaError_t NFG_CAT(launch_fused_infer_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const InferArgs& a,
                                                  int num_sms, cudaStream_t st)
 {
@@ -109,5 +141,7 @@ cudaError_t NFG_CAT(launch_fused_infer_d, NFG_D)(const FieldShape& s, const Leve
 #undef X
     return cudaErrorNotSupported;
 }
+
+#endif
 
 }   // namespace nfg
