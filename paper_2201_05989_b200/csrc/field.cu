@@ -1032,6 +1032,8 @@ nfg_status nfg_ctx_destroy(nfg_ctx* c)
     return guard([&] {
         if (!c)
             return;
+        if (c->stream)
+            cudaStreamSynchronize(c->stream);   // an early-returned step's Adam may still run
         if (c->comm)
             nccl().comm_destroy(c->comm);
         for (auto& r : c->recs) {
@@ -1054,6 +1056,17 @@ nfg_status nfg_ctx_destroy(nfg_ctx* c)
         for (auto e : c->ev_chunk)
             if (e)
                 cudaEventDestroy(e);
+        for (auto e : c->ev_scat)
+            if (e)
+                cudaEventDestroy(e);
+        for (auto e : c->ev_red)
+            if (e)
+                cudaEventDestroy(e);
+        for (cudaEvent_t e : { c->ev_scr, c->ev_res, c->ev_res_done })
+            if (e)
+                cudaEventDestroy(e);
+        if (c->res_stream)
+            cudaStreamDestroy(c->res_stream);
         delete c;
     });
 }
@@ -1272,6 +1285,9 @@ nfg_status nfg_field_destroy(nfg_field* f)
     return guard([&] {
         if (!f)
             return;
+        // a host-pointer train_step may return while its Adam still runs
+        if (f->ctx && f->ctx->stream)
+            cudaStreamSynchronize(f->ctx->stream);
         for (void* p : { (void*)f->d_p, (void*)f->d_g, (void*)f->d_m, (void*)f->d_v, (void*)f->d_shadow,
                          (void*)f->d_levels, (void*)f->d_res, (void*)f->d_ready })
             if (p)
