@@ -747,6 +747,18 @@ void device_backward(nfg_field* f, const float* X, const float* target, int64_t 
     }
 }
 
+// Early step result: once the loss sum and the flags are final on `st`, copy
+// them to the host on the side stream (host_train_step may return before Adam).
+void enqueue_early_result(nfg_field* f, cudaStream_t st)
+{
+    nfg_ctx* c = f->ctx;
+    NFG_CUDA(cudaEventRecord(c->ev_res, st));
+    NFG_CUDA(cudaStreamWaitEvent(c->res_stream, c->ev_res, 0));
+    NFG_CUDA(cudaMemcpyAsync(f->h_res, f->d_res, sizeof(StepResult) + 4 * sizeof(unsigned int), cudaMemcpyDeviceToHost,
+                             c->res_stream));
+    NFG_CUDA(cudaEventRecord(c->ev_res_done, c->res_stream));
+}
+
 // Whether a data-parallel step takes the level-pipelined exchange (NFG_DP_LEVELS).
 bool dp_levels(const nfg_field* f)
 {
@@ -828,6 +840,8 @@ void device_train_step(nfg_field* f, const float* X, const float* target, int64_
         }
         nfg::AdamArgs a = adam_args(f, lr_now);
         NFG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_scr, 0));
+        if (f->early_result)   // after the reduced scratch AND the last scatter (it reads the staged inputs)
+            enqueue_early_result(f, c->stream);
         for (size_t k = 0; k < groups.size(); ++k) {
             const bool last = k + 1 == groups.size();
             NFG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_red[k], 0));
@@ -850,16 +864,12 @@ void device_train_step(nfg_field* f, const float* X, const float* target, int64_
     device_backward(f, X, target, B_local, B_global, loss_kind, sm, true, /*reduce_grads=*/!dp);
     after_backward();   // streamed steps: enqueue the batch copies before the optimizer launches
     const float lr_now = float(nfg::host::lr_at(f->milestones, f->factor, f->hyper.lr, step));
-    if (!dp && f->early_result) {
-        // the loss sum and the producers' flags are final here: read them back
-        // on a side stream while Adam runs (host_train_step returns without
-        // waiting for Adam when no flag is set: Adam then cannot abort)
-        NFG_CUDA(cudaEventRecord(c->ev_res, c->stream));
-        NFG_CUDA(cudaStreamWaitEvent(c->res_stream, c->ev_res, 0));
-        NFG_CUDA(cudaMemcpyAsync(f->h_res, f->d_res, sizeof(StepResult) + 4 * sizeof(unsigned int),
-                                 cudaMemcpyDeviceToHost, c->res_stream));
-        NFG_CUDA(cudaEventRecord(c->ev_res_done, c->res_stream));
-    }
+    // the loss sum and the producers' flags are final here (after the
+    // cross-rank scratch reduction with a communicator): read them back on a
+    // side stream while Adam runs (host_train_step returns without waiting for
+    // Adam when no flag is set: Adam then cannot abort)
+    if (!dp && f->early_result)
+        enqueue_early_result(f, c->stream);
     if (!dp) {
         Span span(c, 1);
         run_adam(f, lr_now, false);
@@ -873,6 +883,8 @@ void device_train_step(nfg_field* f, const float* X, const float* target, int64_
     // "throw before any update" (adam.hpp:86-90) holds across ranks.
     Span span(c, 2);
     reduce_scratch(f, c->stream);
+    if (f->early_result)
+        enqueue_early_result(f, c->stream);
     nfg::AdamArgs a = adam_args(f, lr_now);
     NFG_CUDA(cudaEventRecord(c->ev_grads, c->stream));
     NFG_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_grads, 0));
@@ -1447,7 +1459,7 @@ static void host_train_step(nfg_field* f, const float* X, const float* target, i
     const bool was_clean = f->grads_clean;
     const bool staging_idle = c->staging_idle;
     c->staging_idle = false;
-    f->early_result = c->comm == nullptr;   // single process: read the result while Adam runs
+    f->early_result = true;   // read the result while Adam (and a data-parallel exchange) runs
     const bool can_stream = f->stream_warm && f->grads_clean && f->opts.fused_train && !f->opts.deterministic &&
                             c->write_value32 && B >= (int64_t(1) << 15) && !launches_serialized();
     const bool pinned = can_stream && is_pinned(X) && is_pinned(target);

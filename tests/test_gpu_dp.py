@@ -64,18 +64,22 @@ def test_dp_fused_path_and_invalid_input():
     assert np.isfinite(lb2)
 
 
-def test_dp_streamed_host_pointer_steps():
+@pytest.mark.parametrize("exchange", [1, 2])
+def test_dp_streamed_host_pointer_steps(exchange):
     """Pinned host buffers with B >= 2^15 through the data-parallel path: the
     fused kernel waits for streamed chunks while the scratch reduction,
-    chunked all-reduce and per-chunk Adam are queued behind it. Losses and
+    exchange and Adam are queued behind it; train_step returns once the
+    reduced loss / flags are known (after the last scatter of the level-
+    pipelined exchange, which reads the staged inputs), and the next step's
+    copies overwrite the staging buffers under the previous Adam. Losses and
     parameters track the single-process streamed path."""
     nf = _nf()
-    (a, b), ctxs = _pair(nf, det=False)
+    (a, b), ctxs = _pair(nf, det=False, exchange=exchange)
     B = 1 << 16
     bufs = [(nf.PinnedBuffer((B, 3)), nf.PinnedBuffer((B, 1))) for _ in range(2)]
     try:
         rng = O.Pcg32(5, 5)
-        for step in range(1, 4):   # step 1 warms both fields up, steps 2-3 stream
+        for step in range(1, 6):   # step 1 warms both fields up, steps 2-5 stream
             X = rng.floats(3 * B).reshape(-1, 3)
             T = O.csg_sdf(X).reshape(-1, 1)
             losses = []
@@ -84,9 +88,9 @@ def test_dp_streamed_host_pointer_steps():
                 th.array[:] = T
                 losses.append(m.train_step_host_ptr(xh.ptr, th.ptr, B, nf.LossKind.Mape, step))
             assert abs(losses[0] - losses[1]) <= 1e-4 * abs(losses[0]), (step, losses)
-        assert a.step == b.step == 3
+        assert a.step == b.step == 5
         d = np.abs(a.params - b.params)
-        assert np.mean(d > 1e-5) < 0.02
+        assert np.mean(d > 1e-5) < 0.03
         assert not b.grads.any()
     finally:
         for xh, th in bufs:
