@@ -354,8 +354,17 @@ def cpu_reference(steps, warmup, seconds_cap, native=True, batch=B_TRAIN):
             break
     dt = time.perf_counter() - t0
     threads = O.lib(native).orc_max_threads()
+    # inference on the same host (queries/s at 2^20 queries; evaluate_chunked's
+    # 2^16-column chunks, tasks.cpp:34-45)
+    Q = O.Pcg32(7, 7).floats(3 * (1 << 20)).reshape(-1, 3)
+    f.evaluate(Q[:1 << 16])
+    t1 = time.perf_counter()
+    for c0 in range(0, 1 << 20, 1 << 16):
+        f.evaluate(Q[c0:c0 + (1 << 16)])
+    qps = (1 << 20) / (time.perf_counter() - t1)
     return {"value": done * batch / dt, "steps": done, "seconds": dt, "threads": threads,
-            "phases_s_per_step": {k: v / done for k, v in f.phase_times().items()}, "native": native}
+            "phases_s_per_step": {k: v / done for k, v in f.phase_times().items()}, "native": native,
+            "inference_queries_per_s": qps}
 
 
 def run_reference(args, rank, world):
@@ -372,7 +381,8 @@ def run_reference(args, rank, world):
             "data": "synthetic", "impl": "reference",
             "config": {"workload": WORKLOAD, "global_batch": B_TRAIN, "parallelism": "cpu"},
             "cpu_baseline": {"value": r["value"], "unit": "samples/s", "cores": r["threads"], "kind": "port",
-                             "sample": sample, "phases_s_per_step": r["phases_s_per_step"]},
+                             "sample": sample, "phases_s_per_step": r["phases_s_per_step"],
+                             "inference_queries_per_s": r["inference_queries_per_s"]},
             "e2e": {"value": r["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -671,7 +681,8 @@ def main():
         cpu = {"value": r["value"], "unit": "samples/s", "cores": r["threads"], "kind": "port",
                "sample": f"config2 at batch 2^16 (a quarter of the 2^18 workload), {r['steps']} steps in "
                          f"{r['seconds']:.1f} s, CPU restatement of the reference (-O2 -march=native, OpenMP)",
-               "phases_s_per_step": r["phases_s_per_step"]}
+               "phases_s_per_step": r["phases_s_per_step"],
+               "inference_queries_per_s": r["inference_queries_per_s"]}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,

@@ -18,6 +18,16 @@ for step in range(1, 3):
     X = rng.floats(700 * 3).reshape(-1, 3)
     print("loss", m.train_step(X, O.csg_sdf(X).reshape(-1, 1), nf.LossKind.Mape, step))
 print("eval", float(m.evaluate(X[:100]).sum()))
+if "engines" in sys.argv:   # both tensor-core engines, several tiles per CTA (TMEM accumulators, rescale)
+    for eng in (1, 2):
+        e = nf.FieldModel(options=nf.Options(mlp_engine=eng))
+        e.hash_cfg = nf.HashEncodingConfig(levels=16, table_size=1 << 14, features=2, n_min=16, n_max=512, dims=3)
+        e.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=1)
+        e.init(4)
+        X = rng.floats(70000 * 3).reshape(-1, 3)
+        T = (O.csg_sdf(X).reshape(-1, 1) * np.linspace(0.01, 100.0, 70000, dtype=np.float32)[:, None])
+        print("engine", eng, e.train_step(X, T.astype(np.float32), nf.LossKind.L2, 1),
+              float(e.evaluate(X[:5000]).sum()), e.last_kernel_variant(0), e.last_kernel_variant(1))
 if "nerf" in sys.argv:
     cams, focal = nf.orbit_cameras(2, width=16)
     imgs = nf.nerf_scene_render(cams, 16, 16, focal)
