@@ -42,6 +42,9 @@ cudaError_t NFG_CAT(launch_fused_train_d, NFG_D)(const FieldShape& s, const Leve
 {
     if (s.table_fp32 != 0)
         return NFG_CAT(launch_fused_train_f32_d, NFG_D)(s, lv, a, num_sms, st, grid_used);
+    if (train_ws_enabled() && train_tcw(s) && s.grid.F == 2 && s.in_steps == 2 && s.hidden_layers == 2 &&
+        a.part_wb == nullptr)   // warp-specialised variant (train_ws.cuh)
+        return run_train_ws<NFG_D, __half, 2, 2>(s, lv, a, num_sms, st, grid_used);
 #define X(F_, TT_, IS_, NH_)                                                                               \
     if (sizeof(TT_) == 2 && s.grid.F == F_ && s.in_steps == IS_ && s.hidden_layers == NH_)                 \
         return run_train<SRC_ENCODE, GRAD_LOSS, SINK_SCATTER, NFG_D, F_, __half, IS_, NH_>(s, lv, a, num_sms,  \

@@ -8,9 +8,13 @@
 
 #include "field_kernels.cuh"
 #include "infer_tc.cuh"
+#include "train_ws.cuh"
 
 #ifndef NFG_MAX_DEVICES
 #define NFG_MAX_DEVICES 64
+#endif
+#ifndef NFG_TRAIN_WS_DEFAULT
+#define NFG_TRAIN_WS_DEFAULT 0
 #endif
 
 namespace nfg {
@@ -89,6 +93,49 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
         *grid_used = grid * NG;
     k<<<grid, threads, SM::BYTES, st>>>(a, s, lv);
     return cudaGetLastError();
+}
+
+// Warp-specialised variant (train_ws.cuh): producers gather, consumers run the
+// MLP / reductions; 2 CTAs x 8 warps per SM.
+template <int D, typename TT, int IS, int NH>
+cudaError_t run_train_ws(const FieldShape& s, const LevelDev* lv, const TrainArgs& a, int num_sms, cudaStream_t st,
+                         int* grid_used)
+{
+    using SM = TrainWsSmem<D, TT, IS, NH>;
+    auto k = k_train_ws<D, TT, IS, NH>;
+    static bool ready_dev[NFG_MAX_DEVICES];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= NFG_MAX_DEVICES)
+        return cudaErrorInvalidDevice;
+    if (!ready_dev[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
+        if (e != cudaSuccess)
+            return e;
+        ready_dev[dev] = true;
+    }
+    static char desc[192];
+    if (!desc[0])
+        snprintf(desc, sizeof(desc), "k_train_ws src=0 grad=0 sink=0 d=%d F=2 table=%s in_steps=%d hidden=%d "
+                 "stage_alias=0 ctas_per_sm=2 warps=4+4 dw=tcgen05", D, sizeof(TT) == 2 ? "f16" : "f32", IS, NH);
+    note_kernel_variant(0, desc);
+    const int64_t ntiles = (a.B + TS - 1) / TS;
+    if (ntiles <= 0)
+        return cudaSuccess;
+    const int per_sm = getenv("NFG_WS_CTAS") ? std::max(1, atoi(getenv("NFG_WS_CTAS"))) : 2;
+    const int grid = int(std::min<int64_t>(ntiles, int64_t(num_sms) * per_sm));
+    if (grid_used)
+        *grid_used = grid;
+    k<<<grid, 256, SM::BYTES, st>>>(a, s, lv);
+    return cudaGetLastError();
+}
+
+inline bool train_ws_enabled()
+{
+    static const int on = [] {
+        const char* e = getenv("NFG_TRAIN_WS");
+        return e ? atoi(e) : NFG_TRAIN_WS_DEFAULT;
+    }();
+    return on != 0;
 }
 
 // Engine of the fused training kernel's dW reduction (nfg_options.mlp_engine).
