@@ -1,5 +1,7 @@
 // aux_kernels.cu — standalone encode fwd/bwd (component API), Adam, loss.
 #include "encode.cuh"
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace nfg {
@@ -225,6 +227,9 @@ cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cuda
 // forced): exact isfinite scan; records the first bad group and aborts.
 __global__ void __launch_bounds__(256) k_adam_check(const AdamArgs a, int force)
 {
+    // programmatic dependent launch (launch_adam): the producer's gradients are
+    // complete and visible past this point (a no-op for ordinary launches)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint64_t nn = a.n_tab + a.n_w + a.n_b;
     if (a.restore_on_invalid && (a.flags[3] & 3u) != 0u) {
         // invalid batch detected inside the speculative fused kernel: the slab
@@ -322,6 +327,7 @@ __device__ __forceinline__ void adam_quad(const AdamArgs& a, uint64_t i0, float4
 #endif
 __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
 {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (a.flags[1] != 0u) {   // non-finite gradient: state untouched (the reference throws first)
         // every Adam step that does not apply (the aborting one and those standing
         // down behind it, k_step_begin) is counted once, so nfg_field_check can
@@ -447,10 +453,36 @@ cudaError_t launch_adam_fallback(const AdamArgs& a, int num_sms, cudaStream_t st
     return cudaGetLastError();
 }
 
+// Launches with programmatic stream serialization: the grid may be scheduled
+// while its predecessor drains (the fused kernel's tail), and waits in
+// griddepcontrol.wait for its completion before touching the gradients.
+template <class K, class... Args>
+static cudaError_t launch_pdl(K kernel, int grid, int block, cudaStream_t st, Args... args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(unsigned(block));
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 cudaError_t launch_adam(const AdamArgs& a, bool force_check, int num_sms, cudaStream_t st)
 {
     const uint64_t n = a.n_tab + a.n_w + a.n_b;
     const int blocks = int(std::min<uint64_t>((n / 4 + 255) / 256 + 1, uint64_t(num_sms) * 8));
+    static const bool pdl = !getenv("NFG_NO_PDL");
+    if (pdl) {
+        cudaError_t e = launch_pdl(k_adam_check, num_sms * 4, 256, st, a, force_check ? 1 : 0);
+        if (e == cudaSuccess)
+            e = launch_pdl(k_adam, blocks, 256, st, a);
+        return e;
+    }
     k_adam_check<<<num_sms * 4, 256, 0, st>>>(a, force_check ? 1 : 0);
     k_adam<<<blocks, 256, 0, st>>>(a);
     return cudaGetLastError();

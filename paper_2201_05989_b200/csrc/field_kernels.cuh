@@ -357,6 +357,9 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
 #endif
     if (a.scratch.flags[3] != 0u)
         return;   // invalid input (k_validate): the reference throws before any update
+    // the optimizer launched behind this kernel (programmatic dependent launch)
+    // may get scheduled as CTAs retire; it waits for this grid's completion
+    asm volatile("griddepcontrol.launch_dependents;");
     const MlpShape msh{ s.in_real, s.n_out, s.sigmoid, s.hidden_width };
     load_weights<IN_STEPS, NH>(ws, bs, a.W, a.b, msh);
     if (SRC == SRC_ENCODE)
