@@ -596,10 +596,14 @@ def main():
             del Xs_, o_
 
     # ---- config 3: gigapixel image, tables beyond L2 (one GPU) ----------------------
+    # Secondary single-GPU numbers run on rank 0 only, on a context WITHOUT the
+    # communicator: a field on the data-parallel context would issue collectives
+    # the other ranks never join.
+    sctx = nf.Context(local) if world > 1 and rank == 0 and not args.no_nerf else ctx
     giga_line = None
     if rank == 0 and not args.no_nerf:   # secondary, single-GPU numbers: rank 0 only
         try:
-            giga_line = bench_gigapixel(nf, ctx, steps=max(5, args.steps // 2), warmup=3)
+            giga_line = bench_gigapixel(nf, sctx, steps=max(5, args.steps // 2), warmup=3)
         except Exception as e:
             giga_line = {"error": str(e)[:200]}
 
@@ -607,7 +611,7 @@ def main():
     nerf_line = None
     if rank == 0 and not args.no_nerf:
         try:
-            nerf_line = bench_nerf(nf, ctx, steps=max(10, args.steps), warmup=40)
+            nerf_line = bench_nerf(nf, sctx, steps=max(10, args.steps), warmup=40)
         except Exception as e:   # secondary number: never lose the headline line
             nerf_line = {"error": str(e)[:200]}
 
@@ -714,6 +718,7 @@ def main():
                 "params": n_params}
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()   # the other ranks wait for rank 0's single-GPU secondaries
         dist.destroy_process_group()
 
 

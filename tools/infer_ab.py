@@ -13,6 +13,7 @@ from paper_2201_05989_b200 import nf  # noqa: E402
 
 
 def main():
+    # arguments: log2 sizes (<= 40) or explicit query counts
     sizes = [int(a) for a in sys.argv[1:]] or [16, 18, 20, 22, 24, 26]
     ctx = nf.Context(0)
     ms = {}
@@ -33,7 +34,7 @@ def main():
     res = []
     gen = torch.Generator(device="cuda").manual_seed(7)
     for lg in sizes:
-        n = 1 << lg
+        n = 1 << lg if lg <= 40 else lg
         X = torch.rand(n, 3, device="cuda", generator=gen)
         outs = {}
         row = {"queries": n}
