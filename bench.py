@@ -234,14 +234,16 @@ def image_target_torch(X):
     return torch.stack([r, g, b], 1).clamp(0.0, 1.0).float().contiguous()
 
 
-def bench_gigapixel(nf, ctx, steps, warmup, T_log2=24):
+def bench_gigapixel(nf, ctx, steps, warmup, T_log2=24, n_max=8192, batch=None, metric=None, config=None):
     """BASELINE config 3 on one GPU: 2D hash L16 F2 T=2^24, N_max 8192, 2x64 MLP
     -> RGB sigmoid, L2, batch 2^18 of random points on the procedural image. The
     fp16 tables (1 GB) exceed L2: the HBM-bound gather regime; Adam runs its
-    sparse (skip-zero) pass since 2^18 x 4 corners touch ~6% of each level."""
+    sparse (skip-zero) pass since 2^18 x 4 corners touch ~6% of each level.
+    With T_log2=14, n_max=1024, batch 2^16 the same harness times config 1."""
     import torch
+    B_TRAIN = batch or globals()["B_TRAIN"]
     m = nf.FieldModel(ctx)
-    m.hash_cfg = nf.HashEncodingConfig(levels=16, table_size=1 << T_log2, features=2, n_min=16, n_max=8192, dims=2)
+    m.hash_cfg = nf.HashEncodingConfig(levels=16, table_size=1 << T_log2, features=2, n_min=16, n_max=n_max, dims=2)
     m.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=3,
                              output_activation=nf.OutputActivation.Sigmoid)
     m.hyper = nf.AdamHyper(lr=1e-2)
@@ -274,11 +276,13 @@ def bench_gigapixel(nf, ctx, steps, warmup, T_log2=24):
     ms = e0.elapsed_time(e1) / steps
     n = m.parameter_count()
     m.close()
-    return {"metric": "gigapixel-image training samples/s (config 3, one GPU)", "value": B_TRAIN / (ms / 1000.0),
+    return {"metric": metric or "gigapixel-image training samples/s (config 3, one GPU)",
+            "value": B_TRAIN / (ms / 1000.0),
             "unit": "samples/s", "ms_per_step": ms, "params": n, "steps": steps, "warmup": warmup,
             "phases_ms_per_step": {"train_kernel": prof[0] / steps, "adam": prof[1] / steps},
-            "config": f"2D hash L16 F2 T2^{T_log2} Nmin16 Nmax8192, MLP 32-64-64-3 sigmoid, L2, batch 2^18 random "
-                      "points of the procedural image (helpers.hpp:99-125) evaluated on the fly"}
+            "config": config or (f"2D hash L16 F2 T2^{T_log2} Nmin16 Nmax{n_max}, MLP 32-64-64-3 sigmoid, L2, batch "
+                                 f"2^{B_TRAIN.bit_length() - 1} random points of the procedural image "
+                                 "(helpers.hpp:99-125) evaluated on the fly")}
 
 
 def bench_nerf(nf, ctx, steps, warmup, W=128, views=16, samples=1 << 18):
@@ -607,6 +611,18 @@ def main():
         except Exception as e:
             giga_line = {"error": str(e)[:200]}
 
+    # ---- config 1: 2D image regression (the reference's CPU-runnable case) ----------
+    c1_line = None
+    if rank == 0 and not args.no_nerf:
+        try:
+            c1_line = bench_gigapixel(nf, sctx, steps=max(10, args.steps), warmup=5, T_log2=14, n_max=1024,
+                                      batch=1 << 16, metric="image training samples/s (config 1, one GPU)",
+                                      config="2D hash L16 F2 T2^14 Nmin16 Nmax1024, MLP 32-64-64-3 sigmoid, L2, "
+                                             "lr 1e-2, batch 2^16 random points of the procedural image "
+                                             "(helpers.hpp:99-125)")
+        except Exception as e:
+            c1_line = {"error": str(e)[:200]}
+
     # ---- config 4: NeRF training (occupancy-grid marching, compacted samples) ----
     nerf_line = None
     if rank == 0 and not args.no_nerf:
@@ -706,6 +722,7 @@ def main():
                               "ms_per_call": t_inf, "sweep_one_gpu": sweep},
                 "strong_scaling": strong,
                 "gigapixel": giga_line,
+                "config1": c1_line,
                 "nerf": nerf_line,
                 "phases_ms_per_step": ({"train_kernel": phase_ms[0], "adam": phase_ms[1]} if world == 1 else
                                        {"train_kernel": phase_ms[0],
