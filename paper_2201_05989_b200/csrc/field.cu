@@ -1460,6 +1460,10 @@ static void host_train_step(nfg_field* f, const float* X, const float* target, i
     const bool staging_idle = c->staging_idle;
     c->staging_idle = false;
     f->early_result = true;   // read the result while Adam (and a data-parallel exchange) runs
+    struct EarlyReset {       // no other entry point may see it set (an exception leaves through here)
+        nfg_field* f;
+        ~EarlyReset() { f->early_result = false; }
+    } early_reset{ f };
     const bool can_stream = f->stream_warm && f->grads_clean && f->opts.fused_train && !f->opts.deterministic &&
                             c->write_value32 && B >= (int64_t(1) << 15) && !launches_serialized();
     const bool pinned = can_stream && is_pinned(X) && is_pinned(target);
