@@ -189,6 +189,8 @@ __global__ void __launch_bounds__(256) k_validate(const float* __restrict__ X, i
 // that did not apply since the host last read the results (k_adam).
 __global__ void k_step_begin(double* loss_sum, unsigned int* flags, float* dy_max, unsigned int* sticky, int inherit)
 {
+    asm volatile("griddepcontrol.launch_dependents;");   // the next step's fused kernel may get scheduled
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // Adam has read the flags
     if (!inherit) {   // the host has read every earlier result
         sticky[0] = sticky[1] = sticky[2] = sticky[3] = 0u;
     } else if (sticky[0] == 0u && flags[1] != 0u) {
@@ -209,8 +211,7 @@ __global__ void k_step_begin(double* loss_sum, unsigned int* flags, float* dy_ma
 cudaError_t launch_step_begin(double* loss_sum, unsigned int* flags, float* dy_max, unsigned int* sticky, int inherit,
                               cudaStream_t st)
 {
-    k_step_begin<<<1, 1, 0, st>>>(loss_sum, flags, dy_max, sticky, inherit);
-    return cudaGetLastError();
+    return launch_pdl(k_step_begin, dim3(1), dim3(1), 0, st, loss_sum, flags, dy_max, sticky, inherit);
 }
 
 cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cudaStream_t st)
@@ -229,6 +230,7 @@ __global__ void __launch_bounds__(256) k_adam_check(const AdamArgs a, int force)
 {
     // programmatic dependent launch (launch_adam): the producer's gradients are
     // complete and visible past this point (a no-op for ordinary launches)
+    asm volatile("griddepcontrol.launch_dependents;");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint64_t nn = a.n_tab + a.n_w + a.n_b;
     if (a.restore_on_invalid && (a.flags[3] & 3u) != 0u) {
@@ -327,6 +329,7 @@ __device__ __forceinline__ void adam_quad(const AdamArgs& a, uint64_t i0, float4
 #endif
 __global__ void __launch_bounds__(256) k_adam(const AdamArgs a)
 {
+    asm volatile("griddepcontrol.launch_dependents;");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (a.flags[1] != 0u) {   // non-finite gradient: state untouched (the reference throws first)
         // every Adam step that does not apply (the aborting one and those standing
@@ -453,39 +456,20 @@ cudaError_t launch_adam_fallback(const AdamArgs& a, int num_sms, cudaStream_t st
     return cudaGetLastError();
 }
 
-// Launches with programmatic stream serialization: the grid may be scheduled
-// while its predecessor drains (the fused kernel's tail), and waits in
-// griddepcontrol.wait for its completion before touching the gradients.
-template <class K, class... Args>
-static cudaError_t launch_pdl(K kernel, int grid, int block, cudaStream_t st, Args... args)
+bool pdl_enabled()
 {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(grid));
-    cfg.blockDim = dim3(unsigned(block));
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kernel, args...);
+    static const bool on = !getenv("NFG_NO_PDL");
+    return on;
 }
 
 cudaError_t launch_adam(const AdamArgs& a, bool force_check, int num_sms, cudaStream_t st)
 {
     const uint64_t n = a.n_tab + a.n_w + a.n_b;
     const int blocks = int(std::min<uint64_t>((n / 4 + 255) / 256 + 1, uint64_t(num_sms) * 8));
-    static const bool pdl = !getenv("NFG_NO_PDL");
-    if (pdl) {
-        cudaError_t e = launch_pdl(k_adam_check, num_sms * 4, 256, st, a, force_check ? 1 : 0);
-        if (e == cudaSuccess)
-            e = launch_pdl(k_adam, blocks, 256, st, a);
-        return e;
-    }
-    k_adam_check<<<num_sms * 4, 256, 0, st>>>(a, force_check ? 1 : 0);
-    k_adam<<<blocks, 256, 0, st>>>(a);
-    return cudaGetLastError();
+    cudaError_t e = launch_pdl(k_adam_check, dim3(num_sms * 4), dim3(256), 0, st, a, force_check ? 1 : 0);
+    if (e == cudaSuccess)
+        e = launch_pdl(k_adam, dim3(blocks), dim3(256), 0, st, a);
+    return e;
 }
 
 __global__ void k_shadow(const float* __restrict__ p, __half* __restrict__ s, uint64_t n)

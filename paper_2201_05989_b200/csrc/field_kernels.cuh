@@ -355,11 +355,15 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
 #else
     constexpr bool LPG = SRC == SRC_ENCODE && F == 2, LPS = SINK == SINK_SCATTER && F == 2;
 #endif
+    // programmatic dependent launch: this grid may have been scheduled while
+    // the previous kernel (the step's scratch reset, behind Adam) drained;
+    // wait for it before reading the scratch, weights and tables. The
+    // optimizer launched behind this kernel may in turn get scheduled as CTAs
+    // retire; it waits for this grid's completion.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
     if (a.scratch.flags[3] != 0u)
         return;   // invalid input (k_validate): the reference throws before any update
-    // the optimizer launched behind this kernel (programmatic dependent launch)
-    // may get scheduled as CTAs retire; it waits for this grid's completion
-    asm volatile("griddepcontrol.launch_dependents;");
     const MlpShape msh{ s.in_real, s.n_out, s.sigmoid, s.hidden_width };
     load_weights<IN_STEPS, NH>(ws, bs, a.W, a.b, msh);
     if (SRC == SRC_ENCODE)

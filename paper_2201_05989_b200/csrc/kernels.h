@@ -132,6 +132,29 @@ cudaError_t launch_encode_bwd_det(const FieldShape& s, const LevelDev* lv, const
 cudaError_t launch_reduce_partials(const float* part, int nparts, int64_t n, float* out, const double* part_loss,
                                    int nloss, double* loss_sum, const unsigned int* flags, cudaStream_t st);
 int train_warps_per_cta();
+// Programmatic dependent launch (NFG_NO_PDL=1 disables it): the step's kernels
+// are launched so the next grid is scheduled while its predecessor drains and
+// waits in griddepcontrol.wait for the predecessor's completion.
+bool pdl_enabled();
+template <class K, class... Args>
+cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args)
+{
+    if (!pdl_enabled()) {
+        kernel<<<grid, block, smem, st>>>(args...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 // Records the template instantiation a launch helper just launched (which: 0 =
 // train, 1 = infer), so tests can assert that the benchmarked variant is the
 // one they checked (nfg_last_kernel_variant).

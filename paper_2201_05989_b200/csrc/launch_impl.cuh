@@ -91,8 +91,7 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
     const int grid = int(std::min<int64_t>((ntiles + NG - 1) / NG, int64_t(num_sms) * per_sm));
     if (grid_used)
         *grid_used = grid * NG;
-    k<<<grid, threads, SM::BYTES, st>>>(a, s, lv);
-    return cudaGetLastError();
+    return launch_pdl(k, dim3(grid), dim3(threads), SM::BYTES, st, a, s, lv);
 }
 
 // Warp-specialised variant (train_ws.cuh): producers gather, consumers run the
