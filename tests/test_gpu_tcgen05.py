@@ -188,3 +188,42 @@ def test_train_dw_running_scale_rescales():   # the TMEM accumulators' dz scale 
     assert np.linalg.norm(g0[:t] - g1[:t]) <= 1e-4 * np.linalg.norm(g0[:t])
     for a_, r_ in ((g1[t:t + w], g0[t:t + w]), (g1[t + w:], g0[t + w:])):
         assert np.linalg.norm(a_ - r_) <= 1e-3 * np.linalg.norm(r_)
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("F,levels,dims", [(1, 32, 2), (4, 8, 3), (8, 4, 3)])
+def test_train_dw_engines_agree_other_feature_counts(F, levels, dims, fp32):
+    """The fused training kernels for F = 1, 4, 8 (no lane pairs; with fp16
+    tables F = 4 takes the aliased gather staging in the tcgen05 kernel's
+    canonical buffers): tcgen05 vs mma.sync dW, loss vs the oracle."""
+    from paper_2201_05989_b200 import nf
+    g = _grid(nf, dims=dims, levels=levels, table_size=1 << 14, features=F, n_min=4, n_max=256)
+    ms = []
+    for eng in (SYNC, TC):
+        m = nf.FieldModel(options=nf.Options(mlp_engine=eng, table_fp32=fp32))
+        m.hash_cfg = g
+        m.mlp_cfg = nf.MlpConfig(hidden_layers=2, hidden_width=64, output_width=1)
+        m.hyper = nf.AdamHyper(lr=1e-3)
+        m.init(9)
+        ms.append(m)
+    f = _oracle_field(ms[0], lr=1e-3, seed=9)
+    B = 100000
+    X = _points(B, dims, seed=13)
+    T = O.csg_sdf(X if dims == 3 else np.c_[X, X[:, :1]]).reshape(-1, 1).astype(np.float32)
+    out = []
+    for m, eng in zip(ms, ("mma.sync", "tcgen05")):
+        loss = m.gradients(X, T, nf.LossKind.Mape)
+        assert f"dw={eng}" in m.last_kernel_variant(0), m.last_kernel_variant(0)
+        out.append((loss, m.grads))
+    (l0, g0), (l1, g1) = out
+    t, w, b = ms[0].sizes
+    P = ms[0].params
+    if not fp32:
+        P[:t] = P[:t].astype(np.float16).astype(np.float32)
+    f.params[:] = P
+    lo = f.train_step(X, T, O.LOSS_MAPE, 1)   # the oracle's loss on the same parameters
+    assert abs(l0 - lo) <= 1e-3 * abs(lo) and abs(l1 - lo) <= 1e-3 * abs(lo), (l0, l1, lo)
+    assert np.array_equal(g0[:t] != 0, g1[:t] != 0)
+    assert np.linalg.norm(g0[:t] - g1[:t]) <= 1e-4 * np.linalg.norm(g0[:t])
+    for a_, r_ in ((g1[t:t + w], g0[t:t + w]), (g1[t + w:], g0[t + w:])):
+        assert np.linalg.norm(a_ - r_) <= 1e-3 * np.linalg.norm(r_)
