@@ -304,6 +304,7 @@ def bench_nerf(nf, ctx, steps, warmup, W=128, views=16, samples=1 << 18):
         tot_s += ns
         tot_r += nr
         tot_b += nerf.last_backward_samples
+    nerf.sync()   # the last step's deferred Adam belongs in the region
     ctx.synchronize()
     dt = time.perf_counter() - t0
     nerf.close()

@@ -401,6 +401,10 @@ nfg_status nfg_nerf_train_step(nfg_nerf* n, int64_t step, float* loss, int64_t* 
 nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t* rays_used, int64_t* samples_used,
                                 int64_t* samples_backward);
 nfg_status nfg_nerf_update_occupancy(nfg_nerf* n, int64_t step);
+/* Completes the work a training step defers (its networks' Adam step runs at the
+ * start of the next call; every entry point that uses the networks applies it
+ * first) and synchronises the NeRF's stream. */
+nfg_status nfg_nerf_sync(nfg_nerf* n);
 nfg_status nfg_nerf_render(nfg_nerf* n, const float* cam12, int32_t width, int32_t height, float focal, float* rgb);
 nfg_status nfg_nerf_occupancy(nfg_nerf* n, uint8_t* bits, float* density);   /* 128^3/8 bytes, 128^3 floats */
 nfg_status nfg_nerf_set_occupancy(nfg_nerf* n, const uint8_t* bits);

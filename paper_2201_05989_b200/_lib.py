@@ -158,6 +158,7 @@ SIGNATURES = {
     "nfg_nerf_train_step": (C.c_int, [_vp, C.c_int64, _fp, _i64p, _i64p]),
     "nfg_nerf_train_step2": (C.c_int, [_vp, C.c_int64, _fp, _i64p, _i64p, _i64p]),
     "nfg_nerf_update_occupancy": (C.c_int, [_vp, C.c_int64]),
+    "nfg_nerf_sync": (C.c_int, [_vp]),
     "nfg_nerf_render": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_float, _vp]),
     "nfg_nerf_occupancy": (C.c_int, [_vp, _vp, _vp]),
     "nfg_nerf_set_occupancy": (C.c_int, [_vp, _vp]),

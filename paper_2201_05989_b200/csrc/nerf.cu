@@ -654,6 +654,20 @@ struct nfg_nerf {
     float focal = 1.0f;
     int64_t n_rays = 1 << 13;   // adapted to the sample budget
     double last_used_frac = 1.0;   // samples before the transmittance stop / marched (previous step)
+    // The networks' Adam step of a training step is deferred to the next call:
+    // the next step enqueues it behind its ray marching (which only reads the
+    // occupancy grid) and ahead of the host sync for the sample count, so the
+    // GPU runs Adam while the host waits; every other entry point that uses
+    // the networks flushes it first.
+    bool adam_pending = false;
+    void flush_adam()
+    {
+        if (!adam_pending)
+            return;
+        adam_pending = false;
+        ok(nfg_adam_step_device(color, float(cfg.lr)));
+        ok(nfg_adam_step_device(density, float(cfg.lr)));
+    }
     uint32_t* h_used = nullptr;    // pinned
     Buf occ_grid, occ_bits, cams, images;
     Buf rays, target, views, pixels, counts, offsets, fit, scan_tmp, pos, dirs, dens, Yc, rgb, color_out, d_rgb, d_raw,
@@ -673,7 +687,8 @@ struct nfg_nerf {
     }
 
     // march + compact a ray set; returns (rays kept, samples)
-    std::pair<int64_t, int64_t> march_compact(const float* ray_buf, int64_t R, int64_t budget)
+    std::pair<int64_t, int64_t> march_compact(const float* ray_buf, int64_t R, int64_t budget,
+                                              bool flush_before_sync = false)
     {
         uint32_t* cnt = counts.as<uint32_t>(size_t(R));
         uint32_t* off = offsets.as<uint32_t>(size_t(R));
@@ -687,6 +702,8 @@ struct nfg_nerf {
         k_fit_budget<<<1, 1, 0, st>>>(off, cnt, R, budget, f);
         int64_t h_fit[2] = { 0, 0 };
         NFG_HC_CUDA(cudaMemcpyAsync(h_fit, f, sizeof(h_fit), cudaMemcpyDeviceToHost, st));
+        if (flush_before_sync)
+            flush_adam();   // runs on the GPU while the host waits for the counts
         NFG_HC_CUDA(cudaStreamSynchronize(st));
         const int64_t ns = h_fit[1];
         float* P = pos.as<float>(size_t(std::max<int64_t>(ns, 1)) * 3);
@@ -810,6 +827,7 @@ nfg_status nfg_nerf_destroy(nfg_nerf* n)
 nfg_status nfg_nerf_fields(nfg_nerf* n, nfg_field** density, nfg_field** color)
 {
     return run([&] {
+        n->flush_adam();   // the caller sees the trained parameters
         if (density)
             *density = n->density;
         if (color)
@@ -847,8 +865,10 @@ nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t*
         if (n->n_views == 0)
             throw std::invalid_argument("nerf: no dataset");
         cudaStream_t st = n->st;
-        if (step % 16 == 0)
+        if (step % 16 == 0) {
+            n->flush_adam();   // the occupancy update evaluates the density network
             n->update_occupancy(step);
+        }
         const int64_t R = n->n_rays;
         uint32_t* vw = n->views.as<uint32_t>(size_t(R));
         uint32_t* px = n->pixels.as<uint32_t>(size_t(R));
@@ -860,7 +880,7 @@ nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t*
                                                   static_cast<const float*>(n->images.p), n->w, n->h, n->focal, rays,
                                                   tgt);
         NFG_HC_CUDA(cudaGetLastError());
-        const auto fit = n->march_compact(rays, R, n->cfg.target_samples);
+        const auto fit = n->march_compact(rays, R, n->cfg.target_samples, /*flush_before_sync=*/true);
         const int64_t nr = fit.first, ns = fit.second;
         // adapt the ray count to the sample budget (measured samples per ray)
         const double spr = nr > 0 ? std::max(1.0, double(ns) / double(nr)) : 1.0;
@@ -931,8 +951,7 @@ nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t*
                 NFG_HC_CUDA(cudaGetLastError());
                 ok(nfg_field_backward_device(n->density, bpos, nu, dd));
             }
-            ok(nfg_adam_step_device(n->color, float(n->cfg.lr)));
-            ok(nfg_adam_step_device(n->density, float(n->cfg.lr)));
+            n->adam_pending = true;   // enqueued by the next call (flush_adam)
         }
         double h = 0.0;
         NFG_HC_CUDA(cudaMemcpyAsync(&h, ls, 8, cudaMemcpyDeviceToHost, st));
@@ -951,9 +970,20 @@ nfg_status nfg_nerf_train_step2(nfg_nerf* n, int64_t step, float* loss, int64_t*
     });
 }
 
+nfg_status nfg_nerf_sync(nfg_nerf* n)
+{
+    return run([&] {
+        n->flush_adam();
+        NFG_HC_CUDA(cudaStreamSynchronize(n->st));
+        ok(nfg_field_check(n->color));
+        ok(nfg_field_check(n->density));
+    });
+}
+
 nfg_status nfg_nerf_update_occupancy(nfg_nerf* n, int64_t step)
 {
     return run([&] {
+        n->flush_adam();
         n->update_occupancy(step);
         NFG_HC_CUDA(cudaStreamSynchronize(n->st));
     });
@@ -963,6 +993,7 @@ nfg_status nfg_nerf_render(nfg_nerf* n, const float* cam12, int32_t width, int32
                            float* rgb_host)
 {
     return run([&] {
+        n->flush_adam();
         cudaStream_t st = n->st;
         const int64_t R = int64_t(width) * height;
         Buf cam, rays, color;

@@ -878,6 +878,10 @@ class NeRF:
         L.check(self.lib.nfg_nerf_render(self.h, _ptr(cam), width, height, focal, _ptr(out)))
         return out
 
+    def sync(self) -> None:
+        """Apply the Adam step the last train_step deferred and wait for the GPU."""
+        L.check(self.lib.nfg_nerf_sync(self.h))
+
     def occupancy(self):
         bits = np.empty(OCC_RES ** 3 // 8, np.uint8)
         dens = np.empty(OCC_RES ** 3, np.float32)
