@@ -689,12 +689,13 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             isc = ldexpf(1.0f, -k);
         }
         if constexpr (TCW) {
-            // one scale per CTA accumulator: the running minimum of the tile
-            // scales (scaled maxima stay < 16); a smaller tile scale rescales
-            // the TMEM accumulators by the exact power-of-two ratio
+            // the TMEM accumulators hold dz^T act at the scale of the tile last
+            // added; a tile with another power-of-two scale first rescales them
+            // by the exact ratio (fp32, in place), so every tile's fp16 dz
+            // operands use the tile's own scale (as the mma.sync reduction)
             if (kscale == 0.0f) {
                 kscale = sc;
-            } else if (sc < kscale) {
+            } else if (sc != kscale) {
                 if (pending) {
                     tc::mbar_wait(mbar, mphase);
                     mphase ^= 1u;
@@ -715,8 +716,6 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 tc::wait_st();
                 kscale = sc;
             }
-            sc = kscale;
-            isc = 1.0f / kscale;
         }
 
         // ---- MLP backward ---------------------------------------------------

@@ -308,7 +308,7 @@ k_train_ws(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ l
             }
             if (kscale == 0.0f) {
                 kscale = sc;
-            } else if (sc < kscale) {   // rescale the TMEM accumulators (exact power of two)
+            } else if (sc != kscale) {   // rescale the TMEM accumulators to this tile's scale (exact power of two)
                 if (pending) {
                     tc::mbar_wait(dw_bar, mphase);
                     mphase ^= 1u;
@@ -329,8 +329,7 @@ k_train_ws(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ l
                 tc::wait_st();
                 kscale = sc;
             }
-            sc = kscale;
-            const float isc = 1.0f / kscale;
+            const float isc = 1.0f / sc;
 
             // ---- MLP backward -----------------------------------------------
 #pragma unroll
