@@ -434,8 +434,8 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     bool bad = false;
     unsigned int invalid = 0u;
     double loss_acc = 0.0;   // deterministic mode (lane 0 of each warp)
-    // TCW: dz scale of the TMEM accumulators (power of two; the running minimum
-    // of the tiles' own scales — a smaller one rescales the accumulators), the
+    // TCW: dz scale of the TMEM accumulators (power of two: the scale of the
+    // tile last added; a tile with another scale rescales them first), the
     // pending dW commit, the output bias gradient (lanes g == 0)
     float kscale = 0.0f;
     bool pending = false, first_mma = true;

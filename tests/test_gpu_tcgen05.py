@@ -112,7 +112,7 @@ def test_tc_engine_empty_batch():
 @pytest.mark.parametrize("case", ["config2", "config1"])
 def test_train_dw_engines_agree(case, det):   # model.cpp:111-138, dW on tcgen05 vs mma.sync
     """The fused step's dW / db reductions on tcgen05 (TMEM accumulators over
-    all tiles of a CTA, a running power-of-two dz scale) against the mma.sync
+    all tiles of a CTA, rescaled to each tile's power-of-two dz scale) against the mma.sync
     reductions (register accumulators, per-tile scale): same fp16 operands, fp32
     accumulation in a different order; the bias gradients of the output layer
     come from the same fp16 dz in both."""
@@ -162,7 +162,7 @@ def test_train_dw_engines_agree(case, det):   # model.cpp:111-138, dW on tcgen05
 
 def test_train_dw_running_scale_rescales():   # the TMEM accumulators' dz scale decreasing tile by tile
     """Targets that grow along the sample order make every later tile of a
-    CTA need a smaller power-of-two dz scale than the one its accumulators
+    CTA need another power-of-two dz scale than the one its accumulators
     hold, so the tcgen05 path rescales TMEM on (almost) every tile; the
     result must still match the mma.sync path's per-tile-scaled reduction."""
     from paper_2201_05989_b200 import nf
