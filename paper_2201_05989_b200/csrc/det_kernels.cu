@@ -17,6 +17,8 @@
 // reproducible. The MLP gradients and the loss sum of the deterministic path
 // are reduced from per-CTA partials in CTA order (k_reduce_partials) instead of
 // by float atomics.
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "encode.cuh"
@@ -45,6 +47,149 @@ k_det_keys(const GridDev g, LevelDev lv, const float* __restrict__ X, int64_t B,
         keys[p * NC + c] = cs.row(c);
         vals[p * NC + c] = uint32_t(p * NC + c);
     }
+}
+
+// F == 2: the payload is the contribution itself, w * dy for both features
+// (the reference's product, rounded once, no FMA), packed in 64 bits; the
+// stable sort keeps equal rows in (p, c) order and the run sum then reads its
+// contributions contiguously instead of recomputing corners per element.
+template <int D>
+__global__ void __launch_bounds__(256)
+k_det_keys_contrib(const GridDev g, LevelDev lv, int l, const float* __restrict__ X, int64_t B,
+                   const float* __restrict__ dY, uint32_t* __restrict__ keys, unsigned long long* __restrict__ vals,
+                   const unsigned int* flags)
+{
+    if (flags && flags[3] != 0u)
+        return;
+    const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= B)
+        return;
+    float x[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        x[i] = X[p * D + i];
+    const CornerSet<D> cs = corners_of<D>(g, lv, x);
+    const int LF = g.L * 2;
+    const float dy0 = dY[p * LF + l * 2], dy1 = dY[p * LF + l * 2 + 1];
+    constexpr int NC = 1 << D;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const float w = cs.weight(c);
+        keys[p * NC + c] = cs.row(c);
+        vals[p * NC + c] = (static_cast<unsigned long long>(__float_as_uint(__fmul_rn(w, dy1))) << 32) |
+                           __float_as_uint(__fmul_rn(w, dy0));
+    }
+}
+
+// All levels in one pass (F == 2): entry (l, p, c) at (l * B + p) * 2^d + c,
+// key = (l << lb) | row — one stable sort then orders every level's rows and
+// keeps each row's contributions in (p, c) order.
+template <int D>
+__global__ void __launch_bounds__(256)
+k_det_keys_all(const GridDev g, int lb, const float* __restrict__ X, int64_t B, const float* __restrict__ dY,
+               uint32_t* __restrict__ keys, unsigned long long* __restrict__ vals, const unsigned int* flags)
+{
+    if (flags && flags[3] != 0u)
+        return;
+    const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= B)
+        return;
+    float x[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        x[i] = X[p * D + i];
+    const int LF = g.L * 2;
+    constexpr int NC = 1 << D;
+    for (int l = 0; l < g.L; ++l) {
+        const CornerSet<D> cs = corners_of<D>(g, g.lv[l], x);
+        const float dy0 = dY[p * LF + l * 2], dy1 = dY[p * LF + l * 2 + 1];
+        const int64_t e0 = (int64_t(l) * B + p) * NC;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const float w = cs.weight(c);
+            keys[e0 + c] = (uint32_t(l) << lb) | cs.row(c);
+            vals[e0 + c] = (static_cast<unsigned long long>(__float_as_uint(__fmul_rn(w, dy1))) << 32) |
+                           __float_as_uint(__fmul_rn(w, dy0));
+        }
+    }
+}
+
+// Run sums over the all-level sort: the level comes from the key's top bits.
+__global__ void __launch_bounds__(256)
+k_det_segsum_all(const GridDev g, int lb, int64_t n, const uint32_t* __restrict__ keys,
+                 const unsigned long long* __restrict__ vals, float* __restrict__ grads, const unsigned int* flags)
+{
+    if (flags && flags[3] != 0u)
+        return;
+    const int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i0 >= n)
+        return;
+    const uint32_t key = keys[i0];
+    if (i0 > 0 && keys[i0 - 1] == key)
+        return;   // not the head of its run
+    int64_t end = i0 + 1;
+    while (end < n && keys[end] == key)
+        ++end;
+    const uint32_t l = key >> lb, row = key & ((1u << lb) - 1u);
+    float2* dst = reinterpret_cast<float2*>(grads + (size_t(g.lv[l].row_off) + row) * 2);
+    float2 acc = *dst;
+    int64_t i = i0;
+    for (; i + 8 <= end; i += 8) {
+        unsigned long long v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            v[k] = vals[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            acc.x = __fadd_rn(acc.x, __uint_as_float(uint32_t(v[k])));
+            acc.y = __fadd_rn(acc.y, __uint_as_float(uint32_t(v[k] >> 32)));
+        }
+    }
+    for (; i < end; ++i) {
+        const unsigned long long v = vals[i];
+        acc.x = __fadd_rn(acc.x, __uint_as_float(uint32_t(v)));
+        acc.y = __fadd_rn(acc.y, __uint_as_float(uint32_t(v >> 32)));
+    }
+    *dst = acc;
+}
+
+// One thread per run of equal rows adds the run's contributions in order
+// (round-to-nearest, the reference's sequence); loads are issued 8 ahead.
+__global__ void __launch_bounds__(256)
+k_det_segsum_contrib(LevelDev lv, int64_t n, const uint32_t* __restrict__ keys,
+                     const unsigned long long* __restrict__ vals, float* __restrict__ grads, const unsigned int* flags)
+{
+    if (flags && flags[3] != 0u)
+        return;
+    const int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i0 >= n)
+        return;
+    const uint32_t row = keys[i0];
+    if (i0 > 0 && keys[i0 - 1] == row)
+        return;   // not the head of its run
+    int64_t end = i0 + 1;
+    while (end < n && keys[end] == row)
+        ++end;
+    float2* dst = reinterpret_cast<float2*>(grads + (size_t(lv.row_off) + row) * 2);
+    float2 acc = *dst;
+    int64_t i = i0;
+    for (; i + 8 <= end; i += 8) {
+        unsigned long long v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            v[k] = vals[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            acc.x = __fadd_rn(acc.x, __uint_as_float(uint32_t(v[k])));
+            acc.y = __fadd_rn(acc.y, __uint_as_float(uint32_t(v[k] >> 32)));
+        }
+    }
+    for (; i < end; ++i) {
+        const unsigned long long v = vals[i];
+        acc.x = __fadd_rn(acc.x, __uint_as_float(uint32_t(v)));
+        acc.y = __fadd_rn(acc.y, __uint_as_float(uint32_t(v >> 32)));
+    }
+    *dst = acc;
 }
 
 template <int D, int F>
@@ -118,14 +263,18 @@ static int bits_for(uint64_t n)
     return b;
 }
 
-size_t encode_bwd_det_scratch(int64_t B, int d)
+size_t encode_bwd_det_scratch(int64_t B, int d, int L)
 {
-    const size_t n = size_t(B) << d;
-    size_t cub_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, static_cast<const uint32_t*>(nullptr),
+    const size_t n = (size_t(B) << d) * size_t(L);   // all levels (F == 2); a per-level sort needs less
+    size_t cub32 = 0, cub64 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, cub32, static_cast<const uint32_t*>(nullptr),
                                     static_cast<uint32_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
                                     static_cast<uint32_t*>(nullptr), n, 0, 32);
-    return 4 * n * sizeof(uint32_t) + ((cub_bytes + 255) & ~size_t(255));
+    cub::DeviceRadixSort::SortPairs(nullptr, cub64, static_cast<const uint32_t*>(nullptr),
+                                    static_cast<uint32_t*>(nullptr), static_cast<const unsigned long long*>(nullptr),
+                                    static_cast<unsigned long long*>(nullptr), n, 0, 32);
+    // keys x 2 + 64-bit payloads x 2 (the F != 2 path uses 32-bit payloads in the same space)
+    return 6 * n * sizeof(uint32_t) + ((std::max(cub32, cub64) + 255) & ~size_t(255));
 }
 
 template <int D, int F>
@@ -134,13 +283,52 @@ static cudaError_t enc_bwd_det(const FieldShape& s, const LevelDev* lv, const fl
 {
     (void)lv;
     const size_t n = size_t(B) << D;
+    const unsigned blocks_p = unsigned((B + 255) / 256), blocks_n = unsigned((n + 255) / 256);
+    if constexpr (F == 2) {
+        // one sort over every level: key = (level << lb) | row
+        int lb = 1;
+        for (int l = 0; l < s.grid.L; ++l)
+            lb = std::max(lb, bits_for(s.grid.lv[l].len));
+        const int kb = lb + bits_for(uint64_t(s.grid.L));
+        const size_t na = n * size_t(s.grid.L);
+        if (kb <= 32 && na < (size_t(1) << 31)) {
+            uint32_t* k0 = static_cast<uint32_t*>(scratch);
+            uint32_t* k1 = k0 + na;
+            unsigned long long* v0 = reinterpret_cast<unsigned long long*>(k1 + na);   // 8-byte aligned: na even
+            unsigned long long* v1 = v0 + na;
+            void* tmp = v1 + na;
+            size_t tmp_bytes = bytes - 6 * na * sizeof(uint32_t);
+            k_det_keys_all<D><<<blocks_p, 256, 0, st>>>(s.grid, lb, X, B, dY, k0, v0, flags);
+            cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, v1, na, 0, kb, st);
+            if (e != cudaSuccess)
+                return e;
+            k_det_segsum_all<<<unsigned((na + 255) / 256), 256, 0, st>>>(s.grid, lb, int64_t(na), k1, v1, grads,
+                                                                          flags);
+            return cudaGetLastError();
+        }
+        uint32_t* k0 = static_cast<uint32_t*>(scratch);
+        uint32_t* k1 = k0 + n;
+        unsigned long long* v0 = reinterpret_cast<unsigned long long*>(k1 + n);   // 8-byte aligned: n even
+        unsigned long long* v1 = v0 + n;
+        void* tmp = v1 + n;
+        size_t tmp_bytes = bytes - 6 * n * sizeof(uint32_t);
+        for (int l = 0; l < s.grid.L; ++l) {
+            const LevelDev L = s.grid.lv[l];
+            k_det_keys_contrib<D><<<blocks_p, 256, 0, st>>>(s.grid, L, l, X, B, dY, k0, v0, flags);
+            cudaError_t e =
+                cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, v1, n, 0, bits_for(L.len), st);
+            if (e != cudaSuccess)
+                return e;
+            k_det_segsum_contrib<<<blocks_n, 256, 0, st>>>(L, int64_t(n), k1, v1, grads, flags);
+        }
+        return cudaGetLastError();
+    }
     uint32_t* k0 = static_cast<uint32_t*>(scratch);
     uint32_t* v0 = k0 + n;
     uint32_t* k1 = v0 + n;
     uint32_t* v1 = k1 + n;
     void* tmp = v1 + n;
     size_t tmp_bytes = bytes - 4 * n * sizeof(uint32_t);
-    const unsigned blocks_p = unsigned((B + 255) / 256), blocks_n = unsigned((n + 255) / 256);
     for (int l = 0; l < s.grid.L; ++l) {
         const LevelDev L = s.grid.lv[l];
         k_det_keys<D><<<blocks_p, 256, 0, st>>>(s.grid, L, X, B, k0, v0, flags);
@@ -160,7 +348,7 @@ cudaError_t launch_encode_bwd_det(const FieldShape& s, const LevelDev* lv, const
         return cudaSuccess;
     if ((uint64_t(B) << s.grid.d) > (uint64_t(1) << 31))
         return cudaErrorInvalidValue;
-    if (bytes < encode_bwd_det_scratch(B, s.grid.d))
+    if (bytes < encode_bwd_det_scratch(B, s.grid.d, s.grid.L))
         return cudaErrorInvalidValue;
 #define NFG_DET_B(D_, F_)                                                                                   \
     if (s.grid.d == D_ && s.grid.F == F_)                                                                    \

@@ -625,7 +625,7 @@ void det_finish(nfg_field* f, const nfg::TrainArgs& a, int grid)
 void det_encode_bwd(nfg_field* f, const float* X, int64_t B, const float* dY)
 {
     nfg_ctx* c = f->ctx;
-    const size_t bytes = nfg::encode_bwd_det_scratch(B, f->gcfg.dims);
+    const size_t bytes = nfg::encode_bwd_det_scratch(B, f->gcfg.dims, f->gcfg.levels);
     void* scratch = f->det_sort.get(std::max<size_t>(bytes, 16));
     NFG_CUDA(nfg::launch_encode_bwd_det(f->shape, f->d_levels, X, B, dY, f->d_g, f->d_res->flags, scratch, bytes,
                                         c->stream));

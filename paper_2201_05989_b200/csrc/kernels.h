@@ -125,7 +125,7 @@ cudaError_t launch_validate(const float* X, int64_t n, unsigned int* flags, cuda
 cudaError_t launch_step_begin(double* loss_sum, unsigned int* flags, float* dy_max, unsigned int* sticky, int inherit,
                               cudaStream_t st);
 cudaError_t launch_shadow(const float* p, __half* shadow, uint64_t n, cudaStream_t st);
-size_t encode_bwd_det_scratch(int64_t B, int d);
+size_t encode_bwd_det_scratch(int64_t B, int d, int L);
 cudaError_t launch_encode_bwd_det(const FieldShape& s, const LevelDev* lv, const float* X, int64_t B,
                                   const float* dY, float* grads, const unsigned int* flags, void* scratch,
                                   size_t bytes, cudaStream_t st);
