@@ -367,9 +367,20 @@ def cpu_reference(steps, warmup, seconds_cap, native=True, batch=B_TRAIN):
     for c0 in range(0, 1 << 20, 1 << 16):
         f.evaluate(Q[c0:c0 + (1 << 16)])
     qps = (1 << 20) / (time.perf_counter() - t1)
+    # one thread (the reference's deterministic single-thread mode, acceptance.cpp:675;
+    # SURVEY §8d): two steps, capped at a few seconds
+    lib = O.lib(native)
+    lib.orc_set_threads(1)
+    t2 = time.perf_counter()
+    one = 0
+    while one < 2 and time.perf_counter() - t2 < 8.0:
+        f.train_step(X, T, O.LOSS_MAPE, warmup + done + one + 1)
+        one += 1
+    v1 = one * batch / (time.perf_counter() - t2)
+    lib.orc_set_threads(threads)
     return {"value": done * batch / dt, "steps": done, "seconds": dt, "threads": threads,
             "phases_s_per_step": {k: v / done for k, v in f.phase_times().items()}, "native": native,
-            "inference_queries_per_s": qps}
+            "inference_queries_per_s": qps, "value_1_thread": v1}
 
 
 def run_reference(args, rank, world):
@@ -387,7 +398,8 @@ def run_reference(args, rank, world):
             "config": {"workload": WORKLOAD, "global_batch": B_TRAIN, "parallelism": "cpu"},
             "cpu_baseline": {"value": r["value"], "unit": "samples/s", "cores": r["threads"], "kind": "port",
                              "sample": sample, "phases_s_per_step": r["phases_s_per_step"],
-                             "inference_queries_per_s": r["inference_queries_per_s"]},
+                             "inference_queries_per_s": r["inference_queries_per_s"],
+                             "value_1_thread": r["value_1_thread"]},
             "e2e": {"value": r["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -703,7 +715,7 @@ def main():
                "sample": f"config2 at batch 2^16 (a quarter of the 2^18 workload), {r['steps']} steps in "
                          f"{r['seconds']:.1f} s, CPU restatement of the reference (-O2 -march=native, OpenMP)",
                "phases_s_per_step": r["phases_s_per_step"],
-               "inference_queries_per_s": r["inference_queries_per_s"]}
+               "inference_queries_per_s": r["inference_queries_per_s"], "value_1_thread": r["value_1_thread"]}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
