@@ -244,7 +244,8 @@ struct InferSmem {
 __device__ __forceinline__ bool sane(float v) { return fabsf(v) <= 1e30f; }   // false for NaN/inf/huge
 
 // Input fragments of the warp's 16 rows: encoded from X, or loaded from Y.
-template <int SRC, int D, int F, typename TT, int IN_STEPS>
+// PC: xg / xg8 were clamped once (clamp_x).
+template <int SRC, int D, int F, typename TT, int IN_STEPS, bool PC = false>
 __device__ __forceinline__ void input_frags(uint32_t (&afr)[IN_STEPS][4], const FieldShape& s, const LevelDev* lvs,
                                             const float* xg, const float* xg8, bool vg, bool vg8, int64_t sg,
                                             const float* __restrict__ Y, const void* table, int lane)
@@ -260,8 +261,8 @@ __device__ __forceinline__ void input_frags(uint32_t (&afr)[IN_STEPS][4], const 
                 const TT* tab = static_cast<const TT*>(table);
 #ifndef NFG_NO_LANE_PAIRS
                 if constexpr (F == 2) {   // warp-uniform: invalid samples encode x = 0, discarded
-                    e0 = encode_pair_lp<D, F, TT>(s.grid, lvs, xg, col, tab);
-                    e8 = encode_pair_lp<D, F, TT>(s.grid, lvs, xg8, col, tab);
+                    e0 = encode_pair_lp<D, F, TT, PC>(s.grid, lvs, xg, col, tab);
+                    e8 = encode_pair_lp<D, F, TT, PC>(s.grid, lvs, xg8, col, tab);
                     if (!vg)
                         e0 = make_float2(0.f, 0.f);
                     if (!vg8)
@@ -433,7 +434,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
 
     bool bad = false;
     unsigned int invalid = 0u;
-    double loss_acc = 0.0;   // deterministic mode (lane 0 of each warp)
+    double loss_acc = 0.0;   // this warp's loss sum over its tiles (lane 0)
     // TCW: dz scale of the TMEM accumulators (power of two: the scale of the
     // tile last added; a tile with another scale rescales them first), the
     // pending dW commit, the output bias gradient (lanes g == 0)
@@ -471,6 +472,9 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 invalid |= (finite_f(x8[i]) ? 0u : 1u) | ((x8[i] < lo || x8[i] > hi) ? 2u : 0u);
             }
         }
+        // clamp once per sample; every level's corners skip their own clamp
+        clamp_x<D>(x);
+        clamp_x<D>(x8);
     };
     // corner loads of one pass (SG::STS k16 steps) as cp.async copies
     auto issue_pass = [&](int s0, const auto& slots, const float* x, const float* x8, bool v, bool v8) {
@@ -482,9 +486,9 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 const int p = (sl * 2 + h) * 2;
                 if constexpr (LPG) {
                     if (s0 + sl < IN_STEPS && v)
-                        gather_issue_lp<D, F, TT>(s.grid, lvs, x, col, tab, slots, p * SG::NE);
+                        gather_issue_lp<D, F, TT, true>(s.grid, lvs, x, col, tab, slots, p * SG::NE);
                     if (s0 + sl < IN_STEPS && v8)
-                        gather_issue_lp<D, F, TT>(s.grid, lvs, x8, col, tab, slots, (p + 1) * SG::NE);
+                        gather_issue_lp<D, F, TT, true>(s.grid, lvs, x8, col, tab, slots, (p + 1) * SG::NE);
                 } else {
                     if (s0 + sl < IN_STEPS && v)
                         gather_issue<D, F, TT>(s.grid, lvs, x, col, tab, slots, p * SG::NE);
@@ -506,9 +510,9 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 float2 e0 = make_float2(0.f, 0.f), e8 = make_float2(0.f, 0.f);
                 if constexpr (LPG) {
                     if (v)
-                        e0 = gather_blend_lp<D, F, TT>(s.grid, lvs, x, col, slots, p * SG::NE);
+                        e0 = gather_blend_lp<D, F, TT, true>(s.grid, lvs, x, col, slots, p * SG::NE);
                     if (v8)
-                        e8 = gather_blend_lp<D, F, TT>(s.grid, lvs, x8, col, slots, (p + 1) * SG::NE);
+                        e8 = gather_blend_lp<D, F, TT, true>(s.grid, lvs, x8, col, slots, (p + 1) * SG::NE);
                 } else {
                     if (v)
                         e0 = gather_blend<D, F, TT>(s.grid, lvs, x, col, slots, p * SG::NE);
@@ -658,12 +662,8 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         }
         if (lane == 0) {
             red[warp] = mx;
-            if (GRAD == GRAD_LOSS) {
-                if (a.part_loss)
-                    loss_acc += double(term);
-                else
-                    atomicAdd(a.scratch.loss_sum, double(term));
-            }
+            if (GRAD == GRAD_LOSS)
+                loss_acc += double(term);   // one atomic per warp at the end, not per tile
         }
         const int64_t next_tile = tile + vgrid;
         if (SA::PREFETCH && next_tile < ntiles)
@@ -779,9 +779,9 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 const float2 p8 = make_float2(__shfl_xor_sync(0xffffffffu, d8.x, 1),
                                               __shfl_xor_sync(0xffffffffu, d8.y, 1));
                 if (vg)
-                    scatter_pair_lp<D>(s.grid, lvs, xg, col, d0, p0, a.table_grad);
+                    scatter_pair_lp<D, true>(s.grid, lvs, xg, col, d0, p0, a.table_grad);
                 if (vg8)
-                    scatter_pair_lp<D>(s.grid, lvs, xg8, col, d8, p8, a.table_grad);
+                    scatter_pair_lp<D, true>(s.grid, lvs, xg8, col, d8, p8, a.table_grad);
                 continue;
             }
             if (col >= s.in_real)
@@ -1050,8 +1050,12 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 }
     }
     }   // mma.sync dW path
-    if (GRAD == GRAD_LOSS && a.part_loss && lane == 0)
-        a.part_loss[vblk * TW + warp] = loss_acc;
+    if (GRAD == GRAD_LOSS && lane == 0) {
+        if (a.part_loss)
+            a.part_loss[vblk * TW + warp] = loss_acc;
+        else if (loss_acc != 0.0)
+            atomicAdd(a.scratch.loss_sum, loss_acc);
+    }
     if (__any_sync(0xffffffffu, bad) && lane == 0)
         atomicOr(a.scratch.flags, 1u);
     invalid = __reduce_or_sync(0xffffffffu, invalid);
@@ -1091,9 +1095,11 @@ k_infer(const InferArgs a, const FieldShape s, const LevelDev* __restrict__ leve
         if (SRC == SRC_ENCODE) {
             load_x<D>(xg, a.X, sg, vg);
             load_x<D>(xg8, a.X, sg8, vg8);
+            clamp_x<D>(xg);
+            clamp_x<D>(xg8);
         }
         uint32_t afr[IN_STEPS][4];
-        input_frags<SRC, D, F, TT, IN_STEPS>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
+        input_frags<SRC, D, F, TT, IN_STEPS, SRC == SRC_ENCODE>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
         float acc[HT][4];
         uint32_t ah[4][4];
         layer_fwd<IN_STEPS, HT>(afr, W0s, Lay::INS, acc, lane);

@@ -135,8 +135,10 @@ k_infer_tc(const InferArgs a, const FieldShape s, const LevelDev* __restrict__ l
             float xg[D], xg8[D];
             load_x<D>(xg, a.X, sg, vg);
             load_x<D>(xg8, a.X, sg8, vg8);
+            clamp_x<D>(xg);
+            clamp_x<D>(xg8);
             uint32_t afr[IN_STEPS][4];
-            input_frags<SRC, D, F, TT, IN_STEPS>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
+            input_frags<SRC, D, F, TT, IN_STEPS, true>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
 #pragma unroll
             for (int st = 0; st < IN_STEPS; ++st) {
                 const int k = 16 * st + 2 * t;

@@ -53,12 +53,15 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
 // Saturating fp16 pack for backward operands (scaled gradients): a finite
 // overflow saturates instead of becoming inf, but a NaN stays NaN, so a
 // non-finite loss gradient still reaches the gradient slab and Adam's scan
-// rejects the step like the reference (adam.hpp:86-90).
+// rejects the step like the reference (adam.hpp:86-90;
+// tests/test_gpu_parity.py::test_async_abort_is_sticky[nan_target]).
+// One F2FP.SATFINITE: cvt's .satfinite clamps +-inf and finite overflow to
+// +-65504 and keeps NaN. cvt packs its first source into the UPPER half.
 __device__ __forceinline__ uint32_t pack_sat(float a, float b)
 {
-    a = a != a ? a : fminf(fmaxf(a, -65504.0f), 65504.0f);
-    b = b != b ? b : fminf(fmaxf(b, -65504.0f), 65504.0f);
-    return pack_half2(a, b);
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
 }
 
 // ---- shared-memory weight image -----------------------------------------

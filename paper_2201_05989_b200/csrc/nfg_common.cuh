@@ -35,10 +35,16 @@ struct GridDev {
     LevelDev lv[NFG_MAX_LEVELS];
 };
 
-// Clamp, scale, optional half-voxel offset, floor (grid.hpp:199-212).
+// The clamp of grid.hpp:199-201 (NaN -> 0, as fmaxf returns the number).
+__device__ __forceinline__ float clamp_unit(float x) { return fminf(fmaxf(x, 0.0f), 1.0f - 0x1p-20f); }
+
+// Clamp, scale, optional half-voxel offset, floor (grid.hpp:199-212). PC: x was
+// already clamped once per sample (clamp_x), so the per-level clamp is skipped
+// (clamping is idempotent: bit-identical corners and fractions).
+template <bool PC = false>
 __device__ __forceinline__ void voxel_of(float x, float n, bool half, uint32_t& corner, float& frac)
 {
-    float p = __fmul_rn(fminf(fmaxf(x, 0.0f), 1.0f - 0x1p-20f), n);
+    float p = __fmul_rn(PC ? x : clamp_unit(x), n);
     if (half)
         p = fminf(__fadd_rn(p, 0.5f), __fmul_rn(n, 1.0f - 0x1p-20f));
     const float f = floorf(p);
@@ -86,6 +92,14 @@ struct CornerSet {
 };
 
 template <int D>
+__device__ __forceinline__ void clamp_x(float* x)
+{
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        x[i] = clamp_unit(x[i]);
+}
+
+template <int D, bool PC = false>
 __device__ __forceinline__ CornerSet<D> corners_of(const GridDev& g, const LevelDev& lv, const float* x)
 {
     CornerSet<D> cs;
@@ -97,7 +111,7 @@ __device__ __forceinline__ CornerSet<D> corners_of(const GridDev& g, const Level
     for (int i = 0; i < D; ++i) {
         uint32_t c;
         float fr;
-        voxel_of(x[i], lv.res_f, g.smooth != 0, c, fr);
+        voxel_of<PC>(x[i], lv.res_f, g.smooth != 0, c, fr);
         cs.t[i] = g.smooth ? smoothstep1(fr) : fr;
         if (lv.dense) {
             cs.lo[i] = c * mul;

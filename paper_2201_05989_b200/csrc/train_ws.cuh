@@ -71,7 +71,6 @@ k_train_ws(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ l
     using Lay = WLayout<IN_STEPS, NH>;
     using SG = StageGeo<SRC_ENCODE, D, F, TT, IN_STEPS>;
     using SM = TrainWsSmem<D, TT, IN_STEPS, NH>;
-    constexpr int NFR = SM::NFR;
     extern __shared__ __align__(16) unsigned char sm[];
     __half* ws = reinterpret_cast<__half*>(sm);
     float* bs = reinterpret_cast<float*>(sm + Lay::HALVES * 2);
@@ -151,6 +150,8 @@ k_train_ws(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ l
                     invalid |= (finite_f(xg8[i]) ? 0u : 1u) | ((xg8[i] < lo || xg8[i] > hi) ? 2u : 0u);
                 }
             }
+            clamp_x<D>(xg);   // once per sample (the consumers' scatter reads the clamped copy)
+            clamp_x<D>(xg8);
             uint32_t afr[IN_STEPS][4];
 #pragma unroll
             for (int s0 = 0; s0 < IN_STEPS; s0 += SG::STS) {
@@ -161,9 +162,9 @@ k_train_ws(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ l
                         const int col = 16 * (s0 + sl) + 8 * h + 2 * t;
                         const int p = (sl * 2 + h) * 2;
                         if (s0 + sl < IN_STEPS && vg)
-                            gather_issue_lp<D, F, TT>(s.grid, lvs, xg, col, tab, slots, p * SG::NE);
+                            gather_issue_lp<D, F, TT, true>(s.grid, lvs, xg, col, tab, slots, p * SG::NE);
                         if (s0 + sl < IN_STEPS && vg8)
-                            gather_issue_lp<D, F, TT>(s.grid, lvs, xg8, col, tab, slots, (p + 1) * SG::NE);
+                            gather_issue_lp<D, F, TT, true>(s.grid, lvs, xg8, col, tab, slots, (p + 1) * SG::NE);
                     }
                 cp_async_wait_all();
                 __syncwarp();   // the partner lane's copies landed too
@@ -177,9 +178,9 @@ k_train_ws(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ l
                         const int p = (sl * 2 + h) * 2;
                         float2 e0 = make_float2(0.f, 0.f), e8 = make_float2(0.f, 0.f);
                         if (vg)
-                            e0 = gather_blend_lp<D, F, TT>(s.grid, lvs, xg, col, slots, p * SG::NE);
+                            e0 = gather_blend_lp<D, F, TT, true>(s.grid, lvs, xg, col, slots, p * SG::NE);
                         if (vg8)
-                            e8 = gather_blend_lp<D, F, TT>(s.grid, lvs, xg8, col, slots, (p + 1) * SG::NE);
+                            e8 = gather_blend_lp<D, F, TT, true>(s.grid, lvs, xg8, col, slots, (p + 1) * SG::NE);
                         afr[s0 + sl][2 * h] = pack_half2(e0.x, e0.y);
                         afr[s0 + sl][2 * h + 1] = pack_half2(e8.x, e8.y);
                     }
@@ -212,6 +213,7 @@ k_train_ws(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ l
         bool pending = false, first_mma = true;
         uint32_t mphase = 0;
         float dbo4[2][2] = { { 0.0f, 0.0f }, { 0.0f, 0.0f } };
+        double loss_acc = 0.0;
         int k = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
             const int b = k & 1;
@@ -293,7 +295,7 @@ k_train_ws(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ l
             }
             if (lane == 0) {
                 red[w4] = mx;
-                atomicAdd(a.scratch.loss_sum, double(term));
+                loss_acc += double(term);
             }
             csync();
             float tmax = 0.0f;
@@ -379,9 +381,9 @@ k_train_ws(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ l
                 const float2 p8 = make_float2(__shfl_xor_sync(0xffffffffu, d8.x, 1),
                                               __shfl_xor_sync(0xffffffffu, d8.y, 1));
                 if (vg)
-                    scatter_pair_lp<D>(s.grid, lvs, xg, col, d0, p0, a.table_grad);
+                    scatter_pair_lp<D, true>(s.grid, lvs, xg, col, d0, p0, a.table_grad);
                 if (vg8)
-                    scatter_pair_lp<D>(s.grid, lvs, xg8, col, d8, p8, a.table_grad);
+                    scatter_pair_lp<D, true>(s.grid, lvs, xg8, col, d8, p8, a.table_grad);
             }
 
             // ---- dW / db += dz^T [act | 1] on tcgen05 (TMEM) -------------------
@@ -414,6 +416,8 @@ k_train_ws(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ l
             first_mma = false;
             pending = true;
         }
+        if (lane == 0 && loss_acc != 0.0)
+            atomicAdd(a.scratch.loss_sum, loss_acc);
         // ---- flush the TMEM accumulators (x 1/count) -------------------------
         if (pending) {
             tc::mbar_wait(dw_bar, mphase);
