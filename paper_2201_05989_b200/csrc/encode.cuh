@@ -231,7 +231,7 @@ struct LanePair {
 // corners of both levels of the pair, blends them into two partial sums and
 // swaps the partner's partial with one shuffle. Every lane of the warp must
 // call it (invalid samples with x = 0 and the result discarded).
-template <int D, int F, typename TT, bool PC = false>
+template <int D, int F, typename TT, bool PC = false, int IP = IP_RUNTIME>
 __device__ __forceinline__ float2 encode_pair_lp(const GridDev& g, const LevelDev* lvs, const float* x, int col,
                                                  const TT* __restrict__ table)
 {
@@ -245,7 +245,7 @@ __device__ __forceinline__ float2 encode_pair_lp(const GridDev& g, const LevelDe
         if (lb + q >= g.L)
             continue;
         const LevelDev lv = lvs[lb + q];
-        const CornerSet<D> cs = corners_of<D, PC>(g, lv, x);
+        const CornerSet<D> cs = corners_of<D, PC, IP>(g, lv, x);
         const TT* base = table + size_t(lv.row_off) * F;
         float2 v[HC];
 #pragma unroll
@@ -266,7 +266,7 @@ __device__ __forceinline__ float2 encode_pair_lp(const GridDev& g, const LevelDe
 
 // Issue this lane's half of the corner loads of levels (l & ~1) and (l | 1):
 // slot k0 + q*HC + m holds corner 2m + par of level (l & ~1) + q.
-template <int D, int F, typename TT, bool PC = false, class Slots>
+template <int D, int F, typename TT, bool PC = false, int IP = IP_RUNTIME, class Slots>
 __device__ __forceinline__ void gather_issue_lp(const GridDev& g, const LevelDev* lvs, const float* x, int col,
                                                 const TT* __restrict__ table, const Slots& slots, int k0)
 {
@@ -278,7 +278,7 @@ __device__ __forceinline__ void gather_issue_lp(const GridDev& g, const LevelDev
         if (lb + q >= g.L)
             continue;
         const LevelDev lv = lvs[lb + q];
-        const CornerSet<D> cs = corners_of<D, PC>(g, lv, x);
+        const CornerSet<D> cs = corners_of<D, PC, IP>(g, lv, x);
 #pragma unroll
         for (int m = 0; m < HC; ++m)
             cp_async<SB>(slots.ptr(k0 + q * HC + m), table + (size_t(lv.row_off) + cs.row(2 * m + par)) * F);
@@ -289,7 +289,7 @@ __device__ __forceinline__ void gather_issue_lp(const GridDev& g, const LevelDev
 // the others from the partner lane's (same warp; call after the copies have
 // completed on both lanes and a __syncwarp). Same summation order as
 // gather_blend.
-template <int D, int F, typename TT, bool PC = false, class Slots>
+template <int D, int F, typename TT, bool PC = false, int IP = IP_RUNTIME, class Slots>
 __device__ __forceinline__ float2 gather_blend_lp(const GridDev& g, const LevelDev* lvs, const float* x, int col,
                                                   const Slots& slots, int k0)
 {
@@ -298,7 +298,7 @@ __device__ __forceinline__ float2 gather_blend_lp(const GridDev& g, const LevelD
     if (l >= g.L)
         return make_float2(0.0f, 0.0f);
     const LevelDev lv = lvs[l];
-    const CornerSet<D> cs = corners_of<D, PC>(g, lv, x);
+    const CornerSet<D> cs = corners_of<D, PC, IP>(g, lv, x);
     const int pdelta = par ? -SB : SB;
     float a = 0.0f, b = 0.0f;
 #pragma unroll
@@ -381,7 +381,7 @@ __device__ __forceinline__ void scatter_pair(const GridDev& g, const LevelDev* l
 // Lane-pair backward (F == 2): this lane's corner half of levels (l & ~1) and
 // (l | 1) of one sample; dy_own is this lane's level gradient, dy_partner the
 // partner lane's (exchanged by the caller with __shfl_xor_sync(.., 1)).
-template <int D, bool PC = false>
+template <int D, bool PC = false, int IP = IP_RUNTIME>
 __device__ __forceinline__ void scatter_pair_lp(const GridDev& g, const LevelDev* lvs, const float* x, int col,
                                                 float2 dy_own, float2 dy_partner, float* __restrict__ grads)
 {
@@ -392,7 +392,7 @@ __device__ __forceinline__ void scatter_pair_lp(const GridDev& g, const LevelDev
         if (lb + q >= g.L)
             continue;
         const LevelDev lv = lvs[lb + q];
-        const CornerSet<D> cs = corners_of<D, PC>(g, lv, x);
+        const CornerSet<D> cs = corners_of<D, PC, IP>(g, lv, x);
         const float2 dy = q == par ? dy_own : dy_partner;
         float* base = grads + size_t(lv.row_off) * F;
 #pragma unroll

@@ -245,7 +245,7 @@ __device__ __forceinline__ bool sane(float v) { return fabsf(v) <= 1e30f; }   //
 
 // Input fragments of the warp's 16 rows: encoded from X, or loaded from Y.
 // PC: xg / xg8 were clamped once (clamp_x).
-template <int SRC, int D, int F, typename TT, int IN_STEPS, bool PC = false>
+template <int SRC, int D, int F, typename TT, int IN_STEPS, bool PC = false, int IP = IP_RUNTIME>
 __device__ __forceinline__ void input_frags(uint32_t (&afr)[IN_STEPS][4], const FieldShape& s, const LevelDev* lvs,
                                             const float* xg, const float* xg8, bool vg, bool vg8, int64_t sg,
                                             const float* __restrict__ Y, const void* table, int lane)
@@ -261,8 +261,8 @@ __device__ __forceinline__ void input_frags(uint32_t (&afr)[IN_STEPS][4], const 
                 const TT* tab = static_cast<const TT*>(table);
 #ifndef NFG_NO_LANE_PAIRS
                 if constexpr (F == 2) {   // warp-uniform: invalid samples encode x = 0, discarded
-                    e0 = encode_pair_lp<D, F, TT, PC>(s.grid, lvs, xg, col, tab);
-                    e8 = encode_pair_lp<D, F, TT, PC>(s.grid, lvs, xg8, col, tab);
+                    e0 = encode_pair_lp<D, F, TT, PC, IP>(s.grid, lvs, xg, col, tab);
+                    e8 = encode_pair_lp<D, F, TT, PC, IP>(s.grid, lvs, xg8, col, tab);
                     if (!vg)
                         e0 = make_float2(0.f, 0.f);
                     if (!vg8)
@@ -316,7 +316,10 @@ struct TrainGroups {
     static constexpr int MIN_BLOCKS = TCW ? (NFG_TRAIN_MIN_BLOCKS_TC + NG - 1) / NG : NFG_TRAIN_MIN_BLOCKS;
 };
 
-template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IN_STEPS, int NH, bool TCW = false>
+// IP: interpolation mode (nfg_common.cuh), fixed per instantiation for the
+// encoding kernels so the linear path carries no smoothstep work.
+template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IN_STEPS, int NH, bool TCW = false,
+          int IP = IP_RUNTIME>
 __global__ void __launch_bounds__(TW * 32 * TrainGroups<TCW>::NG, TrainGroups<TCW>::MIN_BLOCKS)
 k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ levels)
 {
@@ -486,9 +489,9 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 const int p = (sl * 2 + h) * 2;
                 if constexpr (LPG) {
                     if (s0 + sl < IN_STEPS && v)
-                        gather_issue_lp<D, F, TT, true>(s.grid, lvs, x, col, tab, slots, p * SG::NE);
+                        gather_issue_lp<D, F, TT, true, IP>(s.grid, lvs, x, col, tab, slots, p * SG::NE);
                     if (s0 + sl < IN_STEPS && v8)
-                        gather_issue_lp<D, F, TT, true>(s.grid, lvs, x8, col, tab, slots, (p + 1) * SG::NE);
+                        gather_issue_lp<D, F, TT, true, IP>(s.grid, lvs, x8, col, tab, slots, (p + 1) * SG::NE);
                 } else {
                     if (s0 + sl < IN_STEPS && v)
                         gather_issue<D, F, TT>(s.grid, lvs, x, col, tab, slots, p * SG::NE);
@@ -510,9 +513,9 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 float2 e0 = make_float2(0.f, 0.f), e8 = make_float2(0.f, 0.f);
                 if constexpr (LPG) {
                     if (v)
-                        e0 = gather_blend_lp<D, F, TT, true>(s.grid, lvs, x, col, slots, p * SG::NE);
+                        e0 = gather_blend_lp<D, F, TT, true, IP>(s.grid, lvs, x, col, slots, p * SG::NE);
                     if (v8)
-                        e8 = gather_blend_lp<D, F, TT, true>(s.grid, lvs, x8, col, slots, (p + 1) * SG::NE);
+                        e8 = gather_blend_lp<D, F, TT, true, IP>(s.grid, lvs, x8, col, slots, (p + 1) * SG::NE);
                 } else {
                     if (v)
                         e0 = gather_blend<D, F, TT>(s.grid, lvs, x, col, slots, p * SG::NE);
@@ -779,9 +782,9 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
                 const float2 p8 = make_float2(__shfl_xor_sync(0xffffffffu, d8.x, 1),
                                               __shfl_xor_sync(0xffffffffu, d8.y, 1));
                 if (vg)
-                    scatter_pair_lp<D, true>(s.grid, lvs, xg, col, d0, p0, a.table_grad);
+                    scatter_pair_lp<D, true, IP>(s.grid, lvs, xg, col, d0, p0, a.table_grad);
                 if (vg8)
-                    scatter_pair_lp<D, true>(s.grid, lvs, xg8, col, d8, p8, a.table_grad);
+                    scatter_pair_lp<D, true, IP>(s.grid, lvs, xg8, col, d8, p8, a.table_grad);
                 continue;
             }
             if (col >= s.in_real)
@@ -1065,7 +1068,7 @@ k_train(const TrainArgs a, const FieldShape s, const LevelDev* __restrict__ leve
     }
 }
 
-template <int SRC, int D, int F, typename TT, int IN_STEPS, int NH>
+template <int SRC, int D, int F, typename TT, int IN_STEPS, int NH, int IP = IP_RUNTIME>
 __global__ void __launch_bounds__(IW * 32)
 k_infer(const InferArgs a, const FieldShape s, const LevelDev* __restrict__ levels)
 {
@@ -1099,7 +1102,7 @@ k_infer(const InferArgs a, const FieldShape s, const LevelDev* __restrict__ leve
             clamp_x<D>(xg8);
         }
         uint32_t afr[IN_STEPS][4];
-        input_frags<SRC, D, F, TT, IN_STEPS, SRC == SRC_ENCODE>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
+        input_frags<SRC, D, F, TT, IN_STEPS, SRC == SRC_ENCODE, IP>(afr, s, lvs, xg, xg8, vg, vg8, sg, a.Y, a.table, lane);
         float acc[HT][4];
         uint32_t ah[4][4];
         layer_fwd<IN_STEPS, HT>(afr, W0s, Lay::INS, acc, lane);

@@ -7,7 +7,7 @@
 #error "compile with -DNFG_D=2 or -DNFG_D=3"
 #endif
 #ifndef NFG_PART
-#error "compile with -DNFG_PART=0..3"
+#error "compile with -DNFG_PART=0..5"
 #endif
 #define NFG_CAT2(a, b) a##b
 #define NFG_CAT(a, b) NFG_CAT2(a, b)
@@ -23,18 +23,26 @@ namespace nfg {
 // Built combinations (anything else is NFG_EUNSUPPORTED):
 //   F = 2: fp16 or fp32 tables, in_steps 1..2 (L*F <= 32), hidden_layers 1..3
 //   F = 1, 4, 8: fp16 or fp32 tables, in_steps 2, hidden_layers 2
-#define NFG_FUSED_LIST(X)                                                     \
-    X(2, __half, 1, 1) X(2, __half, 1, 2) X(2, __half, 1, 3)                  \
+// the training lists are split in two (F = 2, in_steps 2 | the rest) so each
+// half compiles in its own translation unit
+#define NFG_FUSED_LIST_A(X)                                                   \
     X(2, __half, 2, 1) X(2, __half, 2, 2) X(2, __half, 2, 3)                  \
+    X(2, float, 2, 1) X(2, float, 2, 2) X(2, float, 2, 3)
+#define NFG_FUSED_LIST_B(X)                                                   \
+    X(2, __half, 1, 1) X(2, __half, 1, 2) X(2, __half, 1, 3)                  \
     X(2, float, 1, 1) X(2, float, 1, 2) X(2, float, 1, 3)                     \
-    X(2, float, 2, 1) X(2, float, 2, 2) X(2, float, 2, 3)                     \
     X(1, __half, 2, 2) X(4, __half, 2, 2) X(8, __half, 2, 2)                  \
     X(1, float, 2, 2) X(4, float, 2, 2) X(8, float, 2, 2)
+#define NFG_FUSED_LIST(X) NFG_FUSED_LIST_A(X) NFG_FUSED_LIST_B(X)
 
-// The instantiations are split over four translation units per dimension
-// (NFG_PART 0..3, Makefile) so a parallel build compiles them side by side.
+// The instantiations are split over six translation units per dimension
+// (NFG_PART 0..5, Makefile) so a parallel build compiles them side by side.
 cudaError_t NFG_CAT(launch_fused_train_f32_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
                                                      int num_sms, cudaStream_t st, int* grid_used);
+cudaError_t NFG_CAT(launch_fused_train_b_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
+                                                   int num_sms, cudaStream_t st, int* grid_used);
+cudaError_t NFG_CAT(launch_fused_train_f32_b_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
+                                                       int num_sms, cudaStream_t st, int* grid_used);
 
 #if NFG_PART == 0
 cudaError_t NFG_CAT(launch_fused_train_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
@@ -49,7 +57,21 @@ cudaError_t NFG_CAT(launch_fused_train_d, NFG_D)(const FieldShape& s, const Leve
     if (sizeof(TT_) == 2 && s.grid.F == F_ && s.in_steps == IS_ && s.hidden_layers == NH_)                 \
         return run_train<SRC_ENCODE, GRAD_LOSS, SINK_SCATTER, NFG_D, F_, __half, IS_, NH_>(s, lv, a, num_sms,  \
                                                                                             st, grid_used);
-    NFG_FUSED_LIST(X)
+    NFG_FUSED_LIST_A(X)
+#undef X
+    return NFG_CAT(launch_fused_train_b_d, NFG_D)(s, lv, a, num_sms, st, grid_used);
+}
+#endif
+
+#if NFG_PART == 4
+cudaError_t NFG_CAT(launch_fused_train_b_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
+                                                   int num_sms, cudaStream_t st, int* grid_used)
+{
+#define X(F_, TT_, IS_, NH_)                                                                               \
+    if (sizeof(TT_) == 2 && s.grid.F == F_ && s.in_steps == IS_ && s.hidden_layers == NH_)                 \
+        return run_train<SRC_ENCODE, GRAD_LOSS, SINK_SCATTER, NFG_D, F_, __half, IS_, NH_>(s, lv, a, num_sms,  \
+                                                                                            st, grid_used);
+    NFG_FUSED_LIST_B(X)
 #undef X
     return cudaErrorNotSupported;
 }
@@ -63,7 +85,21 @@ cudaError_t NFG_CAT(launch_fused_train_f32_d, NFG_D)(const FieldShape& s, const 
     if (sizeof(TT_) == 4 && s.grid.F == F_ && s.in_steps == IS_ && s.hidden_layers == NH_)                 \
         return run_train<SRC_ENCODE, GRAD_LOSS, SINK_SCATTER, NFG_D, F_, float, IS_, NH_>(s, lv, a, num_sms,   \
                                                                                            st, grid_used);
-    NFG_FUSED_LIST(X)
+    NFG_FUSED_LIST_A(X)
+#undef X
+    return NFG_CAT(launch_fused_train_f32_b_d, NFG_D)(s, lv, a, num_sms, st, grid_used);
+}
+#endif
+
+#if NFG_PART == 5
+cudaError_t NFG_CAT(launch_fused_train_f32_b_d, NFG_D)(const FieldShape& s, const LevelDev* lv, const TrainArgs& a,
+                                                       int num_sms, cudaStream_t st, int* grid_used)
+{
+#define X(F_, TT_, IS_, NH_)                                                                               \
+    if (sizeof(TT_) == 4 && s.grid.F == F_ && s.in_steps == IS_ && s.hidden_layers == NH_)                 \
+        return run_train<SRC_ENCODE, GRAD_LOSS, SINK_SCATTER, NFG_D, F_, float, IS_, NH_>(s, lv, a, num_sms,   \
+                                                                                           st, grid_used);
+    NFG_FUSED_LIST_B(X)
 #undef X
     return cudaErrorNotSupported;
 }

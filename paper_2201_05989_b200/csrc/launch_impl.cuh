@@ -19,7 +19,7 @@
 
 namespace nfg {
 
-template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IS, int NH, bool TCW>
+template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IS, int NH, bool TCW, int IP>
 cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& a, int num_sms, cudaStream_t st,
                       int* grid_used)
 {
@@ -27,7 +27,7 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
     constexpr bool ALIAS = StageAlias<SRC, D, F, TT, IS, NH>::ON;
     constexpr int NG = TrainGroups<TCW>::NG;
     using SM = std::conditional_t<TCW, TrainSmemTc<IS, NH, SG::BYTES, ALIAS, NG>, TrainSmem<IS, NH, SG::BYTES, ALIAS>>;
-    auto k = k_train<SRC, GRAD, SINK, D, F, TT, IS, NH, TCW>;
+    auto k = k_train<SRC, GRAD, SINK, D, F, TT, IS, NH, TCW, IP>;
     constexpr int threads = TW * 32 * NG;
     static int per_sm_dev[NFG_MAX_DEVICES];   // resolved once per instantiation and device
     int dev = 0;
@@ -81,8 +81,9 @@ cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& 
     static char desc[192];
     if (!desc[0])
         snprintf(desc, sizeof(desc), "k_train src=%d grad=%d sink=%d d=%d F=%d table=%s in_steps=%d hidden=%d "
-                 "stage_alias=%d ctas_per_sm=%d groups=%d dw=%s", SRC, GRAD, SINK, D, F, sizeof(TT) == 2 ? "f16" : "f32",
-                 IS, NH, int(ALIAS), per_sm, NG, TCW ? "tcgen05" : "mma.sync");
+                 "stage_alias=%d ctas_per_sm=%d groups=%d dw=%s interp=%s", SRC, GRAD, SINK, D, F,
+                 sizeof(TT) == 2 ? "f16" : "f32", IS, NH, int(ALIAS), per_sm, NG, TCW ? "tcgen05" : "mma.sync",
+                 IP == IP_LINEAR ? "linear" : IP == IP_SMOOTH ? "smooth" : "runtime");
     note_kernel_variant(0, desc);
     const int64_t ntiles = (a.B + TS - 1) / TS;
     if (ntiles <= 0)
@@ -150,15 +151,24 @@ template <int SRC, int GRAD, int SINK, int D, int F, typename TT, int IS, int NH
 cudaError_t run_train(const FieldShape& s, const LevelDev* lv, const TrainArgs& a, int num_sms, cudaStream_t st,
                       int* grid_used)
 {
-    return train_tcw(s) ? run_train<SRC, GRAD, SINK, D, F, TT, IS, NH, true>(s, lv, a, num_sms, st, grid_used)
-                        : run_train<SRC, GRAD, SINK, D, F, TT, IS, NH, false>(s, lv, a, num_sms, st, grid_used);
+    // The default (tcgen05) engine's encoding instantiations fix the interpolation
+    // at compile time; the mma.sync engine (A/B runs) and the dY-storing variant
+    // (level-pipelined exchange option) read it at run time.
+    if (!train_tcw(s))
+        return run_train<SRC, GRAD, SINK, D, F, TT, IS, NH, false, IP_RUNTIME>(s, lv, a, num_sms, st, grid_used);
+    if constexpr (SRC == SRC_ENCODE && SINK != SINK_STORE) {
+        if (s.grid.smooth)
+            return run_train<SRC, GRAD, SINK, D, F, TT, IS, NH, true, IP_SMOOTH>(s, lv, a, num_sms, st, grid_used);
+        return run_train<SRC, GRAD, SINK, D, F, TT, IS, NH, true, IP_LINEAR>(s, lv, a, num_sms, st, grid_used);
+    }
+    return run_train<SRC, GRAD, SINK, D, F, TT, IS, NH, true, IP_RUNTIME>(s, lv, a, num_sms, st, grid_used);
 }
 
-template <int SRC, int D, int F, typename TT, int IS, int NH>
-cudaError_t run_infer(const FieldShape& s, const LevelDev* lv, const InferArgs& a, int num_sms, cudaStream_t st)
+template <int SRC, int D, int F, typename TT, int IS, int NH, int IP>
+cudaError_t run_infer_ip(const FieldShape& s, const LevelDev* lv, const InferArgs& a, int num_sms, cudaStream_t st)
 {
     using SM = InferSmem<IS, NH>;
-    auto k = k_infer<SRC, D, F, TT, IS, NH>;
+    auto k = k_infer<SRC, D, F, TT, IS, NH, IP>;
     static int per_sm_dev[NFG_MAX_DEVICES];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= NFG_MAX_DEVICES)
@@ -176,8 +186,9 @@ cudaError_t run_infer(const FieldShape& s, const LevelDev* lv, const InferArgs& 
     }
     static char desc[160];
     if (!desc[0])
-        snprintf(desc, sizeof(desc), "k_infer src=%d d=%d F=%d table=%s in_steps=%d hidden=%d warps=%d", SRC, D, F,
-                 sizeof(TT) == 2 ? "f16" : "f32", IS, NH, IW);
+        snprintf(desc, sizeof(desc), "k_infer src=%d d=%d F=%d table=%s in_steps=%d hidden=%d warps=%d interp=%s", SRC,
+                 D, F, sizeof(TT) == 2 ? "f16" : "f32", IS, NH, IW,
+                 IP == IP_LINEAR ? "linear" : IP == IP_SMOOTH ? "smooth" : "runtime");
     note_kernel_variant(1, desc);
     const int64_t tiles = (a.B + 15) / 16;
     if (tiles <= 0)
@@ -186,6 +197,17 @@ cudaError_t run_infer(const FieldShape& s, const LevelDev* lv, const InferArgs& 
     const int grid = int(std::min<int64_t>(want, int64_t(num_sms) * per_sm));
     k<<<grid, IW * 32, SM::BYTES, st>>>(a, s, lv);
     return cudaGetLastError();
+}
+
+template <int SRC, int D, int F, typename TT, int IS, int NH>
+cudaError_t run_infer(const FieldShape& s, const LevelDev* lv, const InferArgs& a, int num_sms, cudaStream_t st)
+{
+    if constexpr (SRC == SRC_ENCODE) {   // interpolation fixed per instantiation (no smoothstep work when linear)
+        if (s.grid.smooth)
+            return run_infer_ip<SRC, D, F, TT, IS, NH, IP_SMOOTH>(s, lv, a, num_sms, st);
+        return run_infer_ip<SRC, D, F, TT, IS, NH, IP_LINEAR>(s, lv, a, num_sms, st);
+    }
+    return run_infer_ip<SRC, D, F, TT, IS, NH, IP_RUNTIME>(s, lv, a, num_sms, st);
 }
 
 template <int SRC, int D, int F, typename TT, int IS, int NH>

@@ -99,7 +99,12 @@ __device__ __forceinline__ void clamp_x(float* x)
         x[i] = clamp_unit(x[i]);
 }
 
-template <int D, bool PC = false>
+// IP: interpolation known at compile time (IP_LINEAR / IP_SMOOTH), or read from
+// the grid at run time (IP_RUNTIME; both variants are then computed and one is
+// selected per axis).
+enum { IP_RUNTIME = 0, IP_LINEAR = 1, IP_SMOOTH = 2 };
+
+template <int D, bool PC = false, int IP = IP_RUNTIME>
 __device__ __forceinline__ CornerSet<D> corners_of(const GridDev& g, const LevelDev& lv, const float* x)
 {
     CornerSet<D> cs;
@@ -111,8 +116,9 @@ __device__ __forceinline__ CornerSet<D> corners_of(const GridDev& g, const Level
     for (int i = 0; i < D; ++i) {
         uint32_t c;
         float fr;
-        voxel_of<PC>(x[i], lv.res_f, g.smooth != 0, c, fr);
-        cs.t[i] = g.smooth ? smoothstep1(fr) : fr;
+        const bool smooth = IP == IP_RUNTIME ? g.smooth != 0 : IP == IP_SMOOTH;
+        voxel_of<PC>(x[i], lv.res_f, smooth, c, fr);
+        cs.t[i] = smooth ? smoothstep1(fr) : fr;
         if (lv.dense) {
             cs.lo[i] = c * mul;
             cs.hi[i] = (c + 1u) * mul;

@@ -86,6 +86,7 @@ def _assert_headline_variant(m):
     assert v.startswith("k_train src=0 grad=0 sink=0") and f"d={d} " in v, v
     assert "F=2 table=f16 in_steps=2 hidden=2 stage_alias=1" in v, v
     assert "dw=tcgen05" in v, v   # the default engine bench.py measures (profiles/tc_train_r2.md)
+    assert "interp=linear" in v, v   # interpolation fixed at compile time (no smoothstep work)
 
 
 def _train_gpu(m, case, steps, seed=99):

@@ -379,6 +379,9 @@ def test_train_step_parity(case, kind, n_out, sig, fused):   # model.cpp:111-138
     # gradients (no Adam) vs the oracle's composed backward
     P = m.params
     lg = m.gradients(X, T, kind)
+    if fused:   # the encoding instantiation fixes the interpolation at compile time
+        v = m.last_kernel_variant(0)
+        assert ("interp=smooth" if g.interpolation else "interp=linear") in v, v
     G = m.grads
     mc = O.MlpCfg(g.levels * g.features, 2, 64, n_out, sig)
     Y, cache = O.encode_forward(og, P[:t], X)
