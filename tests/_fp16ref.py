@@ -70,3 +70,20 @@ def backward(W, b, shapes, Y, dOut, sigmoid, tile=64):
             dY = da
     flatW = np.concatenate([g.T.ravel() for g in gW])
     return out, flatW, np.concatenate(gb), dY
+
+
+def touched_set_unexplained(got, ref, emu, floor=1e-4):
+    """Table entries whose touched status (gradient != 0) differs between the
+    kernel and the fp32 oracle, and that the fp16 operands do not explain.
+
+    A touched entry's oracle gradient can be exactly zero (a sample with every
+    ReLU unit off in fp32 gives dY = 0) while the fp16-operand step gives a
+    value at the noise floor (seen: 1.6e-10 on the GPU, 2.1e-10 in the
+    emulation, 0 in the oracle). Such an entry is explained when the emulation
+    sits on the kernel's side, or when both gradients are below
+    floor * max|ref|. Returns (all differing indices, unexplained indices)."""
+    got, ref, emu = (np.asarray(v) for v in (got, ref, emu))
+    d = np.flatnonzero((got != 0) != (ref != 0))
+    same_side = (emu[d] != 0) == (got[d] != 0)
+    tiny = np.maximum(np.abs(got[d]), np.abs(ref[d])) <= floor * np.abs(ref).max()
+    return d, d[~(same_side | tiny)]

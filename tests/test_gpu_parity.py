@@ -391,7 +391,6 @@ def test_train_step_parity(case, kind, n_out, sig, fused):   # model.cpp:111-138
     gt = np.zeros(t, np.float32)
     O.encode_backward(og, cache, dY, gt)
     assert abs(lg - lo) <= 1e-4 * abs(lo)
-    assert np.array_equal(G[:t] != 0, gt != 0)           # same touched-entry set
     # Gradient bound, derived rather than asserted (as test_gpu_headline): the
     # kernel vs the exact fp16-operand emulation of the same step <= 1e-3
     # (its math), and by the triangle inequality the kernel vs the fp32 oracle
@@ -404,6 +403,9 @@ def test_train_step_parity(case, kind, n_out, sig, fused):   # model.cpp:111-138
     _, eW, eb, eY = R.backward(P[t:t + w], P[t + w:], shapes, Y, dpe, sig, tile=64)
     ge = np.zeros(t, np.float32)
     O.encode_backward(og, cache, eY.astype(np.float32), ge)
+    # same touched-entry set, up to fp16-operand noise-floor entries (_fp16ref)
+    _, bad = R.touched_set_unexplained(G[:t], gt, ge)
+    assert bad.size == 0, (bad[:10], G[:t][bad[:10]], gt[bad[:10]])
 
     def rel(a, r):
         return np.linalg.norm(np.asarray(a, np.float64) - r) / max(np.linalg.norm(np.asarray(r, np.float64)), 1e-30)

@@ -51,7 +51,11 @@ def test_narrow_mlp_train_parity(hw, hl, fused):
     gt = np.zeros(t, np.float32)
     O.encode_backward(og, cache, dY, gt)
     assert abs(lg - lo) <= 1e-4 * abs(lo)
-    assert np.array_equal(G[:t] != 0, gt != 0)
+    # same touched-entry set, up to entries below 1e-4 of the largest gradient
+    # (an fp32 dY of exactly zero against an fp16-operand noise-floor value)
+    import _fp16ref as R
+    _, bad = R.touched_set_unexplained(G[:t], gt, gt)
+    assert bad.size == 0, (bad[:10], G[:t][bad[:10]], gt[bad[:10]])
     for a, r in ((G[:t], gt), (G[t:t + w], gW), (G[t + w:], gb)):
         assert np.linalg.norm(a - r) <= 6e-2 * np.linalg.norm(r)
     m.write(1, np.zeros_like(G))
