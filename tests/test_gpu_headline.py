@@ -37,9 +37,13 @@ CFG2 = dict(dims=3, levels=16, table_size=1 << 19, features=2, n_min=16, n_max=2
 CFG1 = dict(dims=2, levels=16, table_size=1 << 14, features=2, n_min=16, n_max=1024)   # BASELINE config 1
 
 # (grid, n_out, sigmoid, loss kind, lr, full batch)
+# smoothstep interpolation (grid.hpp:112-133) through the same default
+# options: fp16 tables, the interp=smooth encoding instantiation
+CFGS = dict(dims=3, levels=16, table_size=1 << 16, features=2, n_min=16, n_max=512, interpolation=1)
 CASES = {
     "config2": (CFG2, 1, False, 1, 1e-4, 1 << 18),
     "config1": (CFG1, 3, True, 0, 1e-2, 1 << 16),
+    "smooth3d": (CFGS, 1, False, 1, 1e-3, 1 << 15),
 }
 MATH_TOL = 1e-3      # gpu vs the fp16-operand emulation (kernel math; measured <= 4.2e-4)
 CONTRACT = 1e-2      # SURVEY.md §8c table/MLP gradient contract (trained fields)
@@ -65,14 +69,15 @@ def _model(case):
 
 def _ocfg(grid):
     return O.GridCfg(levels=grid["levels"], table_size=grid["table_size"], features=grid["features"],
-                     n_min=grid["n_min"], n_max=grid["n_max"], dims=grid["dims"])
+                     n_min=grid["n_min"], n_max=grid["n_max"], dims=grid["dims"],
+                     smoothstep=bool(grid.get("interpolation", 0)))
 
 
 def _batch(case, B, seed):
     grid, n_out, sig, _, _, _ = CASES[case]
     rng = O.Pcg32(seed, 2)
     X = rng.floats(B * grid["dims"]).reshape(B, grid["dims"])
-    if case == "config2":
+    if grid["dims"] == 3:
         T = O.csg_sdf(X).reshape(B, 1)
     else:   # the procedural test image (helpers.hpp:99-125) at the sample positions
         w = 1024
@@ -85,10 +90,11 @@ def _batch(case, B, seed):
 def _assert_headline_variant(m):
     v = m.last_kernel_variant(0)
     d = m.hash_cfg.dims
+    smooth = int(m.hash_cfg.interpolation) == 1
     assert v.startswith("k_train src=0 grad=0 sink=0") and f"d={d} " in v, v
     assert "F=2 table=f16 in_steps=2 hidden=2 stage_alias=1" in v, v
     assert "dw=tcgen05" in v, v   # the default engine bench.py measures (profiles/tc_train_r2.md)
-    assert "interp=linear" in v, v   # interpolation fixed at compile time (no smoothstep work)
+    assert ("interp=smooth" if smooth else "interp=linear") in v, v   # interpolation fixed at compile time
 
 
 def _train_gpu(m, case, steps, seed=99):
@@ -130,9 +136,13 @@ def _rel(a, r):
     return float(np.linalg.norm(np.asarray(a, np.float64) - r) / max(np.linalg.norm(np.asarray(r, np.float64)), 1e-30))
 
 
-@pytest.mark.parametrize("state", ["init", "trained"])
+# smooth3d runs on trained fields only: at init its smoothstep-weighted
+# features sit near 1e-5, in fp16's subnormal range, where the kernel's and
+# the oracle's differently ordered blends round Y apart and the emulation is
+# no longer exact (measured up to 5e-3 from the kernel)
 @pytest.mark.parametrize("ragged", [False, True])
-@pytest.mark.parametrize("case", ["config2", "config1"])
+@pytest.mark.parametrize("case,state", [("config2", "init"), ("config2", "trained"), ("config1", "init"),
+                                        ("config1", "trained"), ("smooth3d", "trained")])
 def test_headline_gradients(case, ragged, state):   # model.cpp:111-138 via the benchmarked k_train
     m = _model(case)
     if state == "trained":
@@ -161,7 +171,7 @@ def test_headline_gradients(case, ragged, state):   # model.cpp:111-138 via the 
         report[name] = (d_emu, d_ref, emu_ref)
         assert d_emu <= MATH_TOL, (name, report)
         assert d_ref <= emu_ref + MATH_TOL, (name, report)
-        if state == "trained":
+        if state == "trained" and case != "smooth3d":   # §8c's contract is quoted on configs 1 and 2
             assert d_ref <= CONTRACT, (name, report)
         big = np.abs(r) > 1e-2 * np.abs(r).max()
         agree = float(np.mean(np.sign(a[big]) == np.sign(r[big])))
@@ -211,7 +221,7 @@ def _step_checks(case, m, before, after, ref_p, ref_g, cache, lg, lo):
 
 @pytest.mark.parametrize("path", ["plain", "streamed", "device"])
 @pytest.mark.parametrize("ragged", [False, True])
-@pytest.mark.parametrize("case", ["config2", "config1"])
+@pytest.mark.parametrize("case", ["config2", "config1", "smooth3d"])
 def test_headline_train_step(case, ragged, path):   # model.cpp:111-138 + adam.hpp:78-122, one step
     """One full step through each public entry: numpy arrays (staged copies),
     pinned host pointers (B >= 2^15: chunked H2D streamed under the running
