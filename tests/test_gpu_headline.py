@@ -52,13 +52,14 @@ MATH_TOL = 1e-3      # gpu vs the fp16-operand emulation (kernel math; measured 
 # the emulation when the smoothstep-weighted Y rounds differently in fp16.
 # A wrong interpolation instantiation is off by O(1).
 MATH_TOL_SMOOTH = 1e-2
-# Smoothstep fields also show rare rows where the kernel's gradient is exactly
-# zero while the oracle's and the emulation's are not (or the reverse): seen
-# on 1 of 40 trained batches, at most 8 entries of ~1e5 touched, each below
-# 2e-3 of the largest gradient. It is present in the build before the
-# round-2 instruction diet too (profiles/headline_margins_smooth3d_r2.log), so
-# it is not a regression. A sample whose dY the kernel's fp16 Y rounds to
-# exactly zero is the likely cause; it is not resolved.
+# Well-trained smoothstep fields also show rare rows whose gradient is exactly
+# zero in the kernel but not in the oracle (or the reverse): about 1 in 40
+# batches, at most 8 entries of ~1e5 touched, each below 2e-3 of the largest
+# gradient. Diagnosed (profiles/headline_margins_smooth3d_diag_r2.log): the
+# row is touched by a single sample whose kernel prediction equals its target
+# exactly, so the MAPE gradient sign(0) / den is 0, while the fp32 oracle's
+# prediction is one rounding away. The build before this round's kernel
+# changes shows the same (profiles/headline_margins_smooth3d_r2_old_new.log).
 SMOOTH_ODD_ENTRIES, SMOOTH_ODD_FLOOR = 16, 1e-2
 CONTRACT = 1e-2      # SURVEY.md §8c table/MLP gradient contract (trained fields)
 

@@ -27,7 +27,7 @@ def main():
             P = m.params
             lg = m.gradients(X, T, H.CASES[case][3])
             G = m.grads
-            lo, ref, emu, _ = H._oracle_grads(case, P, m.sizes, X, T)
+            lo, ref, emu, cache = H._oracle_grads(case, P, m.sizes, X, T)
             t, w, _ = m.sizes
             got = (G[:t], G[t:t + w], G[t + w:])
             row = [f"seed={seed} ragged={int(ragged)} loss_rel={abs(lg - lo) / abs(lo):.2e}"]
@@ -36,6 +36,19 @@ def main():
             if dset.size:
                 row.append(f"set_vals got={got[0][dset[:4]]} ref={ref[0][dset[:4]]} emu={emu[0][dset[:4]]} "
                            f"max={np.abs(ref[0]).max():.2e}")
+                # which samples touch the differing rows, and their kernel / oracle residuals
+                grid = H.CASES[case][0]
+                specs = H.O.level_resolutions(H._ocfg(grid))
+                F = grid["features"]
+                rows_d = set((dset // F).tolist())
+                smp = set()
+                for l in range(grid["levels"]):
+                    r = specs[l].row_offset + cache.rows[l].astype(np.int64)   # [B, 2^d]
+                    hit = np.isin(r, list(rows_d)).any(axis=1)
+                    smp.update(np.flatnonzero(hit).tolist())
+                smp = sorted(smp)[:6]
+                pg = m.evaluate(X[smp]).ravel()
+                row.append(f"samples={smp} gpu_pred-t={(pg - T[smp].ravel()).tolist()}")
             for name, a, r, e in zip(("tab", "W", "b"), got, ref, emu):
                 big = np.abs(r) > 1e-2 * np.abs(r).max()
                 dis = int(np.sum(np.sign(a[big]) != np.sign(r[big])))
